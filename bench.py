@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the multilevel NMF hot path.
+
+Workload (N=1): BASELINE.json config 4, the largest single-GPU configuration:
+256x256-pixel images (m = 65536), n = 262144 columns (64 GiB fp32 M), r = 64,
+HALS.  A "step" is one HALS sweep at the finest level (both M-streaming
+products, both Gram matrices, both sweeps) on seeded synthetic data of that
+shape generated on the device.  For N > 1 the columns of
+M are sharded over the ranks (strong scaling: the total problem is fixed) with
+one NCCL allreduce of [M W^T | W W^T] per step.
+
+Arms:
+  default           the B200 engine.  value: device-timed iterations/s (CUDA
+                    events on the engine's stream, max over ranks); e2e: the
+                    same metric through the C-ABI with pinned host buffers.
+  --impl reference  the reference's own CPU implementation (oracle/_ref: the
+                    unmodified mlnmf sources, OpenMP on all host cores) on
+                    bounded column slices of the same workload, extrapolated
+                    linearly in n (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "NMF iterations/sec + time-to-rel-error; HBM GB/s vs roofline, 1/2/4/8 GPU"
+UNIT = "iterations/s"
+CFG = 4
+M_ROWS, N_TOTAL, RANK, LEVELS = 65536, 262144, 64, 5
+WORKLOAD = "config4: 256x256 px (m=65536), n=262144, r=64, HALS, one finest-level sweep per step"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.proc = index, None
+        self.path = f"/tmp/mlb_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        except Exception:
+            return out
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                power.append(float(r[2]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if sm:
+            out.update(sm_mhz=float(np.median(sm)), sm_max_mhz=float(max(mx)), samples=len(sm),
+                       power_w_max=float(max(power)) if power else None)
+        out["reasons"] = sorted(reasons)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# torch.distributed plumbing (gloo: id broadcast, barriers, max of timings)
+# ---------------------------------------------------------------------------
+def dist_setup():
+    world, rank, local = env_int("WORLD_SIZE", 1), env_int("RANK", 0), env_int("LOCAL_RANK", 0)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bcast_obj(b, world):
+    if world == 1:
+        return b
+    import torch.distributed as dist
+    obj = [b]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU): oracle/_ref on column slices of config 4
+# ---------------------------------------------------------------------------
+def reference_steps(steps, warmup, slices=(128, 512)):
+    import oracle
+    ref, restated = oracle.Reference(), oracle.Restated()
+    data = {}
+    for ns in slices:
+        M = oracle.generate_config(CFG, n=N_TOTAL, col0=0, n_cols=ns, restated=restated)
+        V, W = ref.random_init(M_ROWS, ns, RANK, 0)
+        data[ns] = [M, V, W]
+    times = {ns: [] for ns in slices}
+    for it in range(warmup + steps):
+        for ns in slices:
+            M, V, W = data[ns]
+            t0 = time.perf_counter()
+            V, W, _ = ref.hals_step(M, V, W)
+            dt = time.perf_counter() - t0
+            data[ns][1], data[ns][2] = V, W
+            if it >= warmup:
+                times[ns].append(dt)
+    n1, n2 = slices
+    t1, t2 = float(np.median(times[n1])), float(np.median(times[n2]))
+    b = (t2 - t1) / (n2 - n1)
+    a = t1 - b * n1
+    return a + b * N_TOTAL, dict(t_slices_s={str(k): float(np.median(v)) for k, v in times.items()},
+                                 fit_a_s=a, fit_b_s_per_col=b)
+
+
+def ref_sample_text(steps, info):
+    return (f"reference hals_step (oracle/_ref = unmodified mlnmf sources, fp64, OpenMP) on column slices "
+            f"n=128 and n=512 of config 4 (m=65536, r=64), median of {steps} steps each, extrapolated linearly "
+            f"in n to n=262144: t = {info['fit_a_s']:.4f} s + {info['fit_b_s_per_col'] * 1e3:.4f} ms/column")
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    t0 = time.perf_counter()
+    t_full, info = reference_steps(args.steps, args.warmup)
+    value = 1.0 / t_full
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config-4 generator, column slices)",
+        "config": {"workload": WORKLOAD, "global_batch": N_TOTAL, "seq_len": M_ROWS,
+                   "parallelism": f"cpu{threads}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": ref_sample_text(args.steps, info)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0, **info,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline():
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    t_full, info = reference_steps(steps=3, warmup=1)
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": ref_sample_text(3, info)}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    world, rank, local = dist_setup()
+    import torch
+    import paper_1009_0881_b200 as P
+
+    torch.cuda.set_device(local)
+    nid = bcast_obj(P.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+    col0, n_loc = P.shard_columns(N_TOTAL, world, rank)
+    gemm = {"auto": P.GEMM_AUTO, "simt": P.GEMM_SIMT, "tc": P.GEMM_TCGEN05}[args.gemm]
+    s = P.Session(device=local, dtype=P.F32, gemm_path=gemm, world=world, rank=rank, nccl_id=nid)
+    t_gen = time.perf_counter()
+    s.generate(CFG, seed=0, n_total=N_TOTAL, col0=col0, n_local=n_loc)
+    norm = float(np.sqrt(s.norm2(0)))
+    t_gen = time.perf_counter() - t_gen
+    # random_init(seed 0) on this shard + the start sample; zero budget => no step
+    tr0 = s.run_configuration(1, "hals", "none", RANK, 0, 0.0, 0)
+    ext = torch.cuda.ExternalStream(s.stream, device=local)
+
+    s.steps("hals", args.warmup)
+    s.sync()
+    barrier(world)
+    launches0 = s.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(ext)
+        s.steps("hals", args.steps)
+        ev1.record(ext)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = s.launches - launches0
+    ms_max = allreduce_max(ms, world)
+    value = args.steps / (ms_max / 1e3)
+
+    # per-product durations: a separate profiled pass (CUDA events bracketing
+    # each M-streaming product on the engine stream)
+    s.set_profiling(True)
+    s.steps("hals", 3)
+    kt = s.kernel_times()
+    s.set_profiling(False)
+    mwt_ms = kt["mwt_ms"] / max(kt["mwt_n"], 1)
+    vtm_ms = kt["vtm_ms"] / max(kt["vtm_n"], 1)
+    bytes_per_pass = M_ROWS * n_loc * 4
+    dom_ms, dom = (vtm_ms, "C = V^T M") if vtm_ms >= mwt_ms else (mwt_ms, "A = M W^T")
+    achieved = bytes_per_pass / (dom_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    err_end = s.error()
+    tc = s.tc_active
+
+    e2e = None
+    if args.e2e and world == 1:
+        host = torch.empty((M_ROWS, n_loc), dtype=torch.float32, pin_memory=True)
+        s.export_data(host.data_ptr())
+        s.close()
+        e2e = run_e2e(P, host, local, gemm, args.e2e_iters, norm)
+        del host
+    else:
+        s.close()
+
+    ttt = time_to_target(P, local, gemm) if (args.ttt and world == 1) else None
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if tc else "f32 storage / f64 accumulate",
+        "data": "synthetic (BASELINE config-4 generator on the device, seed 0)",
+        "config": {"workload": WORKLOAD, "global_batch": N_TOTAL, "seq_len": M_ROWS,
+                   "parallelism": f"column-shard x{world}", "l2": "inputs larger than L2 (M = 64 GiB fp32)",
+                   "gemm_path": "tcgen05 3xTF32" if tc else "SIMT fp64-accumulate"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": dom, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_pass,
+                     "avg_ms": {"A = M W^T": mwt_ms, "C = V^T M": vtm_ms},
+                     "step_frac_in_products": (mwt_ms + vtm_ms) / (ms_max / args.steps)},
+        "rel_error": {"start": float(tr0.error[0]) / norm, "after_bench": err_end / norm},
+        "gen_s": t_gen,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if ttt:
+        line["time_to_target"] = ttt
+    if args.cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(P, host, local, gemm, iters, norm):
+    """One reference-facing solve through the C-ABI from pinned host memory:
+    set_data (H2D of M) + run_configuration(levels=1, HALS, none, r=64,
+    work:iters) + get_factors (D2H of V, W), wall-clock timed."""
+    import torch
+    m, nl = host.shape
+    Vh = torch.empty((m, RANK), dtype=torch.float32, pin_memory=True)
+    Wh = torch.empty((RANK, nl), dtype=torch.float32, pin_memory=True)
+    torch.cuda.synchronize()
+    se = P.Session(device=local, dtype=P.F32, gemm_path=gemm)
+    t0 = time.perf_counter()
+    se.set_data_ptr(host.data_ptr(), P.F32, m, nl, P.ImageGrid(256, 256))
+    tr = se.run_configuration(1, "hals", "none", RANK, 0, float(iters), 0)
+    se.get_factors_ptr(Vh.data_ptr(), Wh.data_ptr(), P.F32)
+    wall = time.perf_counter() - t0
+    se.close()
+    steps = int(tr.phase_steps.sum())
+    return {"value": steps / wall, "unit": UNIT, "h2d_bytes_per_step": m * nl * 4 / steps,
+            "d2h_bytes_per_step": (m * RANK + RANK * nl) * 4 / steps,
+            "call": f"mlnmf_session_set_data + mlnmf_session_run_configuration(levels=1, hals, none, r=64, "
+                    f"work:{iters}, trace_every=0) + mlnmf_session_get_factors; pinned host fp32",
+            "iters_per_call": steps, "wall_s": wall, "final_rel_error": float(tr.error[-1]) / norm}
+
+
+def time_to_target(P, local, gemm):
+    """Time-to-target relative error: target = the
+    single-level (cycle none) final relative error at work:20; report the
+    elapsed time of the first finest-level sample at or below it for none and
+    FMG (5 levels), traced every 2 steps."""
+    out = {}
+    with P.Session(device=local, dtype=P.F32, gemm_path=gemm) as s:
+        s.generate(CFG, seed=0)
+        norm = float(np.sqrt(s.norm2(0)))
+        runs = {"none": s.run_configuration(1, "hals", "none", RANK, 0, 20.0, 2)}
+        target = float(runs["none"].error[-1]) / norm
+        runs["fmg"] = s.run_configuration(LEVELS, "hals", "fmg", RANK, 0, 20.0, 2)
+        out["target_rel_error"] = target
+        for cyc, tr in runs.items():
+            rel = tr.error / norm
+            hit = np.nonzero((tr.level == 1) & (rel <= target * (1 + 1e-12)))[0]
+            out[cyc] = {"time_s": float(tr.elapsed_s[hit[0]]) if len(hit) else None,
+                        "final_rel_error": float(rel[-1]), "total_s": float(tr.elapsed_s[-1]),
+                        "phase_steps": tr.phase_steps.tolist()}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-ttt", dest="ttt", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

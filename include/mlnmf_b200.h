@@ -1,0 +1,200 @@
+/*
+ * mlnmf_b200.h -- C-ABI of the B200-native multilevel NMF solver.
+ *
+ * Drop-in boundary for the reference library `mlnmf` (/root/reference/proj).
+ * The reference has no FFI; its boundary is the public C++ headers
+ * proj/include/mlnmf/{matrix,solvers,multilevel,transfer,cost_model}.hpp.
+ * Every entry point below cites the reference declaration it replaces.
+ * Plain pointers and sizes only: matrices are caller-owned, row-major
+ * (element (i,j) at i*cols + j, proj/include/mlnmf/matrix.hpp:47-52);
+ * M is m x n (one column per vectorized image, pixel (i,j) of an h x w image at
+ * row j*h + i, transfer.hpp:15-20), V is m x r, W is r x n.
+ *
+ * Errors: every int-returning call returns a status; the message of the last
+ * failure on the calling thread is mlnmf_last_error().  The codes mirror the
+ * reference's exception classes and its CLI exit codes
+ * (proj/tools/mlnmf_main.cpp:214-233):
+ *   MLNMF_ERR_INVALID  std::invalid_argument   (exit 2)
+ *   MLNMF_ERR_DATA     mlnmf::DataError        (exit 3)
+ *   MLNMF_ERR_NNLS_CAP mlnmf::NnlsCapExceeded  (exit 4)
+ *   MLNMF_ERR_RUNTIME  std::runtime_error, CUDA and NCCL failures (exit 1)
+ *
+ * Threading: a session is single-owner and not thread-safe (the reference is
+ * one logical thread per run).  The one-shot reference-shaped
+ * calls use a per-thread default session.
+ */
+#ifndef MLNMF_B200_H_
+#define MLNMF_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLNMF_B200_VERSION 1
+
+enum {
+  MLNMF_OK = 0,
+  MLNMF_ERR_RUNTIME = 1,
+  MLNMF_ERR_INVALID = 2,
+  MLNMF_ERR_DATA = 3,
+  MLNMF_ERR_NNLS_CAP = 4
+};
+
+/* SolverKind (proj/include/mlnmf/cost_model.hpp:9) */
+enum { MLNMF_ANLS = 0, MLNMF_MU = 1, MLNMF_HALS = 2 };
+/* CycleKind (proj/include/mlnmf/multilevel.hpp:11) */
+enum { MLNMF_SINGLE_LEVEL = 0, MLNMF_NESTED_ITERATION = 1, MLNMF_V_CYCLE = 2, MLNMF_FULL_MULTIGRID = 3 };
+/* Budget::Mode (proj/include/mlnmf/solvers.hpp:37-41) */
+enum { MLNMF_WORK_UNITS = 0, MLNMF_WALL_CLOCK_SECONDS = 1 };
+/* storage / host buffer element types */
+enum { MLNMF_F32 = 0, MLNMF_F64 = 1 };
+/* M-streaming product implementation */
+enum { MLNMF_GEMM_AUTO = 0, MLNMF_GEMM_SIMT = 1, MLNMF_GEMM_TCGEN05 = 2 };
+/* error-sample implementation */
+enum { MLNMF_ERROR_AUTO = 0, MLNMF_ERROR_GRAM = 1, MLNMF_ERROR_DIRECT = 2 };
+
+typedef struct mlnmf_session mlnmf_session;
+typedef struct mlnmf_trace mlnmf_trace;
+
+typedef struct {
+  int device;      /* CUDA device ordinal */
+  int dtype;       /* MLNMF_F32 / MLNMF_F64 storage of M, V, W on the device */
+  int exact;       /* 1: the reference's operation order (fp64 runs bit-identical) */
+  int gemm_path;   /* MLNMF_GEMM_* */
+  int error_mode;  /* MLNMF_ERROR_* */
+  int world;       /* ranks sharing the problem (columns of M sharded) */
+  int rank;        /* this rank */
+  const void* nccl_id; /* 128-byte ncclUniqueId when world > 1 */
+} mlnmf_options;
+
+/* Synthetic BASELINE.json data generator. */
+typedef struct {
+  size_t h, w, r, blobs;
+  double sigma_min, sigma_max;
+  int noise_kind; /* 0: noise_scale * U[0,1); 1: N(0, noise_scale^2) */
+  double noise_scale;
+  uint64_t seed;
+  int scale_to_unit; /* divide M by its global maximum */
+} mlnmf_gen_params;
+
+const char* mlnmf_last_error(void);
+int mlnmf_version(void);
+void mlnmf_default_options(mlnmf_options* o);
+/* Options of the per-thread default session behind the one-shot calls. */
+int mlnmf_set_default_options(const mlnmf_options* o);
+int mlnmf_nccl_unique_id(void* out128);
+
+/* ---------------------------------------------------------------------------
+ * One-shot, reference-shaped calls (host fp64 buffers; H2D/D2H per call).
+ * ------------------------------------------------------------------------- */
+
+/* run_configuration (proj/include/mlnmf/multilevel.hpp:43-47).  V_out (m x r)
+ * and W_out (r x n) receive the factors; *trace_out a trace to free with
+ * mlnmf_trace_free (may be NULL). */
+int mlnmf_run_configuration(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                            size_t level_count, int kind, int cycle, size_t rank, uint64_t seed,
+                            int budget_mode, double budget_amount, size_t trace_every, double* V_out,
+                            double* W_out, mlnmf_trace** trace_out);
+
+/* nested_iteration / v_cycle / full_multigrid (multilevel.hpp:22-38) on the
+ * hierarchy GridHierarchy::build(M, grid, hierarchy_levels) with `levels` in
+ * play, from caller factors V0 (m x r), W0 (r x n).  cycle selects which. */
+int mlnmf_run_cycle(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                    size_t hierarchy_levels, size_t levels, const double* V0, const double* W0, size_t r,
+                    int kind, int cycle, int budget_mode, double budget_amount, size_t trace_every,
+                    double* V_out, double* W_out, mlnmf_trace** trace_out);
+
+/* run_solver (proj/include/mlnmf/solvers.hpp:101-103). */
+int mlnmf_run_solver(const double* M, size_t m, size_t n, const double* V0, const double* W0, size_t r,
+                     int kind, int budget_mode, double budget_amount, size_t trace_every, double* V_out,
+                     double* W_out, mlnmf_trace** trace_out);
+
+/* mu_step / hals_step / anls_step (solvers.hpp:45-68); V, W updated in place.
+ * degenerate: incremented per degenerate diagonal (may be NULL).
+ * iter_counts: m + n exchange counts (may be NULL). */
+int mlnmf_mu_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r);
+int mlnmf_hals_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r, int* degenerate);
+int mlnmf_anls_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r, int* iter_counts);
+
+/* nnls_active_set (solvers.hpp:61-63): G r x r, h and x0 length r. */
+int mlnmf_nnls_active_set(const double* G, const double* h, const double* x0, size_t r, double* x,
+                          int* iterations);
+
+/* frobenius_error (matrix.hpp:99-101) */
+int mlnmf_frobenius_error(const double* M, const double* V, const double* W, size_t m, size_t n, size_t r,
+                          double* out);
+/* random_init (matrix.hpp:106-107) */
+int mlnmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* V_out, double* W_out);
+/* restrict_columns / prolong_columns (transfer.hpp:68-69) with the operators
+ * build_restriction / build_prolongation(fine grid h x w) (transfer.hpp:60-66):
+ * X is (h*w) x ncols (restrict) or (ceil(h/2)*ceil(w/2)) x ncols (prolong). */
+int mlnmf_restrict_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
+int mlnmf_prolong_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
+/* Dry run of the host scheduler (no device work): the phase allocations,
+ * steps per phase and the (work_units, level) stamps of every trace sample a
+ * work-unit-budget run_configuration on an h x w grid with n columns would
+ * produce (multilevel.cpp:116-132 + solvers.cpp:300-341).  Sample errors and
+ * times are zero. */
+int mlnmf_plan_configuration(size_t grid_h, size_t grid_w, size_t n, size_t level_count, int kind, int cycle,
+                             size_t rank, double budget_amount, size_t trace_every, mlnmf_trace** trace_out);
+/* iteration_cost (cost_model.hpp:36) with CostParams::with_default_sr */
+double mlnmf_iteration_cost(size_t m, size_t n, size_t r, int kind);
+
+/* ---------------------------------------------------------------------------
+ * Sessions: device-resident data, fp32 storage, column sharding over ranks.
+ * ------------------------------------------------------------------------- */
+int mlnmf_session_create(const mlnmf_options* o, mlnmf_session** out);
+void mlnmf_session_destroy(mlnmf_session* s);
+/* M_local: m x n_local row-major host buffer (host_dtype MLNMF_F32/F64),
+ * columns [col0, col0 + n_local) of an n_total-column problem.  Validated like
+ * Matrix::from_data (matrix.cpp:10-22). */
+int mlnmf_session_set_data(mlnmf_session* s, const void* M_local, int host_dtype, size_t m, size_t n_local,
+                           size_t n_total, size_t col0, size_t grid_h, size_t grid_w);
+int mlnmf_session_generate(mlnmf_session* s, const mlnmf_gen_params* g, size_t n_total, size_t col0,
+                           size_t n_local);
+int mlnmf_session_run_configuration(mlnmf_session* s, size_t level_count, int kind, int cycle, size_t rank,
+                                    uint64_t seed, int budget_mode, double budget_amount, size_t trace_every,
+                                    mlnmf_trace** trace_out);
+int mlnmf_session_run_cycle(mlnmf_session* s, size_t hierarchy_levels, size_t levels, const void* V0,
+                            const void* W0_local, int host_dtype, size_t r, int kind, int cycle,
+                            int budget_mode, double budget_amount, size_t trace_every, mlnmf_trace** trace_out);
+/* level-0 factors: V (m x r), this rank's W columns (r x n_local) */
+int mlnmf_session_get_factors(mlnmf_session* s, void* V, void* W_local, int host_dtype);
+int mlnmf_session_set_factors(mlnmf_session* s, const void* V, const void* W_local, int host_dtype, size_t r);
+/* Enqueue n_steps solver sweeps at level 0 with no error samples (bench). */
+int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps);
+int mlnmf_session_sync(mlnmf_session* s);
+int mlnmf_session_error(mlnmf_session* s, double* out); /* ||M - VW||_F at level 0, all ranks */
+int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out); /* ||M_level||_F^2, all ranks */
+/* copy this rank's level-0 M (m x n_local) to a host buffer */
+int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
+int mlnmf_session_set_profiling(mlnmf_session* s, int on);
+int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, double* vtm_ms, long* vtm_n);
+long mlnmf_session_launches(mlnmf_session* s);
+void* mlnmf_session_stream(mlnmf_session* s);
+/* 1 if the tcgen05 path serves the M-streaming products */
+int mlnmf_session_tc_active(mlnmf_session* s);
+int mlnmf_session_gram_error(mlnmf_session* s);
+
+/* ---------------------------------------------------------------------------
+ * Traces: RunTrace (proj/include/mlnmf/solvers.hpp:14-35).
+ * ------------------------------------------------------------------------- */
+size_t mlnmf_trace_num_samples(const mlnmf_trace* t);
+void mlnmf_trace_samples(const mlnmf_trace* t, double* elapsed_s, double* work_units, int* level,
+                         double* error);
+size_t mlnmf_trace_num_allocations(const mlnmf_trace* t);
+void mlnmf_trace_allocations(const mlnmf_trace* t, int* level, double* amount);
+size_t mlnmf_trace_num_nnls_counts(const mlnmf_trace* t);
+void mlnmf_trace_nnls_counts(const mlnmf_trace* t, int* counts);
+int mlnmf_trace_degenerate(const mlnmf_trace* t);
+size_t mlnmf_trace_num_phases(const mlnmf_trace* t);
+void mlnmf_trace_phases(const mlnmf_trace* t, int* level, long* steps);
+void mlnmf_trace_free(mlnmf_trace* t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLNMF_B200_H_ */

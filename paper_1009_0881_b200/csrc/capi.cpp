@@ -1,0 +1,415 @@
+// capi.cpp -- the extern "C" boundary (include/mlnmf_b200.h) over the device
+// Engine and the host scheduler.  C++ exceptions become status codes with a
+// per-thread message, mirroring the reference's exception classes.
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/mlnmf_b200.h"
+#include "engine.hpp"
+#include "nccl_shim.hpp"
+#include "scheduler.hpp"
+
+using namespace mlb;
+
+struct mlnmf_session {
+  std::unique_ptr<Engine> e;
+};
+struct mlnmf_trace {
+  RunTrace t;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local mlnmf_options g_default = {0, MLNMF_F64, 0, MLNMF_GEMM_AUTO, MLNMF_ERROR_AUTO, 1, 0, nullptr};
+thread_local std::map<std::tuple<int, int, int, int, int>, std::unique_ptr<Engine>> g_sessions;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MLNMF_OK;
+  } catch (const NnlsCapExceeded& ex) {
+    g_err = ex.what();
+    return MLNMF_ERR_NNLS_CAP;
+  } catch (const DataError& ex) {
+    g_err = ex.what();
+    return MLNMF_ERR_DATA;
+  } catch (const std::invalid_argument& ex) {
+    g_err = ex.what();
+    return MLNMF_ERR_INVALID;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return MLNMF_ERR_RUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return MLNMF_ERR_RUNTIME;
+  }
+}
+
+Options to_opts(const mlnmf_options* o) {
+  Options x;
+  if (!o) return x;
+  x.device = o->device;
+  x.dtype = o->dtype;
+  x.exact = o->exact;
+  x.gemm = o->gemm_path;
+  x.error_mode = o->error_mode;
+  x.world = o->world < 1 ? 1 : o->world;
+  x.rank = o->rank;
+  if (o->nccl_id) {
+    x.has_nccl_id = true;
+    std::memcpy(x.nccl_id, o->nccl_id, 128);
+  }
+  return x;
+}
+
+// Per-thread default session of the one-shot calls (single rank).
+Engine& default_engine() {
+  const mlnmf_options& o = g_default;
+  auto key = std::make_tuple(o.device, o.dtype, o.exact, o.gemm_path, o.error_mode);
+  auto it = g_sessions.find(key);
+  if (it != g_sessions.end()) return *it->second;
+  mlnmf_options single = o;
+  single.world = 1;
+  single.rank = 0;
+  single.nccl_id = nullptr;
+  auto e = std::make_unique<Engine>(to_opts(&single));
+  Engine& ref = *e;
+  g_sessions.emplace(key, std::move(e));
+  return ref;
+}
+
+Kind to_kind(int k) {
+  if (k < 0 || k > 2) throw std::invalid_argument("unknown solver kind");
+  return static_cast<Kind>(k);
+}
+Cycle to_cycle(int c) {
+  if (c < 0 || c > 3) throw std::invalid_argument("unknown cycle kind");
+  return static_cast<Cycle>(c);
+}
+
+void check_dims(size_t m, size_t n, size_t r) {
+  if (m == 0 || n == 0 || r == 0) throw std::invalid_argument("Matrix: dimensions must be positive");
+}
+
+void emit_trace(RunTrace&& t, mlnmf_trace** out) {
+  if (!out) return;
+  auto* tr = new mlnmf_trace;
+  tr->t = std::move(t);
+  *out = tr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mlnmf_last_error(void) { return g_err.c_str(); }
+int mlnmf_version(void) { return MLNMF_B200_VERSION; }
+
+void mlnmf_default_options(mlnmf_options* o) {
+  *o = mlnmf_options{0, MLNMF_F64, 0, MLNMF_GEMM_AUTO, MLNMF_ERROR_AUTO, 1, 0, nullptr};
+}
+
+int mlnmf_set_default_options(const mlnmf_options* o) {
+  return guard([&] {
+    if (!o) throw std::invalid_argument("null options");
+    if (o->dtype != MLNMF_F32 && o->dtype != MLNMF_F64) throw std::invalid_argument("dtype must be F32 or F64");
+    g_default = *o;
+  });
+}
+
+int mlnmf_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    nccl_check(NcclApi::get().GetUniqueId(&id), "GetUniqueId");
+    std::memcpy(out128, &id, 128);
+  });
+}
+
+double mlnmf_iteration_cost(size_t m, size_t n, size_t r, int kind) {
+  return iteration_cost(m, n, r, kind == MLNMF_ANLS ? kAnls : kMu);
+}
+
+int mlnmf_plan_configuration(size_t grid_h, size_t grid_w, size_t n, size_t level_count, int kind, int cycle,
+                             size_t rank, double amount, size_t trace_every, mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    if (level_count < 1) throw std::invalid_argument("run_configuration: need at least one level");
+    std::vector<size_t> rows{grid_h * grid_w};
+    size_t gh = grid_h, gw = grid_w;
+    for (size_t l = 0; l + 1 < level_count; ++l) {
+      if (gh < 2 || gw < 2) throw std::invalid_argument("coarsen_grid: grid below 2x2 cannot be coarsened");
+      gh = (gh + 1) / 2;
+      gw = (gw + 1) / 2;
+      rows.push_back(gh * gw);
+    }
+    const Cycle c = to_cycle(cycle);
+    const size_t hl = c == kNone ? 1 : level_count;
+    rows.resize(hl);
+    if (rank < 1 || rank > std::min(grid_h * grid_w, n))
+      throw std::invalid_argument("random_init: rank must satisfy 1 <= r <= min(m,n)");
+    RunTrace t;
+    plan_cycle(rows, n, hl, rank, to_kind(kind), c, amount, trace_every, t);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+// ---------------------------------------------------------------------------
+int mlnmf_run_configuration(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w, size_t level_count,
+                            int kind, int cycle, size_t rank, uint64_t seed, int budget_mode, double amount,
+                            size_t trace_every, double* V_out, double* W_out, mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    Engine& e = default_engine();
+    if (level_count < 1) throw std::invalid_argument("run_configuration: need at least one level");
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, grid_h, grid_w, false);
+    RunTrace t;
+    run_configuration(e, level_count, to_kind(kind), to_cycle(cycle), rank, seed, budget_mode, amount, trace_every,
+                      t);
+    e.get_factors(0, V_out, W_out, MLNMF_F64);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+int mlnmf_run_cycle(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w, size_t hierarchy_levels,
+                    size_t levels, const double* V0, const double* W0, size_t r, int kind, int cycle,
+                    int budget_mode, double amount, size_t trace_every, double* V_out, double* W_out,
+                    mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, r);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, grid_h, grid_w, false);
+    e.ensure_levels(hierarchy_levels);
+    e.set_factors(0, V0, W0, MLNMF_F64, r);
+    RunTrace t;
+    run_cycle(e, levels, r, to_kind(kind), to_cycle(cycle), budget_mode, amount, trace_every, t);
+    e.get_factors(0, V_out, W_out, MLNMF_F64);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+// run_solver (solvers.cpp:343-355): one level, unit = one iteration on M.
+int mlnmf_run_solver(const double* M, size_t m, size_t n, const double* V0, const double* W0, size_t r, int kind,
+                     int budget_mode, double amount, size_t trace_every, double* V_out, double* W_out,
+                     mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, r);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, m, 1, false);
+    e.set_factors(0, V0, W0, MLNMF_F64, r);
+    RunTrace t;
+    run_cycle(e, 1, r, to_kind(kind), kNone, budget_mode, amount, trace_every, t);
+    e.get_factors(0, V_out, W_out, MLNMF_F64);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+static int one_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r, Kind k, int* deg,
+                    int* counts) {
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, r);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, m, 1, false);
+    e.set_factors(0, V, W, MLNMF_F64, r);
+    e.mark_run_start();
+    e.step(0, k);
+    std::vector<int> cn;
+    int d = 0;
+    e.flush(nullptr, &cn, &d);
+    e.get_factors(0, V, W, MLNMF_F64);
+    if (deg) *deg += d;
+    if (counts && !cn.empty()) std::memcpy(counts, cn.data(), cn.size() * sizeof(int));
+  });
+}
+
+int mlnmf_mu_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r) {
+  return one_step(M, m, n, V, W, r, kMu, nullptr, nullptr);
+}
+int mlnmf_hals_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r, int* degenerate) {
+  return one_step(M, m, n, V, W, r, kHals, degenerate, nullptr);
+}
+int mlnmf_anls_step(const double* M, size_t m, size_t n, double* V, double* W, size_t r, int* iter_counts) {
+  return one_step(M, m, n, V, W, r, kAnls, nullptr, iter_counts);
+}
+
+int mlnmf_nnls_active_set(const double* G, const double* h, const double* x0, size_t r, double* x, int* iterations) {
+  return guard([&] {
+    int it = 0;
+    default_engine().nnls_single(G, h, x0, r, x, &it);
+    if (iterations) *iterations = it;
+  });
+}
+
+int mlnmf_frobenius_error(const double* M, const double* V, const double* W, size_t m, size_t n, size_t r,
+                          double* out) {
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, r);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, m, 1, false);
+    e.set_factors(0, V, W, MLNMF_F64, r);
+    *out = e.frobenius_error(0);
+  });
+}
+
+int mlnmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* V_out, double* W_out) {
+  return guard([&] { default_engine().random_init_host(m, n, r, seed, V_out, W_out); });
+}
+
+int mlnmf_restrict_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y) {
+  return guard([&] { default_engine().apply_transfer(grid_h, grid_w, 0, X, ncols, Y); });
+}
+int mlnmf_prolong_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y) {
+  return guard([&] { default_engine().apply_transfer(grid_h, grid_w, 1, X, ncols, Y); });
+}
+
+// ---------------------------------------------------------------------------
+int mlnmf_session_create(const mlnmf_options* o, mlnmf_session** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto* s = new mlnmf_session;
+    try {
+      s->e = std::make_unique<Engine>(to_opts(o));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void mlnmf_session_destroy(mlnmf_session* s) { delete s; }
+
+int mlnmf_session_set_data(mlnmf_session* s, const void* M, int host_dtype, size_t m, size_t n_local, size_t n_total,
+                           size_t col0, size_t grid_h, size_t grid_w) {
+  return guard([&] { s->e->set_data(M, host_dtype, false, m, n_local, n_total, col0, grid_h, grid_w, true); });
+}
+
+int mlnmf_session_generate(mlnmf_session* s, const mlnmf_gen_params* g, size_t n_total, size_t col0,
+                           size_t n_local) {
+  return guard([&] {
+    GenParams p;
+    p.h = g->h, p.w = g->w, p.r = g->r, p.blobs = g->blobs;
+    p.sigma_min = g->sigma_min, p.sigma_max = g->sigma_max;
+    p.noise_kind = g->noise_kind, p.noise_scale = g->noise_scale, p.seed = g->seed;
+    p.scale_to_unit = g->scale_to_unit;
+    s->e->generate(p, n_total, col0, n_local);
+  });
+}
+
+int mlnmf_session_run_configuration(mlnmf_session* s, size_t level_count, int kind, int cycle, size_t rank,
+                                    uint64_t seed, int budget_mode, double amount, size_t trace_every,
+                                    mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    RunTrace t;
+    run_configuration(*s->e, level_count, to_kind(kind), to_cycle(cycle), rank, seed, budget_mode, amount,
+                      trace_every, t);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+int mlnmf_session_run_cycle(mlnmf_session* s, size_t hierarchy_levels, size_t levels, const void* V0,
+                            const void* W0_local, int host_dtype, size_t r, int kind, int cycle, int budget_mode,
+                            double amount, size_t trace_every, mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    s->e->ensure_levels(hierarchy_levels);
+    s->e->set_factors(0, V0, W0_local, host_dtype, r);
+    RunTrace t;
+    run_cycle(*s->e, levels, r, to_kind(kind), to_cycle(cycle), budget_mode, amount, trace_every, t);
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
+int mlnmf_session_get_factors(mlnmf_session* s, void* V, void* W_local, int host_dtype) {
+  return guard([&] { s->e->get_factors(0, V, W_local, host_dtype); });
+}
+
+int mlnmf_session_set_factors(mlnmf_session* s, const void* V, const void* W_local, int host_dtype, size_t r) {
+  return guard([&] { s->e->set_factors(0, V, W_local, host_dtype, r); });
+}
+
+int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps) {
+  return guard([&] {
+    const Kind k = to_kind(kind);
+    for (size_t i = 0; i < n_steps; ++i) s->e->step(0, k);
+  });
+}
+
+int mlnmf_session_sync(mlnmf_session* s) {
+  return guard([&] { s->e->sync(); });
+}
+
+int mlnmf_session_error(mlnmf_session* s, double* out) {
+  return guard([&] { *out = s->e->frobenius_error(0); });
+}
+
+int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out) {
+  return guard([&] { *out = s->e->norm2(level); });
+}
+
+int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype) {
+  return guard([&] { s->e->export_data(M_local, host_dtype); });
+}
+
+int mlnmf_session_set_profiling(mlnmf_session* s, int on) {
+  return guard([&] {
+    s->e->set_profiling(on != 0);
+    s->e->reset_kernel_times();
+  });
+}
+
+int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, double* vtm_ms, long* vtm_n) {
+  return guard([&] {
+    KernelTimes k = s->e->kernel_times();
+    *mwt_ms = k.mwt_ms, *mwt_n = k.mwt_n, *vtm_ms = k.vtm_ms, *vtm_n = k.vtm_n;
+  });
+}
+
+long mlnmf_session_launches(mlnmf_session* s) { return s->e->launches(); }
+void* mlnmf_session_stream(mlnmf_session* s) { return s->e->stream(); }
+int mlnmf_session_tc_active(mlnmf_session* s) { return s->e->tc_active() ? 1 : 0; }
+int mlnmf_session_gram_error(mlnmf_session* s) { return s->e->gram_error() ? 1 : 0; }
+
+// ---------------------------------------------------------------------------
+size_t mlnmf_trace_num_samples(const mlnmf_trace* t) { return t->t.samples.size(); }
+void mlnmf_trace_samples(const mlnmf_trace* t, double* elapsed_s, double* work_units, int* level, double* error) {
+  for (size_t i = 0; i < t->t.samples.size(); ++i) {
+    const Sample& s = t->t.samples[i];
+    if (elapsed_s) elapsed_s[i] = s.elapsed_s;
+    if (work_units) work_units[i] = s.work_units;
+    if (level) level[i] = s.level;
+    if (error) error[i] = s.error;
+  }
+}
+size_t mlnmf_trace_num_allocations(const mlnmf_trace* t) { return t->t.alloc_level.size(); }
+void mlnmf_trace_allocations(const mlnmf_trace* t, int* level, double* amount) {
+  for (size_t i = 0; i < t->t.alloc_level.size(); ++i) {
+    level[i] = t->t.alloc_level[i];
+    amount[i] = t->t.alloc_amount[i];
+  }
+}
+size_t mlnmf_trace_num_nnls_counts(const mlnmf_trace* t) { return t->t.nnls_counts.size(); }
+void mlnmf_trace_nnls_counts(const mlnmf_trace* t, int* counts) {
+  if (!t->t.nnls_counts.empty()) std::memcpy(counts, t->t.nnls_counts.data(), t->t.nnls_counts.size() * sizeof(int));
+}
+int mlnmf_trace_degenerate(const mlnmf_trace* t) { return t->t.degenerate; }
+size_t mlnmf_trace_num_phases(const mlnmf_trace* t) { return t->t.phase_level.size(); }
+void mlnmf_trace_phases(const mlnmf_trace* t, int* level, long* steps) {
+  for (size_t i = 0; i < t->t.phase_level.size(); ++i) {
+    level[i] = t->t.phase_level[i];
+    steps[i] = t->t.phase_steps[i];
+  }
+}
+void mlnmf_trace_free(mlnmf_trace* t) { delete t; }
+
+}  // extern "C"

@@ -1,0 +1,913 @@
+// engine.cu -- device engine of the multilevel NMF solver (sm_100a).
+//
+// Per step (HALS; MU and ANLS differ only in the update kernels):
+//   [B = W W^T] -> A = M_l W^T -> (allreduce A|B over NCCL) -> V sweep
+//   -> C = V^T M_l, D = V^T V -> W sweep
+// The two M-streaming products go to the SIMT fp64-accumulating GEMMs or, for
+// fp32 storage at scale, to the tcgen05 3xTF32 kernels (tc_gemm.cu).  All
+// state stays on the device; nothing synchronises with the host inside a
+// phase (samples and NNLS counts are collected by flush()).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+#include "nccl_shim.hpp"
+#include "nnls.cuh"
+#include "tc_gemm.hpp"
+#include "transfer_ops.hpp"
+
+namespace mlb {
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e_) + " at " + \
+                               __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")");       \
+  } while (0)
+
+namespace {
+constexpr int kTargetBlocks = 2 * 148;
+constexpr size_t kSmemMax = 227 * 1024;
+
+size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+}  // namespace
+
+struct Engine::Impl {
+  Engine* e;
+  cudaStream_t s = nullptr;
+  int sm_count = 148;
+  // work buffers (fp64)
+  DevBuf AB;      // A (m0 x r) followed by B (r x r): one allreduce
+  DevBuf Cb;      // C (r x n_loc)
+  DevBuf Db;      // D (r x r)
+  DevBuf part;    // split-K partials
+  DevBuf red;     // reduction partials
+  DevBuf scal;    // scalars: [0] ||M||^2 or direct e2, [1] <C,W>, [2] <D,B>, [3] max
+  DevBuf W;       // T (r x n_loc)
+  DevBuf samples; // SampleRec ring
+  DevBuf counts;  // int ring for NNLS counts
+  DevBuf flags;   // [0] degenerate count, [1] nnls error, [2] validate
+  DevBuf tstart;  // run-start globaltimer
+  DevBuf stage;   // host-transfer staging
+  size_t samp_cap = 0, samp_used = 0, cnt_cap = 0, cnt_used = 0;
+  std::vector<Sample> samp_meta;  // host metadata of enqueued samples
+  // validity of cached products w.r.t. current iterates
+  bool B_valid = false;   // B == W W^T (allreduced) for the current W
+  bool CD_valid = false;  // C == V_l^T M_l and D == V_l^T V_l for the current V_l
+  size_t CD_level = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // profiling
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mwt, ev_vtm;
+  std::vector<cudaEvent_t> ev_pool;
+  std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
+  TcGemm* tc = nullptr;
+
+  explicit Impl(Engine* eng) : e(eng) {}
+
+  size_t esz() const { return e->opt_.dtype == 0 ? 4 : 8; }
+  bool exact() const { return e->opt_.exact != 0; }
+
+  template <typename... KArgs, typename... Args>
+  void launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args... args) {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<g, b, smem, s>>>(args...);
+    ++e->launches_;
+    CK(cudaGetLastError());
+  }
+
+  cudaEvent_t ev() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t x = ev_pool.back();
+      ev_pool.pop_back();
+      return x;
+    }
+    cudaEvent_t x;
+    CK(cudaEventCreate(&x));
+    return x;
+  }
+
+  // ---------------- collectives ----------------
+  void allreduce_sum(double* p, size_t count) {
+    if (e->opt_.world <= 1) return;
+    auto& api = NcclApi::get();
+    nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclSum, comm, s), "allreduce");
+  }
+  void allreduce_max(double* p, size_t count) {
+    if (e->opt_.world <= 1) return;
+    auto& api = NcclApi::get();
+    nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclMax, comm, s), "allreduce max");
+  }
+
+  // ---------------- GEMMs ----------------
+  int splits_for(size_t tiles, size_t K) const {
+    if (exact()) return 1;
+    size_t sp = ceil_div(kTargetBlocks, tiles);
+    sp = std::min(sp, ceil_div(K, 256));
+    return (int)std::max<size_t>(sp, 1);
+  }
+
+  // out (rows x ny, fp64) = X (rows x K) * Y (ny x K)^T
+  template <typename T>
+  void gemm_abt(const T* X, const T* Y, size_t rows, size_t ny, size_t K, double* out) {
+    const size_t tiles = ceil_div(rows, GT) * ceil_div(ny, GT);
+    const int sp = splits_for(tiles, K);
+    const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
+    const int spr = (int)ceil_div(K, kchunk);
+    dim3 g((unsigned)ceil_div(rows, GT), (unsigned)ceil_div(ny, GT), (unsigned)spr);
+    double* dst = out;
+    if (spr > 1) {
+      part.ensure((size_t)spr * rows * ny * 8);
+      dst = part.as<double>();
+    }
+    if (exact())
+      launch(k_gemm_abt<T, true>, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst);
+    else
+      launch(k_gemm_abt<T, false>, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst);
+    if (spr > 1) {
+      const size_t cnt = rows * ny;
+      launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0,
+             (const double*)part.as<double>(), cnt, spr, out);
+    }
+  }
+
+  // out (r x ncols, fp64) = V (K x r)^T * X (K x ncols)
+  template <typename T>
+  void gemm_atb(const T* V, const T* X, size_t K, size_t r, size_t ncols, double* out) {
+    const size_t tiles = ceil_div(ncols, GT) * ceil_div(r, GT);
+    const int sp = splits_for(tiles, K);
+    const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
+    const int spr = (int)ceil_div(K, kchunk);
+    dim3 g((unsigned)ceil_div(ncols, GT), (unsigned)ceil_div(r, GT), (unsigned)spr);
+    double* dst = out;
+    if (spr > 1) {
+      part.ensure((size_t)spr * r * ncols * 8);
+      dst = part.as<double>();
+    }
+    if (exact())
+      launch(k_gemm_atb<T, true>, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst);
+    else
+      launch(k_gemm_atb<T, false>, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst);
+    if (spr > 1) {
+      const size_t cnt = r * ncols;
+      launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0,
+             (const double*)part.as<double>(), cnt, spr, out);
+    }
+  }
+
+  double* A() { return AB.as<double>(); }
+  double* B() { return AB.as<double>() + e->lv_[0].m * e->r_; }
+
+  // A = M_l W^T (the first M pass), timed when profiling.
+  template <typename T>
+  void product_mwt(size_t l) {
+    const auto& L = e->lv_[l];
+    std::pair<cudaEvent_t, cudaEvent_t> evp{};
+    if (e->profiling_) {
+      evp = {ev(), ev()};
+      CK(cudaEventRecord(evp.first, s));
+    }
+    if (tc && tc->active())
+      tc->mwt(static_cast<const T*>(L.M), W.as<T>(), L.m, e->n_loc_, e->r_, A(), s, &e->launches_);
+    else
+      gemm_abt<T>(static_cast<const T*>(L.M), W.as<T>(), L.m, e->r_, e->n_loc_, A());
+    if (e->profiling_) {
+      CK(cudaEventRecord(evp.second, s));
+      ev_mwt.push_back(evp);
+    }
+  }
+  // C = V_l^T M_l (the second M pass)
+  template <typename T>
+  void product_vtm(size_t l) {
+    const auto& L = e->lv_[l];
+    std::pair<cudaEvent_t, cudaEvent_t> evp{};
+    if (e->profiling_) {
+      evp = {ev(), ev()};
+      CK(cudaEventRecord(evp.first, s));
+    }
+    if (tc && tc->active())
+      tc->vtm(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->n_loc_, e->r_, Cb.as<double>(), s,
+              &e->launches_);
+    else
+      gemm_atb<T>(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->r_, e->n_loc_, Cb.as<double>());
+    if (e->profiling_) {
+      CK(cudaEventRecord(evp.second, s));
+      ev_vtm.push_back(evp);
+    }
+  }
+  template <typename T>
+  void gram_W() {  // B = W W^T over all ranks
+    gemm_abt<T>(W.as<T>(), W.as<T>(), e->r_, e->r_, e->n_loc_, B());
+  }
+  template <typename T>
+  void gram_V(size_t l) {  // D = V_l^T V_l (replicated)
+    const auto& L = e->lv_[l];
+    gemm_atb<T>(static_cast<const T*>(L.V), static_cast<const T*>(L.V), L.m, e->r_, e->r_, Db.as<double>());
+  }
+
+  // ---------------- row/column sweeps ----------------
+  int sweep_block(int r) const {
+    for (int bd : {128, 64, 32})
+      if ((size_t)r * r * 8 + (size_t)r * bd * 8 <= kSmemMax) return bd;
+    throw std::invalid_argument("rank too large for the device sweep kernels (r <= 128)");
+  }
+
+  template <typename T>
+  void step_t(size_t l, Kind kind) {
+    const auto& L = e->lv_[l];
+    const size_t r = e->r_;
+    int* deg = flags.as<int>();
+    // ---- V half: A = M W^T, B = W W^T (solvers.cpp:82-83,105-106,251-252)
+    const bool needB = !B_valid;
+    if (needB) gram_W<T>();
+    product_mwt<T>(l);
+    if (e->opt_.world > 1) {
+      if (needB && L.m == e->lv_[0].m) {
+        allreduce_sum(A(), L.m * r + r * r);  // A|B contiguous: one collective
+      } else {
+        allreduce_sum(A(), L.m * r);
+        if (needB) allreduce_sum(B(), r * r);
+      }
+    }
+    T* V = static_cast<T*>(L.V);
+    const int bd = sweep_block((int)r);
+    const size_t smem = (r * r + r * bd) * 8;
+    const dim3 gv((unsigned)ceil_div(L.m, bd));
+    if (kind == kHals) {
+      launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
+    } else if (kind == kMu) {
+      launch(k_mu_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
+    } else {
+      nnls<T>((const double*)B(), L.m, (const double*)A(), r, 1, V, r, 1);
+    }
+    // ---- W half: C = V^T M, D = V^T V (solvers.cpp:91-92,124-125,272-273)
+    gram_V<T>(l);
+    product_vtm<T>(l);
+    T* Wp = W.as<T>();
+    const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
+    if (kind == kHals) {
+      launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+             e->n_loc_, (int)r, deg);
+    } else if (kind == kMu) {
+      launch(k_mu_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+             e->n_loc_, (int)r);
+    } else {
+      nnls<T>((const double*)Db.as<double>(), e->n_loc_, (const double*)Cb.as<double>(), 1, e->n_loc_, Wp, 1,
+              e->n_loc_);
+    }
+    B_valid = false;
+    CD_valid = true;
+    CD_level = l;
+  }
+
+  // batched NNLS over nprob problems; counts appended to the count ring
+  template <typename T>
+  void nnls(const double* G, size_t nprob, const double* H, size_t hi, size_t he, T* X, size_t xi, size_t xe) {
+    const int r = (int)e->r_;
+    if (r > 128) throw std::invalid_argument("anls on the device supports rank <= 128");
+    const size_t gbytes = (size_t)r * r * 8, wb = nnls_warp_bytes(r);
+    if (gbytes + wb > kSmemMax) throw std::invalid_argument("anls: rank too large for shared memory");
+    const int nw = (int)std::min<size_t>(8, (kSmemMax - gbytes) / wb);
+    const size_t smem = gbytes + nw * wb;
+    const size_t blocks = std::min<size_t>(ceil_div(nprob, nw), (size_t)sm_count * 8);
+    int* cnt = reserve_counts(nprob);
+    if (exact())
+      launch(k_nnls_batch<T, true>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi, xe,
+             cnt, flags.as<int>() + 1);
+    else
+      launch(k_nnls_batch<T, false>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi,
+             xe, cnt, flags.as<int>() + 1);
+  }
+
+  int* reserve_counts(size_t k) {
+    if (cnt_used + k > cnt_cap) {
+      // grow: keep the already-enqueued counts (device-to-device copy in order)
+      size_t ncap = std::max(cnt_cap * 2, cnt_used + k + (1u << 20));
+      DevBuf nb;
+      nb.ensure(ncap * 4);
+      if (cnt_used) CK(cudaMemcpyAsync(nb.p, counts.p, cnt_used * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      counts.release();
+      counts = nb;
+      cnt_cap = ncap;
+    }
+    int* p = counts.as<int>() + cnt_used;
+    cnt_used += k;
+    return p;
+  }
+
+  // ---------------- error samples ----------------
+  template <typename T>
+  void dot(const void* a, int a_is_t, const void* b, int b_kind, size_t count, double* out) {
+    // b_kind: 0 none (a^2), 1 double, 2 T
+    const size_t blocks = std::min<size_t>(ceil_div(count, 256), 4 * (size_t)sm_count);
+    red.ensure(std::max<size_t>(blocks, 1) * 8);
+    double* rp = red.as<double>();
+    if (a_is_t) {
+      if (b_kind == 0) launch(k_dot_partial<T, T>, dim3((unsigned)blocks), dim3(256), 0, (const T*)a, (const T*)nullptr, count, rp);
+      else launch(k_dot_partial<T, T>, dim3((unsigned)blocks), dim3(256), 0, (const T*)a, (const T*)b, count, rp);
+    } else {
+      if (b_kind == 1) launch(k_dot_partial<double, double>, dim3((unsigned)blocks), dim3(256), 0, (const double*)a, (const double*)b, count, rp);
+      else launch(k_dot_partial<double, T>, dim3((unsigned)blocks), dim3(256), 0, (const double*)a, (const T*)b, count, rp);
+    }
+    launch(k_sum_final, dim3(1), dim3(256), 0, (const double*)rp, blocks, out, 0);
+  }
+
+  template <typename T>
+  void direct_e2(size_t l, double* out) {
+    const auto& L = e->lv_[l];
+    const int r = (int)e->r_;
+    const size_t n = e->n_loc_;
+    const size_t cb = ceil_div(n, 128);
+    size_t sp = 1;
+    if (!exact()) sp = std::max<size_t>(1, std::min(ceil_div(kTargetBlocks, cb), ceil_div(L.m, 256)));
+    const size_t rchunk = ceil_div(ceil_div(L.m, sp), 32) * 32;
+    const size_t spr = ceil_div(L.m, rchunk);
+    part.ensure(spr * n * 8);
+    const size_t smem = ((size_t)r * 128 + 32 * (size_t)r) * 8;
+    if (exact())
+      launch(k_col_sqerr<T, true>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M, (const T*)L.V,
+             (const T*)W.as<T>(), L.m, n, r, rchunk, part.as<double>());
+    else
+      launch(k_col_sqerr<T, false>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M,
+             (const T*)L.V, (const T*)W.as<T>(), L.m, n, r, rchunk, part.as<double>());
+    if (exact()) {
+      launch(k_sum_final, dim3(1), dim3(32), 0, (const double*)part.as<double>(), n, out, 1);
+    } else {
+      red.ensure(n * 8);
+      if (spr > 1)
+        launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(n, 256), 4096)), dim3(256), 0,
+               (const double*)part.as<double>(), n, (int)spr, red.as<double>());
+      const double* colv = spr > 1 ? red.as<double>() : part.as<double>();
+      launch(k_sum_final, dim3(1), dim3(1024), 0, colv, n, out, 0);
+    }
+    allreduce_sum(out, 1);
+  }
+
+  SampleRec* reserve_sample() {
+    if (samp_used == samp_cap) {
+      size_t ncap = std::max<size_t>(samp_cap * 2, 4096);
+      DevBuf nb;
+      nb.ensure(ncap * sizeof(SampleRec));
+      if (samp_used) CK(cudaMemcpyAsync(nb.p, samples.p, samp_used * sizeof(SampleRec), cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      samples.release();
+      samples = nb;
+      samp_cap = ncap;
+    }
+    return samples.as<SampleRec>() + samp_used++;
+  }
+
+  template <typename T>
+  void sample_t(size_t l, double work_units) {
+    double* sc = scal.as<double>();
+    const bool gram = e->gram_error();
+    if (gram) {
+      const auto& L = e->lv_[l];
+      const size_t r = e->r_;
+      if (!(CD_valid && CD_level == l)) {
+        gram_V<T>(l);
+        product_vtm<T>(l);
+        CD_valid = true;
+        CD_level = l;
+      }
+      if (!B_valid) {
+        gram_W<T>();
+        allreduce_sum(B(), r * r);
+        B_valid = true;
+      }
+      CK(cudaMemcpyAsync(sc, &e->lv_[l].norm2, 8, cudaMemcpyHostToDevice, s));
+      dot<T>(Cb.as<double>(), 0, W.as<T>(), 2, r * e->n_loc_, sc + 1);
+      allreduce_sum(sc + 1, 1);
+      dot<T>(Db.as<double>(), 0, B(), 1, r * r, sc + 2);
+      (void)L;
+    } else {
+      direct_e2<T>(l, sc);
+    }
+    SampleRec* rec = reserve_sample();
+    launch(k_write_sample, dim3(1), dim3(1), 0, (const double*)sc, gram ? 1 : 0, rec);
+    samp_meta.push_back({0.0, work_units, (int)l + 1, 0.0});
+  }
+};
+
+// ============================================================================
+
+Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
+  if (o.dtype != 0 && o.dtype != 1) throw std::invalid_argument("dtype must be 0 (fp32) or 1 (fp64)");
+  if (o.gemm == 2 && o.dtype != 0) throw std::invalid_argument("tcgen05 3xTF32 path needs fp32 storage");
+  CK(cudaSetDevice(o.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, o.device));
+  impl_->sm_count = prop.multiProcessorCount;
+  if (prop.major != 10)
+    throw std::runtime_error("mlnmf_b200 requires an sm_100 (B200) GPU; found " + std::string(prop.name));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  impl_->s = st;
+  stream_ = st;
+  impl_->flags.ensure(16);
+  CK(cudaMemsetAsync(impl_->flags.p, 0, 16, st));
+  impl_->scal.ensure(64);
+  impl_->tstart.ensure(8);
+  impl_->tc = make_tc_gemm(o.dtype == 0 && o.gemm != 1, o.gemm == 2);
+  if (o.world > 1) {
+    if (!o.has_nccl_id) throw std::invalid_argument("world > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_id, sizeof(id));
+    nccl_check(NcclApi::get().CommInitRank(&impl_->comm, o.world, id, o.rank), "CommInitRank");
+  }
+}
+
+Engine::~Engine() {
+  if (!impl_) return;
+  cudaStreamSynchronize(impl_->s);
+  for (auto& L : lv_) {
+    cudaFree(L.M);
+    cudaFree(L.V);
+    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+  }
+  for (DevBuf* b : {&impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
+                    &impl_->samples, &impl_->counts, &impl_->flags, &impl_->tstart, &impl_->stage})
+    b->release();
+  for (auto& p : impl_->ev_mwt) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+  for (auto& p : impl_->ev_vtm) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+  for (auto x : impl_->ev_pool) cudaEventDestroy(x);
+  delete impl_->tc;
+  if (impl_->comm) NcclApi::get().CommDestroy(impl_->comm);
+  cudaStreamDestroy(impl_->s);
+  delete impl_;
+}
+
+bool Engine::tc_active() const { return impl_->tc && impl_->tc->active(); }
+bool Engine::gram_error() const {
+  if (opt_.error_mode == 1) return true;
+  if (opt_.error_mode == 2) return false;
+  // auto: the Gram identity needs fp64-accurate C, D (SURVEY finding 4) and a
+  // non-exact run (exact mode reproduces the reference's direct residual).
+  return !opt_.exact && !tc_active();
+}
+
+void Engine::sync() { CK(cudaStreamSynchronize(impl_->s)); }
+
+template <typename T>
+static void validate_dev(Engine::Impl* im, const T* M, size_t count) {
+  CK(cudaMemsetAsync(im->flags.as<int>() + 2, 0, 4, im->s));
+  im->launch(k_validate<T>, dim3((unsigned)std::min<size_t>(ceil_div(count, 256), 4096)), dim3(256), 0, M, count,
+             im->flags.as<int>() + 2);
+  int f = 0;
+  CK(cudaMemcpyAsync(&f, im->flags.as<int>() + 2, 4, cudaMemcpyDeviceToHost, im->s));
+  CK(cudaStreamSynchronize(im->s));
+  if (f) throw std::invalid_argument("Matrix::from_data: negative or non-finite entry");
+}
+
+void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, size_t n_loc, size_t n_total,
+                      size_t col0, size_t h, size_t w, bool validate) {
+  if (m == 0 || n_loc == 0) throw std::invalid_argument("Matrix: dimensions must be positive");
+  if (h * w != m) throw std::invalid_argument("GridHierarchy: grid does not match matrix rows");
+  for (auto& L : lv_) {
+    cudaFree(L.M), cudaFree(L.V);
+    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+  }
+  lv_.clear();
+  n_loc_ = n_loc;
+  n_total_ = n_total;
+  col0_ = col0;
+  Level L0{h, w, m};
+  const size_t count = m * n_loc, es = impl_->esz();
+  CK(cudaMalloc(&L0.M, count * es));
+  lv_.push_back(L0);
+  cudaStream_t s = impl_->s;
+  const size_t hs = host_dtype == 0 ? 4 : 8;
+  const cudaMemcpyKind kind = is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if ((size_t)hs == es) {
+    CK(cudaMemcpyAsync(L0.M, M, count * es, kind, s));
+  } else {
+    // convert through a staging buffer in chunks
+    const size_t chunk = std::min<size_t>(count, (size_t)64 << 20);
+    impl_->stage.ensure(chunk * hs);
+    for (size_t off = 0; off < count; off += chunk) {
+      const size_t c = std::min(chunk, count - off);
+      CK(cudaMemcpyAsync(impl_->stage.p, static_cast<const char*>(M) + off * hs, c * hs, kind, s));
+      const unsigned g = (unsigned)std::min<size_t>(ceil_div(c, 256), 8192);
+      if (hs == 8)
+        impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)impl_->stage.p,
+                      static_cast<float*>(L0.M) + off, c);
+      else
+        impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)impl_->stage.p,
+                      static_cast<double*>(L0.M) + off, c);
+      CK(cudaStreamSynchronize(s));  // staging reuse
+    }
+  }
+  if (validate) {
+    if (opt_.dtype == 0) validate_dev(impl_, static_cast<const float*>(L0.M), count);
+    else validate_dev(impl_, static_cast<const double*>(L0.M), count);
+  }
+  impl_->B_valid = impl_->CD_valid = false;
+  CK(cudaStreamSynchronize(s));
+}
+
+void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_loc) {
+  const size_t m = g.h * g.w;
+  // allocate level 0
+  for (auto& L : lv_) {
+    cudaFree(L.M), cudaFree(L.V);
+    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+  }
+  lv_.clear();
+  n_loc_ = n_loc;
+  n_total_ = n_total;
+  col0_ = col0;
+  Level L0{g.h, g.w, m};
+  CK(cudaMalloc(&L0.M, m * n_loc * impl_->esz()));
+  lv_.push_back(L0);
+  cudaStream_t s = impl_->s;
+  const int r = (int)g.r;
+  if (n_loc > ((size_t)1 << 31)) throw std::invalid_argument("generate: too many columns per rank");
+  DevBuf V0, W0, bm;
+  V0.ensure(m * r * 8);
+  W0.ensure((size_t)r * n_loc * 8);
+  impl_->launch(k_gen_basis, dim3((unsigned)std::min<size_t>(ceil_div(m * r, 256), 8192)), dim3(256), 0,
+                V0.as<double>(), g.h, g.w, r, (int)g.blobs, g.sigma_min, g.sigma_max, gen_key(g.seed, 1));
+  impl_->launch(k_gen_wcols, dim3((unsigned)std::min<size_t>(ceil_div(r * n_loc, 256), 8192)), dim3(256), 0,
+                W0.as<double>(), r, n_loc, n_total, col0, gen_key(g.seed, 2));
+  const uint64_t kn = gen_key(g.seed, 3);
+  const size_t smem = ((size_t)r * 128 + 32 * (size_t)r) * 8;
+  const dim3 gg((unsigned)ceil_div(n_loc, 128), (unsigned)ceil_div(m, 32));
+  auto run = [&](int mode, double div) {
+    if (opt_.dtype == 0)
+      impl_->launch(k_gen_m<float>, gg, dim3(128), smem, static_cast<float*>(L0.M), (const double*)V0.as<double>(),
+                    (const double*)W0.as<double>(), m, n_loc, r, col0, kn, g.noise_kind, g.noise_scale, mode, div,
+                    bm.as<double>());
+    else
+      impl_->launch(k_gen_m<double>, gg, dim3(128), smem, static_cast<double*>(L0.M), (const double*)V0.as<double>(),
+                    (const double*)W0.as<double>(), m, n_loc, r, col0, kn, g.noise_kind, g.noise_scale, mode, div,
+                    bm.as<double>());
+  };
+  if (!g.scale_to_unit) {
+    run(0, 1.0);
+  } else {
+    // M /= max(M) over the whole (all-rank) matrix, computed on the fp64 values
+    bm.ensure((size_t)gg.x * gg.y * 8);
+    run(1, 1.0);
+    impl_->launch(k_max_final, dim3(1), dim3(1024), 0, (const double*)bm.as<double>(), (size_t)gg.x * gg.y,
+                  impl_->scal.as<double>() + 3);
+    impl_->allreduce_max(impl_->scal.as<double>() + 3, 1);
+    double mx = 0;
+    CK(cudaMemcpyAsync(&mx, impl_->scal.as<double>() + 3, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    run(2, mx);
+  }
+  CK(cudaStreamSynchronize(s));
+  V0.release();
+  W0.release();
+  bm.release();
+  impl_->B_valid = impl_->CD_valid = false;
+}
+
+void Engine::ensure_levels(size_t L) {
+  if (lv_.empty()) throw std::invalid_argument("no data set");
+  if (L < 1) throw std::invalid_argument("GridHierarchy: need at least one level");
+  const size_t es = impl_->esz();
+  while (lv_.size() < L) {
+    Level& cur = lv_.back();
+    if (cur.h < 2 || cur.w < 2) throw std::invalid_argument("GridHierarchy: too many levels for this grid");
+    HostCsr R = build_restriction(cur.h, cur.w), P = build_prolongation(cur.h, cur.w);
+    auto up = [&](const HostCsr& op, int** p, int** i, double** w) {
+      CK(cudaMalloc(p, op.rowptr.size() * 4));
+      CK(cudaMalloc(i, op.idx.size() * 4));
+      CK(cudaMalloc(w, op.wt.size() * 8));
+      CK(cudaMemcpy(*p, op.rowptr.data(), op.rowptr.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(*i, op.idx.data(), op.idx.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(*w, op.wt.data(), op.wt.size() * 8, cudaMemcpyHostToDevice));
+    };
+    up(R, &cur.Rp, &cur.Ri, &cur.Rw);
+    up(P, &cur.Pp, &cur.Pi, &cur.Pw);
+    Level nx{(cur.h + 1) / 2, (cur.w + 1) / 2, 0};
+    nx.m = nx.h * nx.w;
+    CK(cudaMalloc(&nx.M, nx.m * n_loc_ * es));
+    const size_t colblocks = ceil_div(n_loc_, 256);
+    if (opt_.dtype == 0)
+      impl_->launch(k_csr_apply<float>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
+                    (const int*)cur.Ri, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), nx.m,
+                    n_loc_, colblocks);
+    else
+      impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
+                    (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M), nx.m,
+                    n_loc_, colblocks);
+    if (r_ > 0) CK(cudaMalloc(&nx.V, nx.m * r_ * es));
+    lv_.push_back(nx);
+  }
+  CK(cudaStreamSynchronize(impl_->s));
+}
+
+double Engine::norm2(size_t l) {
+  Level& L = lv_.at(l);
+  if (L.norm2 < 0) {
+    double* sc = impl_->scal.as<double>();
+    if (opt_.dtype == 0) impl_->dot<float>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
+    else impl_->dot<double>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
+    impl_->allreduce_sum(sc + 4, 1);
+    CK(cudaMemcpyAsync(&L.norm2, sc + 4, 8, cudaMemcpyDeviceToHost, impl_->s));
+    CK(cudaStreamSynchronize(impl_->s));
+  }
+  return L.norm2;
+}
+
+void Engine::init_random(size_t r, uint64_t seed) {
+  if (lv_.empty()) throw std::invalid_argument("no data set");
+  const size_t m0 = lv_[0].m;
+  if (r < 1 || r > std::min(m0, n_total_))
+    throw std::invalid_argument("random_init: rank must satisfy 1 <= r <= min(m,n)");
+  set_factors(0, nullptr, nullptr, opt_.dtype, r);
+  const size_t tot = m0 * r + r * n_loc_;
+  const unsigned g = (unsigned)std::min<size_t>(ceil_div(tot, 256), 8192);
+  if (opt_.dtype == 0)
+    impl_->launch(k_random_init<float>, dim3(g), dim3(256), 0, static_cast<float*>(lv_[0].V), impl_->W.as<float>(), m0,
+                  r, n_loc_, n_total_, col0_, seed);
+  else
+    impl_->launch(k_random_init<double>, dim3(g), dim3(256), 0, static_cast<double*>(lv_[0].V),
+                  impl_->W.as<double>(), m0, r, n_loc_, n_total_, col0_, seed);
+}
+
+void Engine::set_factors(size_t l, const void* V, const void* W, int host_dtype, size_t r) {
+  if (lv_.empty()) throw std::invalid_argument("no data set");
+  const size_t es = impl_->esz();
+  if (r != r_) {
+    for (auto& L : lv_) {
+      cudaFree(L.V);
+      L.V = nullptr;
+    }
+    r_ = r;
+  }
+  for (auto& L : lv_)
+    if (!L.V) CK(cudaMalloc(&L.V, L.m * r * es));
+  impl_->W.ensure(r * n_loc_ * es);
+  impl_->AB.ensure((lv_[0].m * r + r * r) * 8);
+  impl_->Cb.ensure(r * n_loc_ * 8);
+  impl_->Db.ensure(r * r * 8);
+  impl_->B_valid = impl_->CD_valid = false;
+  auto put = [&](void* dst, const void* src, size_t count) {
+    if (!src) return;
+    const size_t hs = host_dtype == 0 ? 4 : 8;
+    if (hs == es) {
+      CK(cudaMemcpyAsync(dst, src, count * es, cudaMemcpyHostToDevice, impl_->s));
+    } else {
+      impl_->stage.ensure(count * hs);
+      CK(cudaMemcpyAsync(impl_->stage.p, src, count * hs, cudaMemcpyHostToDevice, impl_->s));
+      const unsigned g = (unsigned)std::min<size_t>(ceil_div(count, 256), 8192);
+      if (hs == 8) impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)impl_->stage.p, (float*)dst, count);
+      else impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)impl_->stage.p, (double*)dst, count);
+    }
+    CK(cudaStreamSynchronize(impl_->s));
+  };
+  put(lv_.at(l).V, V, lv_[l].m * r);
+  put(impl_->W.p, W, r * n_loc_);
+}
+
+void Engine::get_factors(size_t l, void* V, void* W, int host_dtype) {
+  const size_t es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
+  auto get = [&](const void* src, void* dst, size_t count) {
+    if (!dst) return;
+    if (hs == es) {
+      CK(cudaMemcpyAsync(dst, src, count * es, cudaMemcpyDeviceToHost, impl_->s));
+    } else {
+      impl_->stage.ensure(count * hs);
+      const unsigned g = (unsigned)std::min<size_t>(ceil_div(count, 256), 8192);
+      if (hs == 8) impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)src, (double*)impl_->stage.p, count);
+      else impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)src, (float*)impl_->stage.p, count);
+      CK(cudaMemcpyAsync(dst, impl_->stage.p, count * hs, cudaMemcpyDeviceToHost, impl_->s));
+    }
+    CK(cudaStreamSynchronize(impl_->s));
+  };
+  get(lv_.at(l).V, V, lv_[l].m * r_);
+  get(impl_->W.p, W, r_ * n_loc_);
+}
+
+void Engine::export_data(void* M_host, int host_dtype) {
+  if (lv_.empty()) throw std::invalid_argument("no data set");
+  const size_t count = lv_[0].m * n_loc_, es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
+  if (hs != es) throw std::invalid_argument("export_data: host dtype must match the storage dtype");
+  CK(cudaMemcpyAsync(M_host, lv_[0].M, count * es, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+}
+
+void Engine::restrict_V(size_t l) {
+  Level& f = lv_.at(l);
+  Level& c = lv_.at(l + 1);
+  const size_t cb = ceil_div(r_, 64);
+  if (opt_.dtype == 0)
+    impl_->launch(k_csr_apply<float>, dim3((unsigned)(c.m * cb)), dim3(64), 0, (const int*)f.Rp, (const int*)f.Ri,
+                  (const double*)f.Rw, (const float*)f.V, static_cast<float*>(c.V), c.m, r_, cb);
+  else
+    impl_->launch(k_csr_apply<double>, dim3((unsigned)(c.m * cb)), dim3(64), 0, (const int*)f.Rp, (const int*)f.Ri,
+                  (const double*)f.Rw, (const double*)f.V, static_cast<double*>(c.V), c.m, r_, cb);
+}
+
+void Engine::prolong_V(size_t l) {
+  Level& f = lv_.at(l);
+  Level& c = lv_.at(l + 1);
+  const size_t cb = ceil_div(r_, 64);
+  if (opt_.dtype == 0)
+    impl_->launch(k_csr_apply<float>, dim3((unsigned)(f.m * cb)), dim3(64), 0, (const int*)f.Pp, (const int*)f.Pi,
+                  (const double*)f.Pw, (const float*)c.V, static_cast<float*>(f.V), f.m, r_, cb);
+  else
+    impl_->launch(k_csr_apply<double>, dim3((unsigned)(f.m * cb)), dim3(64), 0, (const int*)f.Pp, (const int*)f.Pi,
+                  (const double*)f.Pw, (const double*)c.V, static_cast<double*>(f.V), f.m, r_, cb);
+  impl_->CD_valid = false;
+}
+
+void Engine::step(size_t l, Kind kind) {
+  if (l >= lv_.size()) throw std::invalid_argument("step: level not built");
+  if (r_ == 0) throw std::invalid_argument("step: factors not initialised");
+  if (impl_->CD_valid && impl_->CD_level != l) impl_->CD_valid = false;
+  if (opt_.dtype == 0) impl_->step_t<float>(l, kind);
+  else impl_->step_t<double>(l, kind);
+}
+
+void Engine::sample(size_t l, double work_units) {
+  norm2(l);  // host-cached after first use (one sync per level per run)
+  if (impl_->CD_valid && impl_->CD_level != l) impl_->CD_valid = false;
+  if (opt_.dtype == 0) impl_->sample_t<float>(l, work_units);
+  else impl_->sample_t<double>(l, work_units);
+}
+
+void Engine::mark_run_start() {
+  impl_->launch(k_timestamp, dim3(1), dim3(1), 0, impl_->tstart.as<unsigned long long>());
+  impl_->host_t0 = std::chrono::steady_clock::now();
+  CK(cudaMemsetAsync(impl_->flags.p, 0, 8, impl_->s));
+  impl_->samp_used = 0;
+  impl_->samp_meta.clear();
+  impl_->cnt_used = 0;
+}
+
+double Engine::host_elapsed_s() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - impl_->host_t0).count();
+}
+
+void Engine::flush(std::vector<Sample>* samples, std::vector<int>* counts, int* degenerate) {
+  cudaStream_t s = impl_->s;
+  std::vector<SampleRec> recs(impl_->samp_used);
+  unsigned long long t0 = 0;
+  int fl[2] = {0, 0};
+  if (!recs.empty())
+    CK(cudaMemcpyAsync(recs.data(), impl_->samples.p, recs.size() * sizeof(SampleRec), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&t0, impl_->tstart.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(fl, impl_->flags.p, 8, cudaMemcpyDeviceToHost, s));
+  std::vector<int> cn(impl_->cnt_used);
+  if (!cn.empty()) CK(cudaMemcpyAsync(cn.data(), impl_->counts.p, cn.size() * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (fl[1] & 1) throw NnlsCapExceeded("anls_step: NNLS exchange cap exceeded");
+  if (fl[1] & 2) throw NnlsCapExceeded("anls_step: NNLS failed (singular passive subsystem)");
+  if (samples) {
+    for (size_t i = 0; i < recs.size(); ++i) {
+      Sample smp = impl_->samp_meta[i];
+      smp.error = recs[i].error;
+      smp.elapsed_s = recs[i].t_ns >= t0 ? (double)(recs[i].t_ns - t0) * 1e-9 : 0.0;
+      samples->push_back(smp);
+    }
+  }
+  if (counts) counts->insert(counts->end(), cn.begin(), cn.end());
+  if (degenerate) *degenerate += fl[0];
+  impl_->samp_used = 0;
+  impl_->samp_meta.clear();
+  impl_->cnt_used = 0;
+  CK(cudaMemsetAsync(impl_->flags.p, 0, 8, s));
+}
+
+double Engine::frobenius_error(size_t l) {
+  double* sc = impl_->scal.as<double>();
+  if (opt_.dtype == 0) impl_->direct_e2<float>(l, sc);
+  else impl_->direct_e2<double>(l, sc);
+  double e2 = 0;
+  CK(cudaMemcpyAsync(&e2, sc, 8, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+  return std::sqrt(e2);
+}
+
+void Engine::apply_transfer(size_t h, size_t w, int which, const double* X, size_t ncols, double* Y) {
+  HostCsr op = which == 0 ? build_restriction(h, w) : build_prolongation(h, w);
+  const size_t in_dim = which == 0 ? h * w : ((h + 1) / 2) * ((w + 1) / 2);
+  const size_t out_dim = op.rowptr.size() - 1;
+  DevBuf p, i, wt, x, y;
+  p.ensure(op.rowptr.size() * 4);
+  i.ensure(std::max<size_t>(op.idx.size(), 1) * 4);
+  wt.ensure(std::max<size_t>(op.wt.size(), 1) * 8);
+  x.ensure(in_dim * ncols * 8);
+  y.ensure(out_dim * ncols * 8);
+  cudaStream_t s = impl_->s;
+  CK(cudaMemcpyAsync(p.p, op.rowptr.data(), op.rowptr.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(i.p, op.idx.data(), op.idx.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(wt.p, op.wt.data(), op.wt.size() * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(x.p, X, in_dim * ncols * 8, cudaMemcpyHostToDevice, s));
+  const size_t cb = ceil_div(ncols, 128);
+  impl_->launch(k_csr_apply<double>, dim3((unsigned)(out_dim * cb)), dim3(128), 0, (const int*)p.p, (const int*)i.p,
+                (const double*)wt.p, (const double*)x.p, (double*)y.p, out_dim, ncols, cb);
+  CK(cudaMemcpyAsync(Y, y.p, out_dim * ncols * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (DevBuf* b : {&p, &i, &wt, &x, &y}) b->release();
+}
+
+void Engine::nnls_single(const double* G, const double* h, const double* x0, size_t r, double* x, int* iterations) {
+  if (r < 1) throw std::invalid_argument("nnls_active_set: dimension mismatch");
+  DevBuf g, hb, xb, cb;
+  g.ensure(r * r * 8);
+  hb.ensure(r * 8);
+  xb.ensure(r * 8);
+  cudaStream_t s = impl_->s;
+  CK(cudaMemcpyAsync(g.p, G, r * r * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(hb.p, h, r * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(xb.p, x0, r * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(impl_->flags.p, 0, 8, s));
+  const size_t r_save = r_;
+  r_ = r;
+  impl_->cnt_used = 0;
+  try {
+    impl_->nnls<double>(g.as<double>(), 1, hb.as<double>(), r, 1, xb.as<double>(), r, 1);
+  } catch (...) {
+    r_ = r_save;
+    throw;
+  }
+  r_ = r_save;
+  int fl[2] = {0, 0}, it = 0;
+  CK(cudaMemcpyAsync(x, xb.p, r * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&it, impl_->counts.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(fl, impl_->flags.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  impl_->cnt_used = 0;
+  for (DevBuf* b : {&g, &hb, &xb, &cb}) b->release();
+  if (fl[1] & 1) throw NnlsCapExceeded("nnls_active_set: exchange cap exceeded");
+  if (fl[1] & 2) throw std::runtime_error("nnls_active_set: singular passive subsystem");
+  *iterations = it;
+}
+
+void Engine::random_init_host(size_t m, size_t n, size_t r, uint64_t seed, double* V, double* W) {
+  if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("random_init: rank must satisfy 1 <= r <= min(m,n)");
+  DevBuf v, w;
+  v.ensure(m * r * 8);
+  w.ensure(r * n * 8);
+  const unsigned g = (unsigned)std::min<size_t>(ceil_div(m * r + r * n, 256), 8192);
+  impl_->launch(k_random_init<double>, dim3(g), dim3(256), 0, v.as<double>(), w.as<double>(), m, r, n, n, (size_t)0,
+                seed);
+  CK(cudaMemcpyAsync(V, v.p, m * r * 8, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaMemcpyAsync(W, w.p, r * n * 8, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+  v.release();
+  w.release();
+}
+
+KernelTimes Engine::kernel_times() {
+  sync();
+  KernelTimes kt;
+  for (auto& p : impl_->ev_mwt) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p.first, p.second));
+    kt.mwt_ms += ms;
+    ++kt.mwt_n;
+  }
+  for (auto& p : impl_->ev_vtm) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p.first, p.second));
+    kt.vtm_ms += ms;
+    ++kt.vtm_n;
+  }
+  return kt;
+}
+
+void Engine::reset_kernel_times() {
+  sync();
+  for (auto& p : impl_->ev_mwt) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
+  for (auto& p : impl_->ev_vtm) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
+  impl_->ev_mwt.clear();
+  impl_->ev_vtm.clear();
+}
+
+}  // namespace mlb

@@ -1,0 +1,575 @@
+// kernels.cuh -- SIMT CUDA kernels of the multilevel NMF solver path (sm_100a).
+//
+// Storage type T is float or double (M, V, W); every accumulation and every
+// r x r / m x r / r x n intermediate (A = M W^T, B = W W^T, C = V^T M,
+// D = V^T V) is fp64.  fp32 products are exact in fp64, so the fp32 path is
+// "fp64 arithmetic on fp32 storage" (the most accurate
+// fp32 variant).
+//
+// EXACT = true reproduces the reference's floating-point operation order
+// (no FMA contraction, sequential K accumulation, no split-K), so an fp64 run
+// is bit-identical to the reference CPU build (proj/src/kernels.cpp,
+// solvers.cpp, transfer.cpp).  EXACT = false uses FMA and split-K for
+// parallelism; parity is then within the stated tolerance.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mlb {
+
+template <typename T>
+__device__ __forceinline__ T to_t(double v);
+template <>
+__device__ __forceinline__ float to_t<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ double to_t<double>(double v) { return v; }
+
+template <bool EXACT>
+__device__ __forceinline__ double madd(double acc, double a, double b) {
+  if constexpr (EXACT) return __dadd_rn(acc, __dmul_rn(a, b));
+  else return fma(a, b, acc);
+}
+
+// reference: `s -= a * b` (solvers.cpp:118,136) -- always unfused, these are
+// O((m+n) r^2) sweeps, not the hot GEMMs.
+__device__ __forceinline__ double msub(double acc, double a, double b) {
+  return __dsub_rn(acc, __dmul_rn(a, b));
+}
+
+// ---------------------------------------------------------------------------
+// SplitMix64 (proj/include/mlnmf/matrix.hpp:76-95), counter form: the c-th
+// (0-based) output of Rng(seed) is mix(seed + (c+1) * gamma).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ double sm64_uniform(uint64_t seed, uint64_t c) {
+  return (double)(sm64_mix(seed + (c + 1) * 0x9E3779B97F4A7C15ULL) >> 11) * 0x1.0p-53;
+}
+
+// ---------------------------------------------------------------------------
+// Tall-skinny GEMMs.  Tiles 64 x 64 outputs, K step 32, 256 threads, 4x4
+// outputs per thread; fp64 accumulators; operand tiles staged in shared
+// memory as fp64.
+// ---------------------------------------------------------------------------
+constexpr int GT = 64;   // output tile edge
+constexpr int GK = 32;   // K step
+
+// part[z][i][k] = sum_{p in split z} X[i][p] * Y[k][p]
+//   X: rows x K (row-major, ld = K), Y: ny x K (row-major, ld = K).
+//   (A = M W^T with X = M, Y = W; B = W W^T with X = Y = W.)
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const T* __restrict__ Y,
+                                                  size_t rows, size_t ny, size_t K, size_t kchunk,
+                                                  double* __restrict__ part) {
+  __shared__ double Xs[GK][GT + 1];
+  __shared__ double Ys[GK][GT + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const size_t i0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
+  const size_t kb = (size_t)blockIdx.z * kchunk;
+  const size_t ke = kb + kchunk < K ? kb + kchunk : K;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (size_t p0 = kb; p0 < ke; p0 += GK) {
+#pragma unroll
+    for (int q = 0; q < (GT * GK) / 256; ++q) {
+      const int e = tid + 256 * q, rr = e / GK, pp = e % GK;
+      const size_t p = p0 + pp;
+      const size_t gi = i0 + rr, gk = k0 + rr;
+      Xs[pp][rr] = (gi < rows && p < ke) ? (double)X[gi * K + p] : 0.0;
+      Ys[pp][rr] = (gk < ny && p < ke) ? (double)Y[gk * K + p] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < GK; ++kk) {
+      double xa[4], yb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xa[a] = Xs[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) yb[b] = Ys[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], xa[a], yb[b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.z * rows * ny;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const size_t gi = i0 + ty + 16 * a;
+    if (gi >= rows) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const size_t gk = k0 + tx + 16 * b;
+      if (gk < ny) out[gi * ny + gk] = acc[a][b];
+    }
+  }
+}
+
+// part[z][k][j] = sum_{i in split z} V[i][k] * X[i][j]
+//   V: K x r (row-major), X: K x ncols (row-major).
+//   (C = V^T M with X = M; D = V^T V with X = V, ncols = r.)
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const T* __restrict__ X,
+                                                  size_t K, size_t r, size_t ncols, size_t kchunk,
+                                                  double* __restrict__ part) {
+  __shared__ double Xs[GK][GT + 1];
+  __shared__ double Vs[GK][GT + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const size_t j0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
+  const size_t ib = (size_t)blockIdx.z * kchunk;
+  const size_t ie = ib + kchunk < K ? ib + kchunk : K;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (size_t p0 = ib; p0 < ie; p0 += GK) {
+#pragma unroll
+    for (int q = 0; q < (GT * GK) / 256; ++q) {
+      const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
+      const size_t i = p0 + ii;
+      const size_t gj = j0 + cc, gk = k0 + cc;
+      Xs[ii][cc] = (i < ie && gj < ncols) ? (double)X[i * ncols + gj] : 0.0;
+      Vs[ii][cc] = (i < ie && gk < r) ? (double)V[i * r + gk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int ii = 0; ii < GK; ++ii) {
+      double va[4], xb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = Vs[ii][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) xb[b] = Xs[ii][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], va[a], xb[b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.z * r * ncols;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const size_t gk = k0 + ty + 16 * a;
+    if (gk >= r) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const size_t gj = j0 + tx + 16 * b;
+      if (gj < ncols) out[gk * ncols + gj] = acc[a][b];
+    }
+  }
+}
+
+// out[e] = sum_z part[z][e], z ascending (deterministic split-K epilogue).
+__global__ void k_reduce_splits(const double* __restrict__ part, size_t count, int splits,
+                                double* __restrict__ out) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (size_t)gridDim.x * blockDim.x) {
+    double s = part[e];
+    for (int z = 1; z < splits; ++z) s += part[(size_t)z * count + e];
+    out[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// HALS sweeps (solvers.cpp:101-141).  One thread per row of V (resp. column
+// of W); the r x r Gram in shared memory; the thread's row/column held in
+// shared memory as fp64, layout [l][thread] (bank-conflict free).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_hals_v(const double* __restrict__ A, const double* __restrict__ B, T* __restrict__ V,
+                         size_t m, int r, int* __restrict__ degenerate) {
+  extern __shared__ double sm[];
+  const int bd = blockDim.x, t = threadIdx.x;
+  double* Bs = sm;
+  double* vs = sm + (size_t)r * r;
+  for (int e = t; e < r * r; e += bd) Bs[e] = B[e];
+  const size_t i = (size_t)blockIdx.x * bd + t;
+  const bool act = i < m;
+  if (act)
+    for (int l = 0; l < r; ++l) vs[l * bd + t] = (double)V[i * r + l];
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    const double bkk = Bs[k * r + k];
+    if (bkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && t == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    if (!act) continue;
+    double num = __dadd_rn(A[i * r + k], __dmul_rn(vs[k * bd + t], bkk));
+    for (int l = 0; l < r; ++l) num = msub(num, vs[l * bd + t], Bs[l * r + k]);
+    const double q = num / bkk;
+    vs[k * bd + t] = q > 0.0 ? q : 0.0;  // std::max(0.0, q)
+  }
+  if (act)
+    for (int l = 0; l < r; ++l) V[i * r + l] = to_t<T>(vs[l * bd + t]);
+}
+
+template <typename T>
+__global__ void k_hals_w(const double* __restrict__ Cm, const double* __restrict__ D, T* __restrict__ W,
+                         size_t n, int r, int* __restrict__ degenerate) {
+  extern __shared__ double sm[];
+  const int bd = blockDim.x, t = threadIdx.x;
+  double* Ds = sm;
+  double* ws = sm + (size_t)r * r;
+  for (int e = t; e < r * r; e += bd) Ds[e] = D[e];
+  const size_t j = (size_t)blockIdx.x * bd + t;
+  const bool act = j < n;
+  if (act)
+    for (int l = 0; l < r; ++l) ws[l * bd + t] = (double)W[(size_t)l * n + j];
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    const double dkk = Ds[k * r + k];
+    if (dkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && t == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    if (!act) continue;
+    double num = __dadd_rn(Cm[(size_t)k * n + j], __dmul_rn(dkk, ws[k * bd + t]));
+    for (int l = 0; l < r; ++l) num = msub(num, Ds[k * r + l], ws[l * bd + t]);
+    const double q = num / dkk;
+    ws[k * bd + t] = q > 0.0 ? q : 0.0;
+  }
+  if (act)
+    for (int l = 0; l < r; ++l) W[(size_t)l * n + j] = to_t<T>(ws[l * bd + t]);
+}
+
+// ---------------------------------------------------------------------------
+// MU updates (solvers.cpp:79-99).  Jacobi within a half: the denominator uses
+// the old factor.  V(i,:) *= A(i,:) / max(V(i,:) B, 1e-16).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double mu_floor(double v) { return v < 1e-16 ? 1e-16 : v; }  // std::max(v, 1e-16)
+
+template <typename T>
+__global__ void k_mu_v(const double* __restrict__ A, const double* __restrict__ B, T* __restrict__ V,
+                       size_t m, int r) {
+  extern __shared__ double sm[];
+  const int bd = blockDim.x, t = threadIdx.x;
+  double* Bs = sm;
+  double* vs = sm + (size_t)r * r;
+  for (int e = t; e < r * r; e += bd) Bs[e] = B[e];
+  const size_t i = (size_t)blockIdx.x * bd + t;
+  const bool act = i < m;
+  if (act)
+    for (int l = 0; l < r; ++l) vs[l * bd + t] = (double)V[i * r + l];
+  __syncthreads();
+  if (!act) return;
+  for (int j = 0; j < r; ++j) {
+    double s = 0.0;
+    for (int p = 0; p < r; ++p) s = __dadd_rn(s, __dmul_rn(vs[p * bd + t], Bs[p * r + j]));
+    V[i * r + j] = to_t<T>(__dmul_rn(vs[j * bd + t], A[i * r + j] / mu_floor(s)));
+  }
+}
+
+// W(:,j) *= C(:,j) / max(D W(:,j), 1e-16)
+template <typename T>
+__global__ void k_mu_w(const double* __restrict__ Cm, const double* __restrict__ D, T* __restrict__ W,
+                       size_t n, int r) {
+  extern __shared__ double sm[];
+  const int bd = blockDim.x, t = threadIdx.x;
+  double* Ds = sm;
+  double* ws = sm + (size_t)r * r;
+  for (int e = t; e < r * r; e += bd) Ds[e] = D[e];
+  const size_t j = (size_t)blockIdx.x * bd + t;
+  const bool act = j < n;
+  if (act)
+    for (int l = 0; l < r; ++l) ws[l * bd + t] = (double)W[(size_t)l * n + j];
+  __syncthreads();
+  if (!act) return;
+  for (int k = 0; k < r; ++k) {
+    double s = 0.0;
+    for (int p = 0; p < r; ++p) s = __dadd_rn(s, __dmul_rn(Ds[k * r + p], ws[p * bd + t]));
+    W[(size_t)k * n + j] = to_t<T>(__dmul_rn(ws[k * bd + t], Cm[(size_t)k * n + j] / mu_floor(s)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Direct residual ||M - VW||^2 per column (kernels.cpp:48-60):
+//   part[z][j] = sum_{i in split z} (M_ij - sum_k V_ik W_kj)^2
+// 128 columns per block; V rows staged 32 at a time; W column tile in smem.
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(128) k_col_sqerr(const T* __restrict__ M, const T* __restrict__ V,
+                                                   const T* __restrict__ W, size_t m, size_t n, int r,
+                                                   size_t rchunk, double* __restrict__ part) {
+  extern __shared__ double sm[];
+  const int t = threadIdx.x;
+  double* Ws = sm;                    // r x 128
+  double* Vs = sm + (size_t)r * 128;  // 32 x r
+  const size_t j = (size_t)blockIdx.x * 128 + t;
+  const bool act = j < n;
+  for (int k = 0; k < r; ++k) Ws[k * 128 + t] = act ? (double)W[(size_t)k * n + j] : 0.0;
+  const size_t ib = (size_t)blockIdx.y * rchunk;
+  const size_t ie = ib + rchunk < m ? ib + rchunk : m;
+  double acc = 0.0;
+  for (size_t i0 = ib; i0 < ie; i0 += 32) {
+    __syncthreads();
+    for (int e = t; e < 32 * r; e += 128) {
+      const size_t i = i0 + e / r;
+      Vs[e] = i < ie ? (double)V[i * r + (e % r)] : 0.0;
+    }
+    __syncthreads();
+    if (!act) continue;
+    const int cnt = (int)((ie - i0) < 32 ? (ie - i0) : 32);
+    for (int ii = 0; ii < cnt; ++ii) {
+      double pred = 0.0;
+      for (int k = 0; k < r; ++k) pred = madd<EXACT>(pred, Vs[ii * r + k], Ws[k * 128 + t]);
+      const double d = EXACT ? __dsub_rn((double)M[(i0 + ii) * n + j], pred) : (double)M[(i0 + ii) * n + j] - pred;
+      acc = madd<EXACT>(acc, d, d);
+    }
+  }
+  if (act) part[(size_t)blockIdx.y * n + j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic reductions.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// partials[block] = sum over a grid-stride slice of a[e] * b[e] (b may be null => a[e]^2)
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(256) k_dot_partial(const TA* __restrict__ a, const TB* __restrict__ b,
+                                                     size_t count, double* __restrict__ partials) {
+  __shared__ double ws[8];
+  double s = 0.0;
+  for (size_t e = (size_t)blockIdx.x * 256 + threadIdx.x; e < count; e += (size_t)gridDim.x * 256) {
+    const double x = (double)a[e];
+    s = fma(x, b ? (double)b[e] : x, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
+// out[0] = sum_{e<count} v[e] (single block, fixed order).  serial=true sums
+// strictly left to right on one thread (reference order, matrix.cpp:39-40).
+__global__ void k_sum_final(const double* __restrict__ v, size_t count, double* __restrict__ out, int serial) {
+  __shared__ double ws[32];
+  if (serial) {
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (size_t e = 0; e < count; ++e) s += v[e];
+      out[0] = s;
+    }
+    return;
+  }
+  double s = 0.0;
+  for (size_t e = threadIdx.x; e < count; e += blockDim.x) s += v[e];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    out[0] = t;
+  }
+}
+
+// column sums of part[z][j] then the per-column values: out[j] = sum_z part[z][j]
+// (already provided by k_reduce_splits).
+
+// sample record: error = sqrt(max(e2, 0)) with e2 assembled from scalars:
+//   gram:   e2 = s[0] - 2 s[1] + s[2]   (||M||^2, <C,W>, <D,WW^T>)
+//   direct: e2 = s[0]
+struct SampleRec {
+  double error;
+  unsigned long long t_ns;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_write_sample(const double* __restrict__ s, int gram, SampleRec* __restrict__ out) {
+  double e2 = gram ? (s[0] - 2.0 * s[1] + s[2]) : s[0];
+  out->error = sqrt(e2 > 0.0 ? e2 : 0.0);
+  out->t_ns = globaltimer();
+}
+
+__global__ void k_timestamp(unsigned long long* out) { *out = globaltimer(); }
+
+// ---------------------------------------------------------------------------
+// Transfer operators (transfer.cpp:17-33): Y[o,:] = sum_e w_e X[idx_e,:],
+// entries in the reference's order, unfused multiply-add, fp64 math.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restrict__ idx,
+                            const double* __restrict__ wt, const T* __restrict__ X, T* __restrict__ Y,
+                            size_t out_rows, size_t ncols, size_t colblocks) {
+  const size_t o = blockIdx.x / colblocks;
+  const size_t c = (blockIdx.x % colblocks) * blockDim.x + threadIdx.x;
+  if (o >= out_rows || c >= ncols) return;
+  const int eb = rowptr[o], ee = rowptr[o + 1];
+  double y = 0.0;
+  for (int e = eb; e < ee; ++e) y = __dadd_rn(y, __dmul_rn(wt[e], (double)X[(size_t)idx[e] * ncols + c]));
+  Y[o * ncols + c] = to_t<T>(y);
+}
+
+// ---------------------------------------------------------------------------
+// random_init (matrix.cpp:51-60) on the device: V row-major first, then W,
+// one SplitMix64 stream.  W is this rank's column slice [col0, col0+n_loc)
+// of an n_total-column W, so the stream counter jumps to m*r + k*n_total + j.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_random_init(T* __restrict__ V, T* __restrict__ W, size_t m, size_t r, size_t n_loc,
+                              size_t n_total, size_t col0, uint64_t seed) {
+  const size_t nv = m * r, nw = r * n_loc;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nv + nw;
+       e += (size_t)gridDim.x * blockDim.x) {
+    if (e < nv) {
+      V[e] = to_t<T>(sm64_uniform(seed, e));
+    } else {
+      const size_t f = e - nv, k = f / n_loc, jl = f % n_loc;
+      W[f] = to_t<T>(sm64_uniform(seed, nv + k * n_total + col0 + jl));
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_convert(const double* __restrict__ src, T* __restrict__ dst, size_t count) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x)
+    dst[e] = to_t<T>(src[e]);
+}
+template <typename T>
+__global__ void k_widen(const T* __restrict__ src, double* __restrict__ dst, size_t count) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x)
+    dst[e] = (double)src[e];
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data generator (BASELINE.json configs; spec DESIGN.md section 3).
+// Counter-based SplitMix64 streams: a column slice generates independently.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t gen_key(uint64_t seed, uint64_t tag) {
+  return sm64_mix(seed ^ (0xA0761D6478BD642FULL * tag));
+}
+
+// V0[px][k] = sum_b amp_kb exp(-((ix - ci)^2 + (jx - cj)^2) / (2 sigma^2)), px = jx*h + ix
+__global__ void k_gen_basis(double* __restrict__ V0, size_t h, size_t w, int r, int blobs, double smin,
+                            double smax, uint64_t key) {
+  const size_t total = h * w * (size_t)r;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t px = e / r, k = e % r, jx = px / h, ix = px % h;
+    double s = 0.0;
+    for (int b = 0; b < blobs; ++b) {
+      const uint64_t c0 = 4 * (k * (uint64_t)blobs + b);
+      const double ci = sm64_uniform(key, c0) * (double)h;
+      const double cj = sm64_uniform(key, c0 + 1) * (double)w;
+      const double sg = smin + sm64_uniform(key, c0 + 2) * (smax - smin);
+      const double amp = 0.5 + 0.5 * sm64_uniform(key, c0 + 3);
+      const double di = (double)ix - ci, dj = (double)jx - cj;
+      s += amp * exp(-(di * di + dj * dj) / (2.0 * sg * sg));
+    }
+    V0[px * r + k] = s;
+  }
+}
+
+// W0[k][jl] = Exp(1) with probability 1/2 else 0, global column col0 + jl
+__global__ void k_gen_wcols(double* __restrict__ W0, int r, size_t n_loc, size_t n_total, size_t col0,
+                            uint64_t key) {
+  const size_t total = (size_t)r * n_loc;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t k = e / n_loc, jl = e % n_loc;
+    const uint64_t c = 2 * ((uint64_t)k * n_total + col0 + jl);
+    W0[e] = sm64_uniform(key, c) < 0.5 ? 0.0 : -log1p(-sm64_uniform(key, c + 1));
+  }
+}
+
+// M[px][jl] = max(sum_k V0[px][k] W0[k][jl] + noise, 0).  mode 0: store;
+// mode 1: only block maxima into bmax[]; mode 2: store value / div.
+template <typename T>
+__global__ void __launch_bounds__(128) k_gen_m(T* __restrict__ M, const double* __restrict__ V0,
+                                               const double* __restrict__ W0, size_t m, size_t n_loc, int r,
+                                               size_t col0, uint64_t keyn, int noise_kind, double noise_scale,
+                                               int mode, double div, double* __restrict__ bmax) {
+  extern __shared__ double sm[];
+  double* Ws = sm;                    // r x 128
+  double* Vs = sm + (size_t)r * 128;  // 32 x r
+  __shared__ double red[4];
+  const int t = threadIdx.x;
+  const size_t jl = (size_t)blockIdx.x * 128 + t;
+  const bool act = jl < n_loc;
+  for (int k = 0; k < r; ++k) Ws[k * 128 + t] = act ? W0[(size_t)k * n_loc + jl] : 0.0;
+  const size_t p0 = (size_t)blockIdx.y * 32;
+  for (int e = t; e < 32 * r; e += 128) {
+    const size_t px = p0 + e / r;
+    Vs[e] = px < m ? V0[px * r + (e % r)] : 0.0;
+  }
+  __syncthreads();
+  double mx = 0.0;
+  if (act) {
+    const int cnt = (int)((m - p0) < 32 ? (m - p0) : 32);
+    for (int ii = 0; ii < cnt; ++ii) {
+      const size_t px = p0 + ii;
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s = __dadd_rn(s, __dmul_rn(Vs[ii * r + k], Ws[k * 128 + t]));
+      const uint64_t e = (uint64_t)(col0 + jl) * m + px;
+      double noise;
+      if (noise_kind == 0) {
+        noise = noise_scale * sm64_uniform(keyn, e);
+      } else {
+        const double u1 = sm64_uniform(keyn, 2 * e), u2 = sm64_uniform(keyn, 2 * e + 1);
+        noise = noise_scale * sqrt(-2.0 * log1p(-u1)) * cos(6.283185307179586 * u2);
+      }
+      const double v0 = __dadd_rn(s, noise);
+      const double v = v0 > 0.0 ? v0 : 0.0;
+      if (mode == 0) M[px * n_loc + jl] = to_t<T>(v);
+      else if (mode == 2) M[px * n_loc + jl] = to_t<T>(v / div);
+      else mx = v > mx ? v : mx;
+    }
+  }
+  if (mode == 1) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0) red[t >> 5] = mx;
+    __syncthreads();
+    if (t == 0) bmax[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  }
+}
+
+__global__ void k_max_final(const double* __restrict__ v, size_t count, double* __restrict__ out) {
+  __shared__ double ws[32];
+  double s = 0.0;
+  for (size_t e = threadIdx.x; e < count; e += blockDim.x) s = fmax(s, v[e]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, ws[w]);
+    out[0] = t;
+  }
+}
+
+// validation: flag |= 1 if any entry is negative or non-finite
+template <typename T>
+__global__ void k_validate(const T* __restrict__ M, size_t count, int* __restrict__ flag) {
+  bool bad = false;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    const double v = (double)M[e];
+    bad |= !(v >= 0.0) || !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+}  // namespace mlb

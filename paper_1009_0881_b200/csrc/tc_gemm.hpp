@@ -1,0 +1,27 @@
+// tc_gemm.hpp -- tcgen05 (5th-gen tensor core) 3xTF32 kernels for the two
+// M-streaming products at fp32 storage (tc_gemm.cu):
+//   A (m x r, fp64) = M (m x n) W^T      and      C (r x n, fp64) = V^T M.
+#pragma once
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace mlb {
+
+class TcGemm {
+ public:
+  virtual ~TcGemm() = default;
+  virtual bool active() const = 0;
+  virtual void mwt(const float* M, const float* W, size_t m, size_t n, size_t r, double* A, cudaStream_t s,
+                   long* launches) = 0;
+  virtual void vtm(const float* V, const float* M, size_t m, size_t n, size_t r, double* C, cudaStream_t s,
+                   long* launches) = 0;
+  // fp64 instantiations exist only to satisfy the templated engine; never active
+  void mwt(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
+  void vtm(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
+};
+
+// allowed: fp32 storage and not forced to SIMT; forced: the caller demanded
+// tcgen05 (throws if unavailable).
+TcGemm* make_tc_gemm(bool allowed, bool forced);
+
+}  // namespace mlb
