@@ -169,6 +169,11 @@ int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps);
 int mlnmf_session_sync(mlnmf_session* s);
 int mlnmf_session_error(mlnmf_session* s, double* out); /* ||M - VW||_F at level 0, all ranks */
 int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out); /* ||M_level||_F^2, all ranks */
+/* The two M-streaming products at level 0 with the current factors, through
+ * the active implementation: A = M W^T (m x r) and C = V^T M (r x n_local),
+ * fp64 host buffers (either may be NULL).  Note: A is this rank's partial
+ * (not allreduced). */
+int mlnmf_session_products(mlnmf_session* s, double* A, double* C);
 /* copy this rank's level-0 M (m x n_local) to a host buffer */
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
 int mlnmf_session_set_profiling(mlnmf_session* s, int on);

@@ -213,6 +213,7 @@ _proto("mlnmf_session_sync", C.c_int, _vp)
 _proto("mlnmf_session_error", C.c_int, _vp, _dp)
 _proto("mlnmf_session_norm2", C.c_int, _vp, _sz, _dp)
 _proto("mlnmf_session_export_data", C.c_int, _vp, _vp, C.c_int)
+_proto("mlnmf_session_products", C.c_int, _vp, _dp, _dp)
 _proto("mlnmf_session_set_profiling", C.c_int, _vp, C.c_int)
 _proto("mlnmf_session_kernel_times", C.c_int, _vp, _dp, _lp, _dp, _lp)
 _proto("mlnmf_session_launches", C.c_long, _vp)
@@ -651,6 +652,14 @@ class Session:
         out = C.c_double()
         _check(_lib.mlnmf_session_norm2(self._h, level, C.byref(out)))
         return out.value
+
+    def products(self):
+        """(A, C) = (M W^T, V^T M) at level 0 with the current factors, through
+        the active implementation (SIMT or tcgen05); this rank's partials."""
+        A = np.zeros((self.m, self.r))
+        Cm = np.zeros((self.r, self.n_local))
+        _check(_lib.mlnmf_session_products(self._h, _d(A), _d(Cm)))
+        return A, Cm
 
     def export_data(self, ptr: Optional[int] = None):
         """Level-0 M (m x n_local) to a host buffer (numpy array if ptr is None)."""

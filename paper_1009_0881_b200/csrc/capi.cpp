@@ -357,6 +357,10 @@ int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out) {
   return guard([&] { *out = s->e->norm2(level); });
 }
 
+int mlnmf_session_products(mlnmf_session* s, double* A, double* C) {
+  return guard([&] { s->e->products(A, C); });
+}
+
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype) {
   return guard([&] { s->e->export_data(M_local, host_dtype); });
 }

@@ -187,6 +187,11 @@ struct Engine::Impl {
   double* A() { return AB.as<double>(); }
   double* B() { return AB.as<double>() + e->lv_[0].m * e->r_; }
 
+  // tensor path for a level of m rows (fp32 storage, supported shape, policy;
+  // a forced tensor path still serves unsupported levels -- e.g. coarse
+  // grids below one 128-row tile -- with the SIMT kernels)
+  bool use_tc(size_t m) const { return tc && tc->wants(m, e->n_loc_, e->r_); }
+
   // A = M_l W^T (the first M pass), timed when profiling.
   template <typename T>
   void product_mwt(size_t l) {
@@ -196,7 +201,7 @@ struct Engine::Impl {
       evp = {ev(), ev()};
       CK(cudaEventRecord(evp.first, s));
     }
-    if (tc && tc->active())
+    if (use_tc(L.m))
       tc->mwt(static_cast<const T*>(L.M), W.as<T>(), L.m, e->n_loc_, e->r_, A(), s, &e->launches_);
     else
       gemm_abt<T>(static_cast<const T*>(L.M), W.as<T>(), L.m, e->r_, e->n_loc_, A());
@@ -214,7 +219,7 @@ struct Engine::Impl {
       evp = {ev(), ev()};
       CK(cudaEventRecord(evp.first, s));
     }
-    if (tc && tc->active())
+    if (use_tc(L.m))
       tc->vtm(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->n_loc_, e->r_, Cb.as<double>(), s,
               &e->launches_);
     else
@@ -467,7 +472,9 @@ Engine::~Engine() {
   delete impl_;
 }
 
-bool Engine::tc_active() const { return impl_->tc && impl_->tc->active(); }
+bool Engine::tc_active() const {
+  return impl_->tc && !lv_.empty() && r_ > 0 && impl_->tc->wants(lv_[0].m, n_loc_, r_);
+}
 bool Engine::gram_error() const {
   if (opt_.error_mode == 1) return true;
   if (opt_.error_mode == 2) return false;
@@ -717,6 +724,21 @@ void Engine::export_data(void* M_host, int host_dtype) {
   const size_t count = lv_[0].m * n_loc_, es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
   if (hs != es) throw std::invalid_argument("export_data: host dtype must match the storage dtype");
   CK(cudaMemcpyAsync(M_host, lv_[0].M, count * es, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+}
+
+void Engine::products(double* A, double* C) {
+  if (lv_.empty() || r_ == 0) throw std::invalid_argument("products: no data or factors");
+  if (opt_.dtype == 0) {
+    impl_->product_mwt<float>(0);
+    impl_->product_vtm<float>(0);
+  } else {
+    impl_->product_mwt<double>(0);
+    impl_->product_vtm<double>(0);
+  }
+  impl_->CD_valid = false;
+  if (A) CK(cudaMemcpyAsync(A, impl_->A(), lv_[0].m * r_ * 8, cudaMemcpyDeviceToHost, impl_->s));
+  if (C) CK(cudaMemcpyAsync(C, impl_->Cb.p, r_ * n_loc_ * 8, cudaMemcpyDeviceToHost, impl_->s));
   CK(cudaStreamSynchronize(impl_->s));
 }
 

@@ -92,6 +92,9 @@ class Engine {
   void set_factors(size_t l, const void* V, const void* W, int host_dtype, size_t r);  // V at level l, W
   void get_factors(size_t l, void* V, void* W, int host_dtype);
   void export_data(void* M_host, int host_dtype);  // level-0 M to a host buffer
+  // the two M-streaming products at level 0 with the current factors, through
+  // the active path: A = M W^T (m x r), C = V^T M (r x n_loc), fp64 to host
+  void products(double* A, double* C);
   void restrict_V(size_t l);  // V_{l+1} = R_l V_l   (multilevel.cpp:39)
   void prolong_V(size_t l);   // V_l = P_l V_{l+1}   (multilevel.cpp:41)
 

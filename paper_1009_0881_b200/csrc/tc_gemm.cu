@@ -1,16 +1,576 @@
-// tc_gemm.cu -- tcgen05 3xTF32 M-streaming products (placeholder until the
-// kernels land: the engine falls back to the SIMT fp64-accumulating GEMMs;
-// forcing the tensor path fails loudly).
+// tc_gemm.cu -- the two M-streaming products on the 5th-generation tensor
+// cores (tcgen05, sm_100a), fp32 storage, 3xTF32 precision:
+//
+//   product 1 (TRANS = false):  A (m x r)  = M (m x n) . W^T       (solvers.cpp:82,105,252)
+//   product 2 (TRANS = true):   C^T (n x r) = M^T (n x m) . V      (solvers.cpp:91,124,273)
+//
+// Both stream M from HBM exactly once.  MMA operand roles (M = 128 rows of the
+// MMA, N = 2 r_pad, K = 8 per tcgen05.mma, kind::tf32):
+//   A operand: a 128 x 32 slice of M (product 1) or of M^T (product 2), split
+//              by the converter warps into tf32 hi = rna(x) and lo = rna(x - hi)
+//              and written straight into TMEM (tcgen05.st) -- no shared-memory
+//              round trip, so the MMA's A reads never touch shared memory.
+//   B operand: [F_hi ; F_lo] (2 r_pad x 32, K-major, SWIZZLE_128B) where F is
+//              W (product 1) or V^T (product 2), pre-split once per step by a
+//              tiny kernel and brought in by TMA next to the M slice.
+// Per K-step two MMAs:  D[:, 0:2r) += A_hi [F_hi;F_lo]^T   (N = 2 r_pad)
+//                       D[:, 0:r)  += A_lo  F_hi^T          (N = r_pad)
+// so D[:, 0:r) + D[:, r:2r) = A_hi F_hi + A_hi F_lo + A_lo F_hi (3xTF32).
+// fp32 TMEM accumulation is limited to windows of kWindow chunks; the
+// epilogue warps drain each window into fp64 registers (double-buffered
+// accumulators), and write fp64 split-K partials that a deterministic reduce
+// sums in fixed order.
+//
+// Warp roles (448 threads, one persistent CTA per SM, 512 TMEM columns):
+//   warp 0: TMA producer      warp 1: TMEM allocator + MMA issuer
+//   warps 2-5: converters     warps 6-13: epilogue (lane quarter x column half)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
 #include <stdexcept>
+#include <string>
 
 #include "tc_gemm.hpp"
 
 namespace mlb {
+namespace tc {
+
+constexpr int kStages = 6;        // smem pipeline depth (M slice + B slice per stage)
+constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
+constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
+constexpr int kWindow = 64;       // chunks per fp32 accumulation window (2048 K)
+constexpr int kThreads = 448;
+constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
+
+#define TC_CK(x)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess)                                                                        \
+      throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e_) + " at " +    \
+                               __FILE__ + ":" + std::to_string(__LINE__));                        \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// PTX helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+// Bounded wait: a pipeline bug traps (kernel error) after ~2^34 cycles instead
+// of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  do {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::tf32, M = 128
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+#define TC_REG32(v) \
+  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), \
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),          \
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),           \
+      "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+#define TC_OREG32(v)                                                                                           \
+  "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), \
+      "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),  \
+      "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), \
+      "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      TC_REG32(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : TC_OREG32(v)
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row atoms of
+// 128 B (SBO = 1024 B), Blackwell version bit.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;       // SBO
+  d |= (uint64_t)1u << 46;                 // version = 1 (sm_100)
+  d |= (uint64_t)2u << 61;                 // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+struct Params {
+  int rows;        // MMA-M extent: m (product 1) or n (product 2)
+  int kdim;        // K extent: n (product 1) or m (product 2)
+  int r;           // true rank
+  int rp;          // padded rank (multiple of 16, <= 64)
+  int tiles;       // ceil(rows / 128)
+  int splits;      // split-K factor
+  int chunks_per_split;
+  int nchunks;     // ceil(kdim / 32)
+  double* part;    // [splits][...] fp64 partial outputs
+};
+
+// ----------------------------------------------------------------------------
+// The persistent warp-specialised kernel
+// ----------------------------------------------------------------------------
+template <bool TRANS>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
+                 const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // carve: [stages x M slice 16 KB][stages x B slice 2rp*128 B][barriers]
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int b_bytes = 2 * p.rp * 128;
+  unsigned char* sm_m = base;
+  unsigned char* sm_b = base + kStages * kMTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kStages * b_bytes);
+  uint64_t* full = bars;                   // [kStages]
+  uint64_t* empty = full + kStages;        // [kStages]
+  uint64_t* sfull = empty + kStages;       // [kSlots]
+  uint64_t* sempty = sfull + kSlots;       // [kSlots]
+  uint64_t* afull = sempty + kSlots;       // [2]
+  uint64_t* aempty = afull + 2;            // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int acc_cols = 2 * p.rp;
+  const int stg_col0 = 2 * acc_cols;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 4 + 1);  // 4 converter warps + MMA commit
+    }
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(smem_u32(&sfull[i]), 4);
+      mbar_init(smem_u32(&sempty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&afull[i]), 1);
+      mbar_init(smem_u32(&aempty[i]), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_m)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  const int total_units = p.tiles * p.splits;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int tile = u % p.tiles, split = u / p.tiles;
+        const int c_beg = split * p.chunks_per_split;
+        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+        for (int c = c_beg; c < c_end; ++c) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_expect_tx(fb, kMTileBytes + b_bytes);
+          if (!TRANS)
+            tma_load_2d(smem_u32(sm_m + stage * kMTileBytes), &map_m, c * kChunk, tile * 128, fb);
+          else
+            tma_load_2d(smem_u32(sm_m + stage * kMTileBytes), &map_m, tile * 128, c * kChunk, fb);
+          tma_load_2d(smem_u32(sm_b + stage * b_bytes), &map_b, c * kChunk, 0, fb);
+          if (++stage == kStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, sphase = 0, aphase = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int split = u / p.tiles;
+        const int c_beg = split * p.chunks_per_split;
+        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+        for (int c = c_beg; c < c_end; ++c) {
+          const int wpos = (c - c_beg) % kWindow;
+          const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
+          if (wpos == 0) {
+            mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
+          }
+          mbar_wait(smem_u32(&sfull[slot]), sphase);
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * acc_cols;
+          const uint32_t a_hi = tmem + stg_col0 + slot * 64, a_lo = a_hi + 32;
+          const uint32_t bsm = smem_u32(sm_b + stage * b_bytes);
+#pragma unroll
+          for (int kk = 0; kk < kChunk / 8; ++kk) {
+            const uint64_t bd = sdesc_sw128(bsm + kk * 32);
+            mma_ts(d, a_hi + kk * 8, bd, id_full, (wpos > 0 || kk > 0) ? 1u : 0u);
+            mma_ts(d, a_lo + kk * 8, bd, id_hi, 1u);
+          }
+          tc_commit(smem_u32(&empty[stage]));
+          tc_commit(smem_u32(&sempty[slot]));
+          if (last_in_window) {
+            tc_commit(smem_u32(&afull[acc]));
+            if (++acc == 2) acc = 0, aphase ^= 1;
+          }
+          if (++stage == kStages) stage = 0, phase ^= 1;
+          if (++slot == kSlots) slot = 0, sphase ^= 1;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, sphase = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int split = u / p.tiles;
+      const int c_beg = split * p.chunks_per_split;
+      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+      for (int c = c_beg; c < c_end; ++c) {
+        mbar_wait(smem_u32(&full[stage]), phase);
+        mbar_wait(smem_u32(&sempty[slot]), sphase ^ 1);
+        tc_fence_after();
+        float x[32];
+        const unsigned char* tile = sm_m + stage * kMTileBytes;
+        if (!TRANS) {
+          // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
+          const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = rp[j ^ (row & 7)];
+            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+          }
+        } else {
+          // column `row` of a 32 x 128 (k x j) tile, no swizzle
+          const float* cp = reinterpret_cast<const float*>(tile) + row;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) x[k] = cp[k * 128];
+        }
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          hi[k] = tf32_rna(x[k]);
+          lo[k] = tf32_rna(x[k] - __uint_as_float(hi[k]));
+        }
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + stg_col0 + slot * 64;
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(&sfull[slot]));
+          mbar_arrive(smem_u32(&empty[stage]));
+        }
+        if (++stage == kStages) stage = 0, phase ^= 1;
+        if (++slot == kSlots) slot = 0, sphase ^= 1;
+      }
+    }
+  } else {
+    // ======================= epilogue: fp32 windows -> fp64 =======================
+    // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int cb = ((warp - 6) >> 2) * 32;
+    const bool live = cb < p.rp;
+    int acc = 0;
+    uint32_t aphase = 0;
+    double sum[32];
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int tile = u % p.tiles, split = u / p.tiles;
+      const int c_beg = split * p.chunks_per_split;
+      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) sum[k] = 0.0;
+      for (int c0 = c_beg; c0 < c_end; c0 += kWindow) {
+        mbar_wait(smem_u32(&afull[acc]), aphase);
+        tc_fence_after();
+        if (live) {
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * acc_cols + cb;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // hi part, then lo part of the stacked accumulator
+            uint32_t v[32];
+            tmem_ld32(ta + h * p.rp, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) sum[k] += (double)__uint_as_float(v[k]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&aempty[acc]));
+        if (++acc == 2) acc = 0, aphase ^= 1;
+      }
+      const int gi = tile * 128 + row;
+      if (live && gi < p.rows) {
+        if (!TRANS) {
+          double* out = p.part + (size_t)split * p.rows * p.r + (size_t)gi * p.r + cb;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (cb + k < p.r) out[k] = sum[k];
+        } else {
+          double* out = p.part + (size_t)split * p.r * p.rows + (size_t)cb * p.rows + gi;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (cb + k < p.r) out[(size_t)k * p.rows] = sum[k];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+// F (rows x ld, row-major, rows <= r) -> S (2 rp x K): S[k] = rna(F[k]),
+// S[rp + k] = rna(F[k] - S[k]); padding rows zero.  trans: F is K x r
+// (V, row-major) and row k of S is column k of F.
+__global__ void k_split_factor(const float* __restrict__ F, float* __restrict__ S, int r, int rp, size_t K,
+                               int trans) {
+  const size_t total = (size_t)rp * K;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t k = e / K, j = e % K;
+    float hi = 0.f, lo = 0.f;
+    if ((int)k < r) {
+      const float x = trans ? F[j * r + k] : F[k * K + j];
+      const uint32_t h = tf32_rna(x);
+      hi = __uint_as_float(h);
+      lo = __uint_as_float(tf32_rna(x - hi));
+    }
+    S[k * K + j] = hi;
+    S[((size_t)rp + k) * K + j] = lo;
+  }
+}
+
+// out[e] = sum_z part[z][e], z ascending (deterministic split-K epilogue)
+__global__ void k_split_reduce(const double* __restrict__ part, size_t count, int splits, double* __restrict__ out) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    double s = part[e];
+    for (int z = 1; z < splits; ++z) s += part[(size_t)z * count + e];
+    out[e] = s;
+  }
+}
+
+}  // namespace tc
+
+// ============================================================================
+// host side
+// ============================================================================
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    TC_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner extent `inner`, outer extent `outer`, row stride
+// inner*4 bytes, box (bi x bo), optional 128-byte swizzle.
+CUtensorMap make_map(const void* ptr, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo, bool swz) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {bi, bo};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
+
+class TcGemmImpl final : public TcGemm {
+ public:
+  explicit TcGemmImpl(bool forced) : forced_(forced) {
+    int dev = 0;
+    TC_CK(cudaGetDevice(&dev));
+    TC_CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+  }
+  ~TcGemmImpl() override {
+    if (split_) cudaFree(split_);
+    if (part_) cudaFree(part_);
+  }
+  bool active() const override { return true; }
+  bool supports(size_t m, size_t n, size_t r) const override {
+    return r >= 1 && r <= 64 && m % 4 == 0 && n % 4 == 0 && m >= 128 && n >= 128 && m < (1u << 31) &&
+           n < (1u << 31);
+  }
+  bool wants(size_t m, size_t n, size_t r) const override {
+    if (!supports(m, n, r)) return false;
+    return forced_ || m * n >= ((size_t)1 << 24);
+  }
+
+  void mwt(const float* M, const float* W, size_t m, size_t n, size_t r, double* A, cudaStream_t s,
+           long* launches) override {
+    run<false>(M, W, m, n, r, A, s, launches);
+  }
+  void vtm(const float* V, const float* M, size_t m, size_t n, size_t r, double* C, cudaStream_t s,
+           long* launches) override {
+    run<true>(M, V, m, n, r, C, s, launches);
+  }
+
+ private:
+  template <bool TRANS>
+  void run(const float* M, const float* F, size_t m, size_t n, size_t r, double* out, cudaStream_t s,
+           long* launches) {
+    if (!supports(m, n, r)) throw std::invalid_argument("tcgen05 path: unsupported shape");
+    const int rp = (int)cdiv(r, 16) * 16;
+    const size_t K = TRANS ? m : n;        // contraction
+    const size_t rows = TRANS ? n : m;     // MMA-M extent
+    // split factor F -> [F_hi ; F_lo] (2 rp x K)
+    ensure(&split_, &split_bytes_, (size_t)2 * rp * K * 4);
+    {
+      const size_t tot = (size_t)rp * K;
+      const unsigned g = (unsigned)std::min<size_t>(cdiv(tot, 256), 16384);
+      tc::k_split_factor<<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
+      TC_CK(cudaGetLastError());
+      ++*launches;
+    }
+    tc::Params p{};
+    p.rows = (int)rows;
+    p.kdim = (int)K;
+    p.r = (int)r;
+    p.rp = rp;
+    p.tiles = (int)cdiv(rows, 128);
+    p.nchunks = (int)cdiv(K, tc::kChunk);
+    // split-K so that there are >= ~8 units per SM (balance)
+    int splits = (int)std::max<size_t>(1, cdiv((size_t)sms_ * 8, p.tiles));
+    splits = std::min(splits, p.nchunks);
+    p.chunks_per_split = (int)cdiv(p.nchunks, splits);
+    p.splits = (int)cdiv(p.nchunks, p.chunks_per_split);
+    const size_t out_count = rows * r;
+    double* dst = out;
+    if (p.splits > 1) {
+      ensure(&part_, &part_bytes_, (size_t)p.splits * out_count * 8);
+      dst = static_cast<double*>(part_);
+    }
+    p.part = dst;
+    const CUtensorMap mm = TRANS ? make_map(M, n, m, 128, tc::kChunk, false) : make_map(M, n, m, tc::kChunk, 128, true);
+    const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, 2 * rp, true);
+    const size_t smem = 1024 + tc::kStages * (tc::kMTileBytes + 2 * rp * 128) + 256;
+    auto kern = tc::k_tc_product<TRANS>;
+    if (!attr_set_[TRANS ? 1 : 0]) {
+      TC_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set_[TRANS ? 1 : 0] = true;
+    }
+    const int units = p.tiles * p.splits;
+    const int grid = std::min(units, sms_);
+    kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
+    TC_CK(cudaGetLastError());
+    ++*launches;
+    if (p.splits > 1) {
+      const unsigned g = (unsigned)std::min<size_t>(cdiv(out_count, 256), 4096);
+      tc::k_split_reduce<<<g, 256, 0, s>>>(static_cast<const double*>(part_), out_count, p.splits, out);
+      TC_CK(cudaGetLastError());
+      ++*launches;
+    }
+  }
+
+  static void ensure(void** p, size_t* have, size_t need) {
+    if (need <= *have) return;
+    if (*p) TC_CK(cudaFree(*p));
+    *p = nullptr;
+    TC_CK(cudaMalloc(p, need));
+    *have = need;
+  }
+
+  bool forced_;
+  int sms_ = 148;
+  void* split_ = nullptr;
+  size_t split_bytes_ = 0;
+  void* part_ = nullptr;
+  size_t part_bytes_ = 0;
+  bool attr_set_[2] = {false, false};
+};
+
+}  // namespace
 
 TcGemm* make_tc_gemm(bool allowed, bool forced) {
-  (void)allowed;
-  if (forced) throw std::invalid_argument("tcgen05 path not available in this build");
-  return nullptr;
+  if (!allowed) {
+    if (forced) throw std::invalid_argument("tcgen05 path needs fp32 storage");
+    return nullptr;
+  }
+  return new TcGemmImpl(forced);
 }
 
 }  // namespace mlb

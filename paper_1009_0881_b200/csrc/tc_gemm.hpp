@@ -11,17 +11,21 @@ class TcGemm {
  public:
   virtual ~TcGemm() = default;
   virtual bool active() const = 0;
+  // shape supported by the kernels (r <= 64, 16-byte aligned rows)
+  virtual bool supports(size_t m, size_t n, size_t r) const = 0;
+  // policy: use the tensor path for this level (forced, or large enough)
+  virtual bool wants(size_t m, size_t n, size_t r) const = 0;
   virtual void mwt(const float* M, const float* W, size_t m, size_t n, size_t r, double* A, cudaStream_t s,
                    long* launches) = 0;
   virtual void vtm(const float* V, const float* M, size_t m, size_t n, size_t r, double* C, cudaStream_t s,
                    long* launches) = 0;
-  // fp64 instantiations exist only to satisfy the templated engine; never active
+  // fp64 storage never takes the tensor path (kept for the templated engine)
   void mwt(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
   void vtm(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
 };
 
 // allowed: fp32 storage and not forced to SIMT; forced: the caller demanded
-// tcgen05 (throws if unavailable).
+// tcgen05 for every supported shape.
 TcGemm* make_tc_gemm(bool allowed, bool forced);
 
 }  // namespace mlb

@@ -1,0 +1,82 @@
+"""GPU: the tcgen05 3xTF32 M-streaming products against fp64 references.
+
+A = M W^T and C = V^T M from fp32 storage: the tensor-core path must agree
+with an fp64 numpy product of the same fp32 inputs to 3xTF32 accuracy
+(relative Frobenius error <= 2e-6 stated here; measured ~1e-7), on aligned and
+ragged shapes, r in {16..64}; and whole fp32 runs through the tensor path must
+track the fp64 oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-6
+
+
+def relnorm(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("m,n,r", [
+    (1024, 2048, 64), (1024, 2048, 20), (4096, 1024, 40), (1028, 1500, 49),
+    (256, 16384, 64), (16384, 256, 64), (640, 640, 16), (2052, 4100, 33),
+])
+def test_tc_products(P, gpu, m, n, r):
+    rng = np.random.default_rng(m * 7 + n + r)
+    M = rng.random((m, n)).astype(np.float32)
+    M[rng.random((m, n)) < 0.1] = 0.0
+    V = rng.random((m, r)).astype(np.float32)
+    W = (rng.random((r, n)) * 3).astype(np.float32)
+    M64, V64, W64 = M.astype(np.float64), V.astype(np.float64), W.astype(np.float64)
+    A_ref, C_ref = M64 @ W64.T, V64.T @ M64
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V64, W64)
+        assert s.tc_active
+        A, C = s.products()
+    ea, ec = relnorm(A, A_ref), relnorm(C, C_ref)
+    assert ea < TOL and ec < TOL, (ea, ec)
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_SIMT) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V64, W64)
+        assert not s.tc_active
+        A2, C2 = s.products()
+    assert relnorm(A2, A_ref) < 1e-13 and relnorm(C2, C_ref) < 1e-13
+
+
+def test_tc_deterministic(P, gpu):
+    rng = np.random.default_rng(5)
+    M = rng.random((2048, 4096)).astype(np.float32)
+    V, W = rng.random((2048, 64)), rng.random((64, 4096))
+    outs = []
+    for _ in range(2):
+        with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+            s.set_data(M, P.ImageGrid(2048, 1))
+            s.set_factors(V, W)
+            outs.append(s.products())
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def round32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("cycle", ["none", "fmg"])
+def test_tc_run_tracks_oracle(P, restated, gpu, cycle):
+    """Config-0 generator at a tensor-path size (32x32 grid, n = 4096, r = 20,
+    HALS, work:30): the fp32 tcgen05 run stays within 2e-5 of the fp64 oracle
+    fed the fp32-rounded inputs, with an identical schedule."""
+    M = oracle.generate_config(0, n=4096, restated=restated).astype(np.float32)
+    V0, W0 = restated.random_init(1024, 4096, 20, 0)
+    L = 1 if cycle == "none" else 3
+    _, _, to = restated.run_cycle_on(round32(M), 32, 32, L, L, round32(V0), round32(W0), "hals", cycle, 30.0, 1)
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M, P.ImageGrid(32, 32))
+        tg = s.run_configuration(3, "hals", cycle, 20, 0, 30.0, 1)
+        assert s.tc_active
+    assert np.array_equal(tg.level, to.level) and np.array_equal(tg.work_units, to.work)
+    dev = float(np.max(np.abs(tg.error - to.error) / to.error))
+    assert dev < 2e-5, dev
