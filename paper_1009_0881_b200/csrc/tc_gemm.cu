@@ -21,9 +21,10 @@
 // accumulators), and write fp64 split-K partials that a deterministic reduce
 // sums in fixed order.
 //
-// Warp roles (448 threads, one persistent CTA per SM, 512 TMEM columns):
+// Warp roles (576 threads, one persistent CTA per SM, 512 TMEM columns):
 //   warp 0: TMA producer      warp 1: TMEM allocator + MMA issuer
-//   warps 2-5: converters     warps 6-13: epilogue (lane quarter x column half)
+//   warps 2-9: converters (two groups of 4, alternate chunks)
+//   warps 10-17: epilogue (lane quarter x column half)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -39,10 +40,11 @@ namespace mlb {
 namespace tc {
 
 constexpr int kStages = 6;        // smem pipeline depth (M slice + B slice per stage)
-constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
+constexpr int kSlots = 6;         // TMEM staging slots (hi|lo, 64 columns each)
 constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
 constexpr int kWindow = 64;       // chunks per fp32 accumulation window (2048 K)
-constexpr int kThreads = 448;
+constexpr int kConvGroups = 2;    // converter groups of 4 warps (alternate chunks)
+constexpr int kThreads = (2 + 4 * kConvGroups + 8) * 32;
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
 
 #define TC_CK(x)                                                                                  \
@@ -92,15 +94,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// warp-wide call; one elected lane commits
 __device__ __forceinline__ void tc_commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(mbar)
+      : "memory");
 }
-// D[tmem] (+)= A[tmem] . B[smem]^T, kind::tf32, M = 128
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::tf32, M = 128; warp-wide call, one
+// elected lane issues.
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p;\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -126,6 +134,23 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
       "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
       TC_REG32(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -163,6 +188,7 @@ struct Params {
   int splits;      // split-K factor
   int chunks_per_split;
   int nchunks;     // ceil(kdim / 32)
+  int nacc;        // accumulator buffers in TMEM (1 or 2)
   double* part;    // [splits][...] fp64 partial outputs
 };
 
@@ -190,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int acc_cols = 2 * p.rp;
-  const int stg_col0 = 2 * acc_cols;
+  const int stg_col0 = p.nacc * acc_cols;   // accumulators first, then staging
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -219,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (tmem != 0) __trap();  // one CTA per SM owning all 512 columns: base is lane 0, column 0
 
   const int total_units = p.tiles * p.splits;
 
@@ -246,82 +273,94 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
-    if (lane == 0) {
-      const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
-      int stage = 0, slot = 0, acc = 0;
-      uint32_t phase = 0, sphase = 0, aphase = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int split = u / p.tiles;
-        const int c_beg = split * p.chunks_per_split;
-        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-        for (int c = c_beg; c < c_end; ++c) {
-          const int wpos = (c - c_beg) % kWindow;
-          const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
-          if (wpos == 0) {
-            mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
-          }
-          mbar_wait(smem_u32(&sfull[slot]), sphase);
-          mbar_wait(smem_u32(&full[stage]), phase);
-          tc_fence_after();
-          const uint32_t d = tmem + acc * acc_cols;
-          const uint32_t a_hi = tmem + stg_col0 + slot * 64, a_lo = a_hi + 32;
-          const uint32_t bsm = smem_u32(sm_b + stage * b_bytes);
-#pragma unroll
-          for (int kk = 0; kk < kChunk / 8; ++kk) {
-            const uint64_t bd = sdesc_sw128(bsm + kk * 32);
-            mma_ts(d, a_hi + kk * 8, bd, id_full, (wpos > 0 || kk > 0) ? 1u : 0u);
-            mma_ts(d, a_lo + kk * 8, bd, id_hi, 1u);
-          }
-          tc_commit(smem_u32(&empty[stage]));
-          tc_commit(smem_u32(&sempty[slot]));
-          if (last_in_window) {
-            tc_commit(smem_u32(&afull[acc]));
-            if (++acc == 2) acc = 0, aphase ^= 1;
-          }
-          if (++stage == kStages) stage = 0, phase ^= 1;
-          if (++slot == kSlots) slot = 0, sphase ^= 1;
-        }
-      }
-    }
-  } else if (warp < 6) {
-    // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, sphase = 0;
+    // The whole warp runs the (warp-uniform) loop so every MMA operand stays in
+    // the uniform datapath; one elected lane issues each tcgen05 instruction.
+    // (A single-lane loop costs ~240 cycles/instruction in R2UR/ELECT
+    // overhead -- tools/mma_probe2.cu measures 2047 MAC/cycle/SM this way.)
+    const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
+    const uint32_t sm_b_u32 = smem_u32(sm_b);
+    int stage = 0, slot = 0, acc = 0;
+    uint32_t phase = 0, sphase = 0, aphase = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int split = u / p.tiles;
       const int c_beg = split * p.chunks_per_split;
       const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
       for (int c = c_beg; c < c_end; ++c) {
+        const int wpos = (c - c_beg) % kWindow;
+        const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
+        if (wpos == 0) mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
+        mbar_wait(smem_u32(&sfull[slot]), sphase);
+        mbar_wait(smem_u32(&full[stage]), phase);
+        tc_fence_after();
+        const uint32_t d = (uint32_t)(acc * acc_cols);  // TMEM base is column 0 (512-column allocation)
+        const uint32_t a_hi = (uint32_t)(stg_col0 + slot * 64), a_lo = a_hi + 32;
+        const uint32_t bsm = sm_b_u32 + (uint32_t)(stage * b_bytes);
+#pragma unroll
+        for (int kk = 0; kk < kChunk / 8; ++kk) {
+          const uint64_t bd = sdesc_sw128(bsm + kk * 32);
+          mma_ts(d, a_hi + kk * 8, bd, id_full, (wpos > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(d, a_lo + kk * 8, bd, id_hi, 1u);
+        }
+        tc_commit(smem_u32(&empty[stage]));
+        tc_commit(smem_u32(&sempty[slot]));
+        if (last_in_window) {
+          tc_commit(smem_u32(&afull[acc]));
+          if (++acc == p.nacc) acc = 0, aphase ^= 1;
+        }
+        __syncwarp();
+        if (++stage == kStages) stage = 0, phase ^= 1;
+        if (++slot == kSlots) slot = 0, sphase ^= 1;
+      }
+    }
+  } else if (warp < 2 + 4 * kConvGroups) {
+    // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
+    // kConvGroups groups of 4 warps take alternate chunks (more chunks in
+    // flight); within a group warp q owns TMEM lane quarter q (access rule).
+    const int grp = (warp - 2) >> 2;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
+    int g = 0;                       // global chunk sequence number
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int split = u / p.tiles;
+      const int c_beg = split * p.chunks_per_split;
+      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+      for (int c = c_beg; c < c_end; ++c, ++g) {
+        if (g % kConvGroups != grp) continue;
+        const int stage = g % kStages, slot = g % kSlots;
+        const uint32_t phase = (uint32_t)(g / kStages) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
         mbar_wait(smem_u32(&full[stage]), phase);
         mbar_wait(smem_u32(&sempty[slot]), sphase ^ 1);
         tc_fence_after();
-        float x[32];
         const unsigned char* tile = sm_m + stage * kMTileBytes;
-        if (!TRANS) {
-          // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
-          const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 v = rp[j ^ (row & 7)];
-            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-          }
-        } else {
-          // column `row` of a 32 x 128 (k x j) tile, no swizzle
-          const float* cp = reinterpret_cast<const float*>(tile) + row;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) x[k] = cp[k * 128];
-        }
-        uint32_t hi[32], lo[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          hi[k] = tf32_rna(x[k]);
-          lo[k] = tf32_rna(x[k] - __uint_as_float(hi[k]));
-        }
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + stg_col0 + slot * 64;
-        tmem_st32(ta, hi);
-        tmem_st32(ta + 32, lo);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float x[16];
+          if (!TRANS) {
+            // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
+            const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 v = rp[(half * 4 + j) ^ (row & 7)];
+              x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+            }
+          } else {
+            // column `row` of a 32 x 128 (k x j) tile, no swizzle
+            const float* cp = reinterpret_cast<const float*>(tile) + row + half * 16 * 128;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) x[k] = cp[k * 128];
+          }
+          // tf32 round-to-nearest(-away) on the bit pattern (== cvt.rna.tf32):
+          // hi = rna(x), lo = rna(x - hi); x - hi is exact in fp32
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            hi[k] = (__float_as_uint(x[k]) + 0x1000u) & 0xFFFFE000u;
+            lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
+          }
+          tmem_st16(ta + half * 16, hi);
+          tmem_st16(ta + 32 + half * 16, lo);
+        }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -329,8 +368,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&sfull[slot]));
           mbar_arrive(smem_u32(&empty[stage]));
         }
-        if (++stage == kStages) stage = 0, phase ^= 1;
-        if (++slot == kSlots) slot = 0, sphase ^= 1;
       }
     }
   } else {
@@ -338,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int cb = ((warp - 6) >> 2) * 32;
+    const int cb = ((warp - 2 - 4 * kConvGroups) >> 2) * 32;
     const bool live = cb < p.rp;
     int acc = 0;
     uint32_t aphase = 0;
@@ -355,18 +392,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (live) {
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * acc_cols + cb;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // hi part, then lo part of the stacked accumulator
-            uint32_t v[32];
-            tmem_ld32(ta + h * p.rp, v);
+          for (int h = 0; h < 4; ++h) {  // hi part, then lo part of the stacked accumulator, 16 cols each
+            uint32_t v[16];
+            tmem_ld16(ta + (h >> 1) * p.rp + (h & 1) * 16, v);
             tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) sum[k] += (double)__uint_as_float(v[k]);
+            for (int k = 0; k < 16; ++k) sum[(h & 1) * 16 + k] += (double)__uint_as_float(v[k]);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&aempty[acc]));
-        if (++acc == 2) acc = 0, aphase ^= 1;
+        if (++acc == p.nacc) acc = 0, aphase ^= 1;
       }
       const int gi = tile * 128 + row;
       if (live && gi < p.rows) {
@@ -513,6 +550,7 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
+    p.nacc = std::min(2, (512 - tc::kSlots * 64) / (2 * rp));
     // split-K so that there are >= ~8 units per SM (balance)
     int splits = (int)std::max<size_t>(1, cdiv((size_t)sms_ * 8, p.tiles));
     splits = std::min(splits, p.nchunks);

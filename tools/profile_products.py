@@ -1,0 +1,49 @@
+"""Profiling driver: the two M-streaming products at config-4 shape on a
+column slice (m = 65536, r = 64, n = --n), through the active path.
+
+    python tools/profile_products.py --n 32768 --reps 3 [--gemm tc|simt]
+
+Prints per-product device times (CUDA events) and achieved HBM GB/s.
+Intended to be wrapped by ncu (-k regex:k_tc_product).
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "auto"])
+    ap.add_argument("--steps", type=int, default=0, help="also time full HALS steps")
+    a = ap.parse_args()
+    import paper_1009_0881_b200 as P
+    gemm = {"tc": P.GEMM_TCGEN05, "simt": P.GEMM_SIMT, "auto": P.GEMM_AUTO}[a.gemm]
+    with P.Session(dtype=P.F32, gemm_path=gemm) as s:
+        s.generate(4, seed=0, n_total=a.n)
+        s.run_configuration(1, "hals", "none", 64, 0, 0.0, 0)  # random_init
+        s.set_profiling(True)
+        for _ in range(a.reps):
+            s.products()
+        kt = s.kernel_times()
+        mb = 65536 * a.n * 4
+        mw, vt = kt["mwt_ms"] / kt["mwt_n"], kt["vtm_ms"] / kt["vtm_n"]
+        print(f"n={a.n} tc={s.tc_active} A=MW^T {mw:.3f} ms ({mb / mw / 1e6:.0f} GB/s)  "
+              f"C=V^TM {vt:.3f} ms ({mb / vt / 1e6:.0f} GB/s)")
+        if a.steps:
+            s.set_profiling(False)
+            import time
+            s.sync()
+            t = time.perf_counter()
+            s.steps("hals", a.steps)
+            s.sync()
+            print(f"hals step {1e3 * (time.perf_counter() - t) / a.steps:.3f} ms")
+
+
+if __name__ == "__main__":
+    main()
