@@ -39,7 +39,8 @@
 namespace mlb {
 namespace tc {
 
-constexpr int kStages = 6;        // smem pipeline depth (M slice + B slice per stage)
+constexpr int kMStages = 8;       // M-slice ring (TMA -> converters), 16 KB each
+constexpr int kBStages = 4;       // factor-slice ring (TMA -> MMA), 2 r_pad x 128 B each
 constexpr int kSlots = 6;         // TMEM staging slots (hi|lo, 64 columns each)
 constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
 constexpr int kWindow = 64;       // chunks per fp32 accumulation window (2048 K)
@@ -72,19 +73,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
 }
 // Bounded wait: a pipeline bug traps (kernel error) after ~2^34 cycles instead
 // of hanging the GPU.
+__device__ __forceinline__ uint32_t mbar_try(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok;
+}
+template <int SLEEP_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-  uint32_t ok = 0;
+  if (mbar_try(a, parity)) return;
   const long long t0 = clock64();
-  do {
-    if (clock64() - t0 > (1ll << 34)) __trap();
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
+  for (uint32_t i = 1;; ++i) {
+    if (SLEEP_NS) __nanosleep(SLEEP_NS);  // off-critical-path waiters yield issue slots
+    if (mbar_try(a, parity)) return;
+    if ((i & 255) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
@@ -200,18 +208,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
                  const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // carve: [stages x M slice 16 KB][stages x B slice 2rp*128 B][barriers]
+  // carve: [M ring: kMStages x 16 KB][B ring: kBStages x 2rp*128 B][barriers]
+  // The rings are separate so an M slice is released as soon as the
+  // converters have read it (more HBM bytes in flight), while a factor slice
+  // lives until the MMAs reading it complete.
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_bytes = 2 * p.rp * 128;
   unsigned char* sm_m = base;
-  unsigned char* sm_b = base + kStages * kMTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kStages * b_bytes);
-  uint64_t* full = bars;                   // [kStages]
-  uint64_t* empty = full + kStages;        // [kStages]
-  uint64_t* sfull = empty + kStages;       // [kSlots]
-  uint64_t* sempty = sfull + kSlots;       // [kSlots]
-  uint64_t* afull = sempty + kSlots;       // [2]
-  uint64_t* aempty = afull + 2;            // [2]
+  unsigned char* sm_b = base + kMStages * kMTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * b_bytes);
+  uint64_t* mfull = bars;                  // [kMStages]  TMA -> converters
+  uint64_t* mempty = mfull + kMStages;     // [kMStages]  converters -> TMA
+  uint64_t* bfull = mempty + kMStages;     // [kBStages]  TMA -> MMA
+  uint64_t* bempty = bfull + kBStages;     // [kBStages]  MMA commit -> TMA
+  uint64_t* sfull = bempty + kBStages;     // [kSlots]    converters -> MMA
+  uint64_t* sempty = sfull + kSlots;       // [kSlots]    MMA commit -> converters
+  uint64_t* afull = sempty + kSlots;       // [2]         MMA commit -> epilogue
+  uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -219,9 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stg_col0 = p.nacc * acc_cols;   // accumulators first, then staging
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(smem_u32(&full[i]), 1);
-      mbar_init(smem_u32(&empty[i]), 4 + 1);  // 4 converter warps + MMA commit
+    for (int i = 0; i < kMStages; ++i) {
+      mbar_init(smem_u32(&mfull[i]), 1);
+      mbar_init(smem_u32(&mempty[i]), 4);  // the 4 warps of the converting group
+    }
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init(smem_u32(&bfull[i]), 1);
+      mbar_init(smem_u32(&bempty[i]), 1);
     }
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(smem_u32(&sfull[i]), 4);
@@ -252,22 +269,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
+      int ms = 0, bs = 0;
+      uint32_t mph = 0, bph = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
         for (int c = c_beg; c < c_end; ++c) {
-          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t fb = smem_u32(&full[stage]);
-          mbar_expect_tx(fb, kMTileBytes + b_bytes);
+          mbar_wait(smem_u32(&mempty[ms]), mph ^ 1);
+          const uint32_t fm = smem_u32(&mfull[ms]);
+          mbar_expect_tx(fm, kMTileBytes);
           if (!TRANS)
-            tma_load_2d(smem_u32(sm_m + stage * kMTileBytes), &map_m, c * kChunk, tile * 128, fb);
+            tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, c * kChunk, tile * 128, fm);
           else
-            tma_load_2d(smem_u32(sm_m + stage * kMTileBytes), &map_m, tile * 128, c * kChunk, fb);
-          tma_load_2d(smem_u32(sm_b + stage * b_bytes), &map_b, c * kChunk, 0, fb);
-          if (++stage == kStages) stage = 0, phase ^= 1;
+            tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, tile * 128, c * kChunk, fm);
+          mbar_wait(smem_u32(&bempty[bs]), bph ^ 1);
+          const uint32_t fb = smem_u32(&bfull[bs]);
+          mbar_expect_tx(fb, b_bytes);
+          tma_load_2d(smem_u32(sm_b + bs * b_bytes), &map_b, c * kChunk, 0, fb);
+          if (++ms == kMStages) ms = 0, mph ^= 1;
+          if (++bs == kBStages) bs = 0, bph ^= 1;
         }
       }
     }
@@ -279,8 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // overhead -- tools/mma_probe2.cu measures 2047 MAC/cycle/SM this way.)
     const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
     const uint32_t sm_b_u32 = smem_u32(sm_b);
-    int stage = 0, slot = 0, acc = 0;
-    uint32_t phase = 0, sphase = 0, aphase = 0;
+    int bs = 0, slot = 0, acc = 0;
+    uint32_t bphase = 0, sphase = 0, aphase = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int split = u / p.tiles;
       const int c_beg = split * p.chunks_per_split;
@@ -290,25 +311,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
         if (wpos == 0) mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
         mbar_wait(smem_u32(&sfull[slot]), sphase);
-        mbar_wait(smem_u32(&full[stage]), phase);
+        mbar_wait(smem_u32(&bfull[bs]), bphase);
         tc_fence_after();
         const uint32_t d = (uint32_t)(acc * acc_cols);  // TMEM base is column 0 (512-column allocation)
         const uint32_t a_hi = (uint32_t)(stg_col0 + slot * 64), a_lo = a_hi + 32;
-        const uint32_t bsm = sm_b_u32 + (uint32_t)(stage * b_bytes);
+        const uint32_t bsm = sm_b_u32 + (uint32_t)(bs * b_bytes);
 #pragma unroll
         for (int kk = 0; kk < kChunk / 8; ++kk) {
           const uint64_t bd = sdesc_sw128(bsm + kk * 32);
           mma_ts(d, a_hi + kk * 8, bd, id_full, (wpos > 0 || kk > 0) ? 1u : 0u);
           mma_ts(d, a_lo + kk * 8, bd, id_hi, 1u);
         }
-        tc_commit(smem_u32(&empty[stage]));
+        tc_commit(smem_u32(&bempty[bs]));
         tc_commit(smem_u32(&sempty[slot]));
         if (last_in_window) {
           tc_commit(smem_u32(&afull[acc]));
           if (++acc == p.nacc) acc = 0, aphase ^= 1;
         }
         __syncwarp();
-        if (++stage == kStages) stage = 0, phase ^= 1;
+        if (++bs == kBStages) bs = 0, bphase ^= 1;
         if (++slot == kSlots) slot = 0, sphase ^= 1;
       }
     }
@@ -326,37 +347,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
       for (int c = c_beg; c < c_end; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
-        const int stage = g % kStages, slot = g % kSlots;
-        const uint32_t phase = (uint32_t)(g / kStages) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
-        mbar_wait(smem_u32(&full[stage]), phase);
+        const int ms = g % kMStages, slot = g % kSlots;
+        const uint32_t mph = (uint32_t)(g / kMStages) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
+        mbar_wait(smem_u32(&mfull[ms]), mph);
+        // the thread's 32 values of this chunk (its MMA row / TMEM lane)
+        float x[32];
+        const unsigned char* tile = sm_m + ms * kMTileBytes;
+        if (!TRANS) {
+          // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
+          const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = rp[j ^ (row & 7)];
+            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+          }
+        } else {
+          // column `row` of a 32 x 128 (k x j) tile, no swizzle
+          const float* cp = reinterpret_cast<const float*>(tile) + row;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) x[k] = cp[k * 128];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&mempty[ms]));  // slice consumed: TMA may refill it
         mbar_wait(smem_u32(&sempty[slot]), sphase ^ 1);
         tc_fence_after();
-        const unsigned char* tile = sm_m + stage * kMTileBytes;
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + stg_col0 + slot * 64;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          float x[16];
-          if (!TRANS) {
-            // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
-            const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 v = rp[(half * 4 + j) ^ (row & 7)];
-              x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-            }
-          } else {
-            // column `row` of a 32 x 128 (k x j) tile, no swizzle
-            const float* cp = reinterpret_cast<const float*>(tile) + row + half * 16 * 128;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) x[k] = cp[k * 128];
-          }
           // tf32 round-to-nearest(-away) on the bit pattern (== cvt.rna.tf32):
           // hi = rna(x), lo = rna(x - hi); x - hi is exact in fp32
           uint32_t hi[16], lo[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            hi[k] = (__float_as_uint(x[k]) + 0x1000u) & 0xFFFFE000u;
-            lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
+            const float v = x[half * 16 + k];
+            hi[k] = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
+            lo[k] = (__float_as_uint(v - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
           }
           tmem_st16(ta + half * 16, hi);
           tmem_st16(ta + 32 + half * 16, lo);
@@ -364,10 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(smem_u32(&sfull[slot]));
-          mbar_arrive(smem_u32(&empty[stage]));
-        }
+        if (lane == 0) mbar_arrive(smem_u32(&sfull[slot]));
       }
     }
   } else {
@@ -387,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int k = 0; k < 32; ++k) sum[k] = 0.0;
       for (int c0 = c_beg; c0 < c_end; c0 += kWindow) {
-        mbar_wait(smem_u32(&afull[acc]), aphase);
+        mbar_wait<256>(smem_u32(&afull[acc]), aphase);
         tc_fence_after();
         if (live) {
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * acc_cols + cb;
@@ -565,7 +587,7 @@ class TcGemmImpl final : public TcGemm {
     p.part = dst;
     const CUtensorMap mm = TRANS ? make_map(M, n, m, 128, tc::kChunk, false) : make_map(M, n, m, tc::kChunk, 128, true);
     const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, 2 * rp, true);
-    const size_t smem = 1024 + tc::kStages * (tc::kMTileBytes + 2 * rp * 128) + 256;
+    const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * 2 * rp * 128 + 512;
     auto kern = tc::k_tc_product<TRANS>;
     if (!attr_set_[TRANS ? 1 : 0]) {
       TC_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -27,6 +27,7 @@ def main():
     with P.Session(dtype=P.F32, gemm_path=gemm) as s:
         s.generate(4, seed=0, n_total=a.n)
         s.run_configuration(1, "hals", "none", 64, 0, 0.0, 0)  # random_init
+        s.products()  # warm-up (buffer allocation)
         s.set_profiling(True)
         for _ in range(a.reps):
             s.products()
