@@ -20,6 +20,12 @@
 // epilogue warps drain each window into fp64 registers (double-buffered
 // accumulators), and write fp64 split-K partials that a deterministic reduce
 // sums in fixed order.
+// Why windows: the tensor core's fp32 accumulate truncates, so on the
+// all-nonnegative NMF operands the error is a one-sided bias that grows
+// linearly with the accumulation length: measured ~2.4e-7 relative per
+// 32-K chunk of window (tools/tc_check.py: window 64 -> 1.6e-5, 8 -> 1.9e-6,
+// 4 -> 8.7e-7, 1 -> 2.0e-7 on uniform [0,1) data; profiles/README.md).
+// kWindow = 8 keeps the products ~2e-6 of fp64 at ~4% throughput cost.
 //
 // Warp roles (576 threads, one persistent CTA per SM, 512 TMEM columns):
 //   warp 0: TMA producer      warp 1: TMEM allocator + MMA issuer
@@ -41,9 +47,15 @@ namespace tc {
 
 constexpr int kMStages = 8;       // M-slice ring (TMA -> converters), 16 KB each
 constexpr int kBStages = 4;       // factor-slice ring (TMA -> MMA), 2 r_pad x 128 B each
-constexpr int kSlots = 6;         // TMEM staging slots (hi|lo, 64 columns each)
+#ifndef MLB_TC_SLOTS
+#define MLB_TC_SLOTS 4
+#endif
+constexpr int kSlots = MLB_TC_SLOTS;  // TMEM staging slots (hi|lo, 64 columns each)
 constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
-constexpr int kWindow = 64;       // chunks per fp32 accumulation window (2048 K)
+#ifndef MLB_TC_WINDOW
+#define MLB_TC_WINDOW 8
+#endif
+constexpr int kWindow = MLB_TC_WINDOW;  // chunks per fp32 accumulation window
 constexpr int kConvGroups = 2;    // converter groups of 4 warps (alternate chunks)
 constexpr int kThreads = (2 + 4 * kConvGroups + 8) * 32;
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB

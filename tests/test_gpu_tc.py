@@ -1,10 +1,15 @@
 """GPU: the tcgen05 3xTF32 M-streaming products against fp64 references.
 
 A = M W^T and C = V^T M from fp32 storage: the tensor-core path must agree
-with an fp64 numpy product of the same fp32 inputs to 3xTF32 accuracy
-(relative Frobenius error <= 2e-6 stated here; measured ~1e-7), on aligned and
-ragged shapes, r in {16..64}; and whole fp32 runs through the tensor path must
-track the fp64 oracle.
+with an fp64 numpy product of the same fp32 inputs to 3xTF32 accuracy, on
+aligned and ragged shapes, r in {16..64}; and whole fp32 runs through the
+tensor path must track the fp64 oracle.
+
+Tolerance: the tensor core's fp32 accumulate truncates, a one-sided bias of
+~2.4e-7 relative per 32-K chunk accumulated in TMEM before the fp64 drain
+(kWindow = 8 chunks -> ~2e-6 at long K; short-K shapes ~4e-7).  TOL = 4e-6
+relative Frobenius error is that bound with a 2x margin; the long-K case
+(32768 x 8192, several windows per CTA) exercises it.
 """
 import numpy as np
 import pytest
@@ -13,7 +18,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-TOL = 2e-6
+TOL = 4e-6
 
 
 def relnorm(a, b):
@@ -22,7 +27,7 @@ def relnorm(a, b):
 
 @pytest.mark.parametrize("m,n,r", [
     (1024, 2048, 64), (1024, 2048, 20), (4096, 1024, 40), (1028, 1500, 49),
-    (256, 16384, 64), (16384, 256, 64), (640, 640, 16), (2052, 4100, 33),
+    (256, 16384, 64), (16384, 256, 64), (640, 640, 16), (2052, 4100, 33), (32768, 8192, 64),
 ])
 def test_tc_products(P, gpu, m, n, r):
     rng = np.random.default_rng(m * 7 + n + r)
