@@ -353,6 +353,17 @@ struct Engine::Impl {
     const int r = (int)e->r_;
     const size_t n = e->n_loc_;
     const size_t cb = ceil_div(n, 128);
+    const size_t tiled_smem = 2 * (size_t)r * 128 * sizeof(T);
+    if (!exact() && tiled_smem <= 200 * 1024) {
+      // register-tiled residual: one fp64 partial per 128 x 128 tile
+      const size_t rb = ceil_div(L.m, 128), nb = cb * rb;
+      part.ensure(nb * 8);
+      launch(k_sqerr_tiled<T>, dim3((unsigned)cb, (unsigned)rb), dim3(256), tiled_smem, (const T*)L.M,
+             (const T*)L.V, (const T*)W.as<T>(), L.m, n, r, part.as<double>());
+      launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part.as<double>(), nb, out, 0);
+      allreduce_sum(out, 1);
+      return;
+    }
     size_t sp = 1;
     if (!exact()) sp = std::max<size_t>(1, std::min(ceil_div(kTargetBlocks, cb), ceil_div(L.m, 256)));
     const size_t rchunk = ceil_div(ceil_div(L.m, sp), 32) * 32;
