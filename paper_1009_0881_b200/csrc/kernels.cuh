@@ -334,11 +334,20 @@ __global__ void __launch_bounds__(128) k_col_sqerr(const T* __restrict__ M, cons
 // shared memory (k-major), the prediction accumulated in T with FMA (round-to-
 // nearest, unbiased), the squared residual in fp64.  One fp64 partial per
 // block (deterministic).  FMA-bound: m n r FMAs, ~20x faster than k_col_sqerr.
+__device__ __forceinline__ void ld4_shared(const float* p, float* o) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+}
+__device__ __forceinline__ void ld4_shared(const double* p, double* o) {
+  const double2 u = *reinterpret_cast<const double2*>(p), v = *reinterpret_cast<const double2*>(p + 2);
+  o[0] = u.x, o[1] = u.y, o[2] = v.x, o[3] = v.y;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_sqerr_tiled(const T* __restrict__ M, const T* __restrict__ V,
                                                      const T* __restrict__ W, size_t m, size_t n, int r,
                                                      double* __restrict__ part) {
-  extern __shared__ unsigned char smraw[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   T* Vs = reinterpret_cast<T*>(smraw);  // [r][128]
   T* Ws = Vs + (size_t)r * 128;         // [r][128]
   __shared__ double red[8];
@@ -358,12 +367,15 @@ __global__ void __launch_bounds__(256) k_sqerr_tiled(const T* __restrict__ M, co
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = T(0);
+  // thread rows: (a >> 2) * 64 + ty * 4 + (a & 3); columns likewise with tx:
+  // four consecutive k-major values per 16-byte (fp32) shared-memory load
   for (int k = 0; k < r; ++k) {
     T va[8], wb[8];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) va[a] = Vs[k * 128 + ty + 16 * a];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) wb[b] = Ws[k * 128 + tx + 16 * b];
+    for (int h = 0; h < 2; ++h) {
+      ld4_shared(Vs + k * 128 + h * 64 + ty * 4, va + 4 * h);
+      ld4_shared(Ws + k * 128 + h * 64 + tx * 4, wb + 4 * h);
+    }
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -372,11 +384,11 @@ __global__ void __launch_bounds__(256) k_sqerr_tiled(const T* __restrict__ M, co
   double s = 0.0;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
-    const size_t i = i0 + ty + 16 * a;
+    const size_t i = i0 + (a >> 2) * 64 + ty * 4 + (a & 3);
     if (i >= m) continue;
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const size_t j = j0 + tx + 16 * b;
+      const size_t j = j0 + (b >> 2) * 64 + tx * 4 + (b & 3);
       if (j < n) {
         const double d = (double)M[i * n + j] - (double)acc[a][b];
         s = fma(d, d, s);
