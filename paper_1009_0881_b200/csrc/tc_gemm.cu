@@ -27,16 +27,18 @@
 // 4 -> 8.7e-7, 1 -> 2.0e-7 on uniform [0,1) data; profiles/README.md).
 // kWindow = 8 keeps the products ~2e-6 of fp64 at ~4% throughput cost.
 //
-// Warp roles (576 threads, one persistent CTA per SM, 512 TMEM columns):
-//   warp 0: TMA producer      warp 1: TMEM allocator + MMA issuer
+// Warp roles (608 threads, one persistent CTA per SM, 512 TMEM columns):
+//   warp 0: TMA producer (M)  warp 1: TMEM allocator + MMA issuer
 //   warps 2-9: converters (two groups of 4, alternate chunks)
 //   warps 10-17: epilogue (lane quarter x column half)
+//   warp 18: TMA producer (factor slices)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -46,18 +48,19 @@ namespace mlb {
 namespace tc {
 
 constexpr int kMStages = 8;       // M-slice ring (TMA -> converters), 16 KB each
-constexpr int kBStages = 4;       // factor-slice ring (TMA -> MMA), 2 r_pad x 128 B each
-#ifndef MLB_TC_SLOTS
-#define MLB_TC_SLOTS 4
-#endif
-constexpr int kSlots = MLB_TC_SLOTS;  // TMEM staging slots (hi|lo, 64 columns each)
+constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
+constexpr int kBStages = kSlots;  // factor-slice ring, in lockstep with the staging slots
+constexpr int kBStageBytes = 16384;  // fixed stride (2 r_pad x 128 B <= 16 KB)
+constexpr int kAccStride = 128;   // TMEM columns per accumulator buffer (2 r_pad <= 128)
+constexpr int kStgCol0 = 2 * kAccStride;  // staging slots follow the two accumulators
+static_assert(kStgCol0 + kSlots * 64 == 512, "TMEM map: 2 accumulators + staging = 512 columns");
 constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
 #ifndef MLB_TC_WINDOW
 #define MLB_TC_WINDOW 8
 #endif
 constexpr int kWindow = MLB_TC_WINDOW;  // chunks per fp32 accumulation window
 constexpr int kConvGroups = 2;    // converter groups of 4 warps (alternate chunks)
-constexpr int kThreads = (2 + 4 * kConvGroups + 8) * 32;
+constexpr int kThreads = (2 + 4 * kConvGroups + 8 + 1) * 32;  // + factor-slice producer warp
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
 
 #define TC_CK(x)                                                                                  \
@@ -199,6 +202,35 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
+// One pipeline chunk (K = 32, four K-steps of 8) on staging slot S into
+// accumulator ACC, issued by one elected lane in a single asm block:
+//   D[:, 0:2r) (+)= A_hi [F_hi;F_lo]^T   and   D[:, 0:r) += A_lo F_hi^T.
+// TMEM addresses and the B-descriptor offsets are compile-time constants
+// (TMEM base 0, fixed strides), so the operands sit in uniform registers
+// without per-chunk R2UR traffic.  `first` clears the accumulator (window start).
+template <int S, int ACC>
+__device__ __forceinline__ void issue_chunk(uint64_t bdesc0, uint32_t id_full, uint32_t id_hi, uint32_t first) {
+  constexpr uint32_t d = ACC * kAccStride;
+  constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
+  constexpr uint64_t boff = (uint64_t)(S * kBStageBytes) >> 4;  // descriptor start-address units
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.u32 p, %13, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %9, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %5, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%3], %6, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%4], %6, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], %7, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %7, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %8, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %8, %10, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "r"(a_hi + 8), "r"(a_lo + 8), "l"(bdesc0 + boff), "l"(bdesc0 + boff + 2),
+      "l"(bdesc0 + boff + 4), "l"(bdesc0 + boff + 6), "r"(id_full), "r"(id_hi), "r"(a_hi + 16), "r"(a_lo + 16),
+      "r"(first), "r"(a_hi + 24), "r"(a_lo + 24)
+      : "memory");
+}
+
 struct Params {
   int rows;        // MMA-M extent: m (product 1) or n (product 2)
   int kdim;        // K extent: n (product 1) or m (product 2)
@@ -208,7 +240,6 @@ struct Params {
   int splits;      // split-K factor
   int chunks_per_split;
   int nchunks;     // ceil(kdim / 32)
-  int nacc;        // accumulator buffers in TMEM (1 or 2)
   double* part;    // [splits][...] fp64 partial outputs
 };
 
@@ -220,41 +251,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
                  const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // carve: [M ring: kMStages x 16 KB][B ring: kBStages x 2rp*128 B][barriers]
+  // carve: [M ring: kMStages x 16 KB][B ring: kBStages x 16 KB][barriers]
   // The rings are separate so an M slice is released as soon as the
   // converters have read it (more HBM bytes in flight), while a factor slice
   // lives until the MMAs reading it complete.
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int b_bytes = 2 * p.rp * 128;
+  const int b_bytes = 2 * p.rp * 128;      // bytes TMA writes per factor slice
   unsigned char* sm_m = base;
   unsigned char* sm_b = base + kMStages * kMTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * b_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * kBStageBytes);
   uint64_t* mfull = bars;                  // [kMStages]  TMA -> converters
   uint64_t* mempty = mfull + kMStages;     // [kMStages]  converters -> TMA
   uint64_t* bfull = mempty + kMStages;     // [kBStages]  TMA -> MMA
-  uint64_t* bempty = bfull + kBStages;     // [kBStages]  MMA commit -> TMA
-  uint64_t* sfull = bempty + kBStages;     // [kSlots]    converters -> MMA
-  uint64_t* sempty = sfull + kSlots;       // [kSlots]    MMA commit -> converters
-  uint64_t* afull = sempty + kSlots;       // [2]         MMA commit -> epilogue
+  uint64_t* sfull = bfull + kBStages;      // [kSlots]    converters -> MMA
+  uint64_t* sdone = sfull + kSlots;        // [kSlots]    MMA commit -> converters + TMA
+                                           //             (staging slot s and B stage s free)
+  uint64_t* afull = sdone + kSlots;        // [2]         MMA commit -> epilogue
   uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int acc_cols = 2 * p.rp;
-  const int stg_col0 = p.nacc * acc_cols;   // accumulators first, then staging
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMStages; ++i) {
       mbar_init(smem_u32(&mfull[i]), 1);
       mbar_init(smem_u32(&mempty[i]), 4);  // the 4 warps of the converting group
     }
-    for (int i = 0; i < kBStages; ++i) {
-      mbar_init(smem_u32(&bfull[i]), 1);
-      mbar_init(smem_u32(&bempty[i]), 1);
-    }
     for (int i = 0; i < kSlots; ++i) {
+      mbar_init(smem_u32(&bfull[i]), 1);
       mbar_init(smem_u32(&sfull[i]), 4);
-      mbar_init(smem_u32(&sempty[i]), 1);
+      mbar_init(smem_u32(&sdone[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&afull[i]), 1);
@@ -281,8 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      int ms = 0, bs = 0;
-      uint32_t mph = 0, bph = 0;
+      int ms = 0;
+      uint32_t mph = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
@@ -295,11 +321,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, c * kChunk, tile * 128, fm);
           else
             tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, tile * 128, c * kChunk, fm);
-          mbar_wait(smem_u32(&bempty[bs]), bph ^ 1);
+          if (++ms == kMStages) ms = 0, mph ^= 1;
+        }
+      }
+    }
+  } else if (warp == kThreads / 32 - 1) {
+    // ======================= TMA producer: factor slices =======================
+    // Own warp: the B ring (4 deep, freed only when a chunk's MMAs complete)
+    // must not throttle the M stream, whose ring is 8 deep.
+    if (lane == 0) {
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int split = u / p.tiles;
+        const int c_beg = split * p.chunks_per_split;
+        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+        for (int c = c_beg; c < c_end; ++c) {
+          mbar_wait<64>(smem_u32(&sdone[bs]), bph ^ 1);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d(smem_u32(sm_b + bs * b_bytes), &map_b, c * kChunk, 0, fb);
-          if (++ms == kMStages) ms = 0, mph ^= 1;
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, c * kChunk, 0, fb);
           if (++bs == kBStages) bs = 0, bph ^= 1;
         }
       }
@@ -311,9 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (A single-lane loop costs ~240 cycles/instruction in R2UR/ELECT
     // overhead -- tools/mma_probe2.cu measures 2047 MAC/cycle/SM this way.)
     const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
-    const uint32_t sm_b_u32 = smem_u32(sm_b);
-    int bs = 0, slot = 0, acc = 0;
-    uint32_t bphase = 0, sphase = 0, aphase = 0;
+    const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
+    int slot = 0, acc = 0;  // B stage == staging slot (lockstep rings)
+    uint32_t sphase = 0, aphase = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int split = u / p.tiles;
       const int c_beg = split * p.chunks_per_split;
@@ -323,25 +364,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
         if (wpos == 0) mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
         mbar_wait(smem_u32(&sfull[slot]), sphase);
-        mbar_wait(smem_u32(&bfull[bs]), bphase);
+        mbar_wait(smem_u32(&bfull[slot]), sphase);
         tc_fence_after();
-        const uint32_t d = (uint32_t)(acc * acc_cols);  // TMEM base is column 0 (512-column allocation)
-        const uint32_t a_hi = (uint32_t)(stg_col0 + slot * 64), a_lo = a_hi + 32;
-        const uint32_t bsm = sm_b_u32 + (uint32_t)(bs * b_bytes);
-#pragma unroll
-        for (int kk = 0; kk < kChunk / 8; ++kk) {
-          const uint64_t bd = sdesc_sw128(bsm + kk * 32);
-          mma_ts(d, a_hi + kk * 8, bd, id_full, (wpos > 0 || kk > 0) ? 1u : 0u);
-          mma_ts(d, a_lo + kk * 8, bd, id_hi, 1u);
+        const uint32_t first = wpos == 0 ? 1u : 0u;
+        switch (slot * 2 + acc) {
+          case 0: issue_chunk<0, 0>(bdesc0, id_full, id_hi, first); break;
+          case 1: issue_chunk<0, 1>(bdesc0, id_full, id_hi, first); break;
+          case 2: issue_chunk<1, 0>(bdesc0, id_full, id_hi, first); break;
+          case 3: issue_chunk<1, 1>(bdesc0, id_full, id_hi, first); break;
+          case 4: issue_chunk<2, 0>(bdesc0, id_full, id_hi, first); break;
+          case 5: issue_chunk<2, 1>(bdesc0, id_full, id_hi, first); break;
+          case 6: issue_chunk<3, 0>(bdesc0, id_full, id_hi, first); break;
+          default: issue_chunk<3, 1>(bdesc0, id_full, id_hi, first); break;
         }
-        tc_commit(smem_u32(&bempty[bs]));
-        tc_commit(smem_u32(&sempty[slot]));
+        tc_commit(smem_u32(&sdone[slot]));  // slot s and B stage s reusable once these MMAs finish
         if (last_in_window) {
           tc_commit(smem_u32(&afull[acc]));
-          if (++acc == p.nacc) acc = 0, aphase ^= 1;
+          if (++acc == 2) acc = 0, aphase ^= 1;
         }
         __syncwarp();
-        if (++bs == kBStages) bs = 0, bphase ^= 1;
         if (++slot == kSlots) slot = 0, sphase ^= 1;
       }
     }
@@ -379,11 +420,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) x[k] = cp[k * 128];
         }
+        // The slice was read through the generic proxy and the refill is an
+        // async-proxy (TMA) write: order the two before releasing the stage
+        // (without this fence a refill can land before lanes' reads retire --
+        // seen as ~1e-3 product errors once the M ring runs far ahead).
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&mempty[ms]));  // slice consumed: TMA may refill it
-        mbar_wait(smem_u32(&sempty[slot]), sphase ^ 1);
+        mbar_wait(smem_u32(&sdone[slot]), sphase ^ 1);
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + stg_col0 + slot * 64;
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStgCol0 + slot * 64;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           // tf32 round-to-nearest(-away) on the bit pattern (== cvt.rna.tf32):
@@ -424,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait<256>(smem_u32(&afull[acc]), aphase);
         tc_fence_after();
         if (live) {
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * acc_cols + cb;
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * kAccStride + cb;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {  // hi part, then lo part of the stacked accumulator, 16 cols each
             uint32_t v[16];
@@ -437,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&aempty[acc]));
-        if (++acc == p.nacc) acc = 0, aphase ^= 1;
+        if (++acc == 2) acc = 0, aphase ^= 1;
       }
       const int gi = tile * 128 + row;
       if (live && gi < p.rows) {
@@ -584,9 +630,9 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
-    p.nacc = std::min(2, (512 - tc::kSlots * 64) / (2 * rp));
     // split-K so that there are >= ~8 units per SM (balance)
     int splits = (int)std::max<size_t>(1, cdiv((size_t)sms_ * 8, p.tiles));
+    if (const char* e = getenv("MLB_TC_SPLITS")) splits = std::max(1, atoi(e));  // debug override
     splits = std::min(splits, p.nchunks);
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
     p.splits = (int)cdiv(p.nchunks, p.chunks_per_split);
@@ -599,14 +645,15 @@ class TcGemmImpl final : public TcGemm {
     p.part = dst;
     const CUtensorMap mm = TRANS ? make_map(M, n, m, 128, tc::kChunk, false) : make_map(M, n, m, tc::kChunk, 128, true);
     const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, 2 * rp, true);
-    const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * 2 * rp * 128 + 512;
+    const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
     auto kern = tc::k_tc_product<TRANS>;
     if (!attr_set_[TRANS ? 1 : 0]) {
       TC_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set_[TRANS ? 1 : 0] = true;
     }
     const int units = p.tiles * p.splits;
-    const int grid = std::min(units, sms_);
+    int grid = std::min(units, sms_);
+    if (const char* e = getenv("MLB_TC_GRID")) grid = std::max(1, std::min(grid, atoi(e)));  // debug override
     kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
     TC_CK(cudaGetLastError());
     ++*launches;
