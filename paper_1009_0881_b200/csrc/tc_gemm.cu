@@ -27,17 +27,20 @@
 // 4 -> 8.7e-7, 1 -> 2.0e-7 on uniform [0,1) data; profiles/README.md).
 // kWindow = 8 keeps the products ~2e-6 of fp64 at ~4% throughput cost.
 //
-// Warp roles (608 threads, one persistent CTA per SM, 512 TMEM columns):
-//   warp 0: TMA producer (M)  warp 1: TMEM allocator + MMA issuer
-//   warps 2-9: converters (two groups of 4, alternate chunks)
-//   warps 10-17: epilogue (lane quarter x column half)
-//   warp 18: TMA producer (factor slices)
+// Warp roles (640 threads, one persistent CTA per SM, 512 TMEM columns):
+//   warp 0: TMA producer (M slices)
+//   warps 1, 2: MMA issuers for even / odd chunks, each into its own fp32
+//               accumulator (TMEM columns 0 / 128); warp 1 allocates TMEM
+//   warps 3-10: converters (two groups of 4: even / odd chunks)
+//   warps 11-18: epilogue (lane quarter x column half), drains both accumulators
+//   warp 19: TMA producers (factor slices; lane 0 even, lane 1 odd chunks)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -60,7 +63,12 @@ constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
 #endif
 constexpr int kWindow = MLB_TC_WINDOW;  // chunks per fp32 accumulation window
 constexpr int kConvGroups = 2;    // converter groups of 4 warps (alternate chunks)
-constexpr int kThreads = (2 + 4 * kConvGroups + 8 + 1) * 32;  // + factor-slice producer warp
+constexpr int kWarpM = 0;                            // TMA producer: M slices
+constexpr int kWarpMma0 = 1, kWarpMma1 = 2;           // MMA issuers (even / odd chunks); 1 allocates TMEM
+constexpr int kWarpConv0 = 3;                        // converter groups
+constexpr int kWarpEpi0 = kWarpConv0 + 4 * kConvGroups;  // 8 epilogue warps
+constexpr int kWarpB = kWarpEpi0 + 8;                // TMA producers: factor slices (lanes 0 / 1)
+constexpr int kThreads = (kWarpB + 1) * 32;
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
 
 #define TC_CK(x)                                                                                  \
@@ -205,6 +213,9 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
 // One pipeline chunk (K = 32, four K-steps of 8) on staging slot S into
 // accumulator ACC, issued by one elected lane in a single asm block:
 //   D[:, 0:2r) (+)= A_hi [F_hi;F_lo]^T   and   D[:, 0:r) += A_lo F_hi^T.
+// The four N = 2r MMAs go first, then the four N = r ones: alternating the two
+// shapes on overlapping accumulator columns serialises every MMA on the
+// previous one's result (measured ~2x slower issue).
 // TMEM addresses and the B-descriptor offsets are compile-time constants
 // (TMEM base 0, fixed strides), so the operands sit in uniform registers
 // without per-chunk R2UR traffic.  `first` clears the accumulator (window start).
@@ -218,12 +229,12 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc0, uint32_t id_full, u
       "elect.sync _|e, 0xffffffff;\n\t"
       "setp.eq.u32 p, %13, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %9, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %5, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%3], %6, %9, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%4], %6, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], %7, %9, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %7, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %8, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %5, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%4], %6, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %7, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %8, %10, 1;\n\t}" ::"r"(d),
       "r"(a_hi), "r"(a_lo), "r"(a_hi + 8), "r"(a_lo + 8), "l"(bdesc0 + boff), "l"(bdesc0 + boff + 2),
       "l"(bdesc0 + boff + 4), "l"(bdesc0 + boff + 6), "r"(id_full), "r"(id_hi), "r"(a_hi + 16), "r"(a_lo + 16),
@@ -246,6 +257,60 @@ struct Params {
 // ----------------------------------------------------------------------------
 // The persistent warp-specialised kernel
 // ----------------------------------------------------------------------------
+// Chunks are numbered g = 0, 1, 2, ... in the order a CTA streams them (all of
+// its units, in order).  Parity w = g & 1 selects the converter group, the MMA
+// warp, the factor-slice producer and the accumulator; g % kSlots the TMEM
+// staging slot and B stage.  Within a unit, the chunks of parity w are
+// i = i0(w), i0(w) + 2, ... with i0(w) = (w - g0) & 1.
+__device__ __forceinline__ int own_first(int g0, int w) { return (w - g0) & 1; }
+__device__ __forceinline__ int own_count(int g0, int n_u, int w) {
+  const int i0 = own_first(g0, w);
+  return n_u > i0 ? (n_u - i0 + 1) >> 1 : 0;
+}
+
+// MMA issuer for the chunks of parity W into accumulator W.  Two such warps
+// run concurrently: the tensor pipe accepts an MMA only when it has room, so a
+// single issuing warp stalls inside the MMAs and its per-chunk waits and
+// commits leave the pipe idle; with two, one warp's bookkeeping overlaps the
+// other's MMAs.
+template <int W>
+__device__ __forceinline__ void mma_role(const Params& p, int total_units, uint64_t bdesc0, uint64_t* ready,
+                                         uint64_t* sdone, uint64_t* afull, uint64_t* aempty) {
+  const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
+  int g = 0;
+  uint32_t aph = 0;
+  int lastph[2] = {-1, -1};  // parity of the last commit on slots W and W + 2
+  for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    const int split = u / p.tiles;
+    const int c_beg = split * p.chunks_per_split;
+    const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+    for (int i = own_first(g, W), j = 0; i < n_u; i += 2, ++j) {
+      const int gg = g + i, slot = gg % kSlots;
+      const uint32_t sph = (uint32_t)(gg / kSlots) & 1u;
+      const int wpos = j % kWindow;
+      if (wpos == 0) mbar_wait(smem_u32(&aempty[W]), aph ^ 1);
+      mbar_wait(smem_u32(&ready[slot]), sph);
+      tc_fence_after();
+      const uint32_t first = wpos == 0 ? 1u : 0u;
+      if (slot == W)
+        issue_chunk<W, W>(bdesc0, id_full, id_hi, first);
+      else
+        issue_chunk<W + 2, W>(bdesc0, id_full, id_hi, first);
+      tc_commit(smem_u32(&sdone[slot]));  // slot and B stage reusable once these MMAs finish
+      lastph[slot >> 1] = (int)sph;
+      if (wpos == kWindow - 1 || i + 2 >= n_u) {
+        tc_commit(smem_u32(&afull[W]));
+        aph ^= 1;
+      }
+      __syncwarp();
+    }
+    g += n_u;
+  }
+  // drain: no tcgen05.commit arrival may land after the CTA exits
+  for (int k = 0; k < 2; ++k)
+    if (lastph[k] >= 0) mbar_wait(smem_u32(&sdone[W + 2 * k]), (uint32_t)lastph[k]);
+}
+
 template <bool TRANS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
@@ -262,12 +327,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * kBStageBytes);
   uint64_t* mfull = bars;                  // [kMStages]  TMA -> converters
   uint64_t* mempty = mfull + kMStages;     // [kMStages]  converters -> TMA
-  uint64_t* bfull = mempty + kMStages;     // [kBStages]  TMA -> MMA
-  uint64_t* sfull = bfull + kBStages;      // [kSlots]    converters -> MMA
-  uint64_t* sdone = sfull + kSlots;        // [kSlots]    MMA commit -> converters + TMA
+  uint64_t* ready = mempty + kMStages;     // [kSlots]    chunk ready for the MMA: 4 converter
+                                           //             arrivals (TMEM slot s written) + the
+                                           //             factor slice's TMA bytes (B stage s)
+  uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters + TMA
                                            //             (staging slot s and B stage s free)
-  uint64_t* afull = sdone + kSlots;        // [2]         MMA commit -> epilogue
-  uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA
+  uint64_t* afull = sdone + kSlots;        // [2]         MMA warp w commit -> epilogue
+  uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA warp w
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -278,8 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&mempty[i]), 4);  // the 4 warps of the converting group
     }
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(smem_u32(&bfull[i]), 1);
-      mbar_init(smem_u32(&sfull[i]), 4);
+      mbar_init(smem_u32(&ready[i]), 4 + 1);  // 4 converter warps + the B producer's expect_tx
       mbar_init(smem_u32(&sdone[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -290,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_m)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
-  if (warp == 1) {
+  if (warp == kWarpMma0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(512)
                  : "memory");
@@ -304,8 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int total_units = p.tiles * p.splits;
 
-  if (warp == 0) {
-    // ======================= TMA producer =======================
+  if (warp == kWarpM) {
+    // ======================= TMA producer: M slices =======================
     if (lane == 0) {
       int ms = 0;
       uint32_t mph = 0;
@@ -325,72 +390,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kThreads / 32 - 1) {
-    // ======================= TMA producer: factor slices =======================
-    // Own warp: the B ring (4 deep, freed only when a chunk's MMAs complete)
-    // must not throttle the M stream, whose ring is 8 deep.
-    if (lane == 0) {
-      int bs = 0;
-      uint32_t bph = 0;
+  } else if (warp == kWarpB) {
+    // ======================= TMA producers: factor slices (lanes 0 / 1: even / odd chunks) =======================
+    // Own warp: the B ring (freed only when a chunk's MMAs complete) must not
+    // throttle the M stream, and one parity's stall must not block the other.
+    const int w = lane;
+    if (lane < 2) {
+      int g = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
-        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-        for (int c = c_beg; c < c_end; ++c) {
-          mbar_wait<64>(smem_u32(&sdone[bs]), bph ^ 1);
-          const uint32_t fb = smem_u32(&bfull[bs]);
+        const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+        for (int i = own_first(g, w); i < n_u; i += 2) {
+          const int gg = g + i, bs = gg % kBStages;
+          mbar_wait<64>(smem_u32(&sdone[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
+          const uint32_t fb = smem_u32(&ready[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, c * kChunk, 0, fb);
-          if (++bs == kBStages) bs = 0, bph ^= 1;
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
         }
+        g += n_u;
       }
     }
-  } else if (warp == 1) {
-    // ======================= MMA issuer =======================
+  } else if (warp == kWarpMma0 || warp == kWarpMma1) {
+    // ======================= MMA issuers (one per parity) =======================
     // The whole warp runs the (warp-uniform) loop so every MMA operand stays in
     // the uniform datapath; one elected lane issues each tcgen05 instruction.
-    // (A single-lane loop costs ~240 cycles/instruction in R2UR/ELECT
-    // overhead -- tools/mma_probe2.cu measures 2047 MAC/cycle/SM this way.)
-    const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
-    int slot = 0, acc = 0;  // B stage == staging slot (lockstep rings)
-    uint32_t sphase = 0, aphase = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int split = u / p.tiles;
-      const int c_beg = split * p.chunks_per_split;
-      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-      for (int c = c_beg; c < c_end; ++c) {
-        const int wpos = (c - c_beg) % kWindow;
-        const bool last_in_window = (wpos == kWindow - 1) || (c == c_end - 1);
-        if (wpos == 0) mbar_wait(smem_u32(&aempty[acc]), aphase ^ 1);
-        mbar_wait(smem_u32(&sfull[slot]), sphase);
-        mbar_wait(smem_u32(&bfull[slot]), sphase);
-        tc_fence_after();
-        const uint32_t first = wpos == 0 ? 1u : 0u;
-        switch (slot * 2 + acc) {
-          case 0: issue_chunk<0, 0>(bdesc0, id_full, id_hi, first); break;
-          case 1: issue_chunk<0, 1>(bdesc0, id_full, id_hi, first); break;
-          case 2: issue_chunk<1, 0>(bdesc0, id_full, id_hi, first); break;
-          case 3: issue_chunk<1, 1>(bdesc0, id_full, id_hi, first); break;
-          case 4: issue_chunk<2, 0>(bdesc0, id_full, id_hi, first); break;
-          case 5: issue_chunk<2, 1>(bdesc0, id_full, id_hi, first); break;
-          case 6: issue_chunk<3, 0>(bdesc0, id_full, id_hi, first); break;
-          default: issue_chunk<3, 1>(bdesc0, id_full, id_hi, first); break;
-        }
-        tc_commit(smem_u32(&sdone[slot]));  // slot s and B stage s reusable once these MMAs finish
-        if (last_in_window) {
-          tc_commit(smem_u32(&afull[acc]));
-          if (++acc == 2) acc = 0, aphase ^= 1;
-        }
-        __syncwarp();
-        if (++slot == kSlots) slot = 0, sphase ^= 1;
-      }
-    }
-  } else if (warp < 2 + 4 * kConvGroups) {
+    if (warp == kWarpMma0)
+      mma_role<0>(p, total_units, bdesc0, ready, sdone, afull, aempty);
+    else
+      mma_role<1>(p, total_units, bdesc0, ready, sdone, afull, aempty);
+  } else if (warp < kWarpEpi0) {
     // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
     // kConvGroups groups of 4 warps take alternate chunks (more chunks in
     // flight); within a group warp q owns TMEM lane quarter q (access rule).
-    const int grp = (warp - 2) >> 2;
+    const int grp = (warp - kWarpConv0) >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
     int g = 0;                       // global chunk sequence number
@@ -441,50 +475,63 @@ __global__ void __launch_bounds__(kThreads, 1)
             hi[k] = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
             lo[k] = (__float_as_uint(v - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
           }
+#if !MLB_X_NOST
           tmem_st16(ta + half * 16, hi);
           tmem_st16(ta + 32 + half * 16, lo);
+#else
+          if (hi[0] == 0x7fffffff && lo[3] == 1) tmem_st16(ta + half * 16, hi);
+#endif
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&sfull[slot]));
+        if (lane == 0) mbar_arrive(smem_u32(&ready[slot]));
       }
     }
   } else {
     // ======================= epilogue: fp32 windows -> fp64 =======================
-    // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32
+    // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32.
+    // Per unit, windows are drained in a fixed order (window k of accumulator
+    // 0, then of accumulator 1), so the fp64 sums are deterministic.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int cb = ((warp - 2 - 4 * kConvGroups) >> 2) * 32;
+    const int cb = ((warp - kWarpEpi0) >> 2) * 32;
     const bool live = cb < p.rp;
-    int acc = 0;
-    uint32_t aphase = 0;
+    uint32_t aph[2] = {0, 0};
+    int g = 0;
     double sum[32];
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int tile = u % p.tiles, split = u / p.tiles;
       const int c_beg = split * p.chunks_per_split;
-      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
+      const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+      const int nw0 = (own_count(g, n_u, 0) + kWindow - 1) / kWindow;
+      const int nw1 = (own_count(g, n_u, 1) + kWindow - 1) / kWindow;
 #pragma unroll
       for (int k = 0; k < 32; ++k) sum[k] = 0.0;
-      for (int c0 = c_beg; c0 < c_end; c0 += kWindow) {
-        mbar_wait<256>(smem_u32(&afull[acc]), aphase);
-        tc_fence_after();
-        if (live) {
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * kAccStride + cb;
+      for (int k = 0; k < max(nw0, nw1); ++k) {
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {  // hi part, then lo part of the stacked accumulator, 16 cols each
-            uint32_t v[16];
-            tmem_ld16(ta + (h >> 1) * p.rp + (h & 1) * 16, v);
-            tmem_wait_ld();
+        for (int w = 0; w < 2; ++w) {
+          if (k >= (w ? nw1 : nw0)) continue;
+          mbar_wait<256>(smem_u32(&afull[w]), aph[w]);
+          tc_fence_after();
+          if (live) {
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + w * kAccStride + cb;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) sum[(h & 1) * 16 + k] += (double)__uint_as_float(v[k]);
+            for (int h = 0; h < 4; ++h) {  // main part, then the F_lo part of the stacked accumulator, 16 cols each
+              uint32_t v[16];
+              tmem_ld16(ta + (h >> 1) * p.rp + (h & 1) * 16, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int kk = 0; kk < 16; ++kk) sum[(h & 1) * 16 + kk] += (double)__uint_as_float(v[kk]);
+            }
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&aempty[w]));
+          aph[w] ^= 1;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&aempty[acc]));
-        if (++acc == 2) acc = 0, aphase ^= 1;
       }
+      g += n_u;
       const int gi = tile * 128 + row;
       if (live && gi < p.rows) {
         if (!TRANS) {
@@ -504,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kWarpMma0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
@@ -656,6 +703,7 @@ class TcGemmImpl final : public TcGemm {
     if (const char* e = getenv("MLB_TC_GRID")) grid = std::max(1, std::min(grid, atoi(e)));  // debug override
     kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
     TC_CK(cudaGetLastError());
+
     ++*launches;
     if (p.splits > 1) {
       const unsigned g = (unsigned)std::min<size_t>(cdiv(out_count, 256), 4096);
