@@ -50,7 +50,11 @@
 namespace mlb {
 namespace tc {
 
-constexpr int kMStages = 8;       // M-slice ring (TMA -> converters), 16 KB each
+#ifndef MLB_TC_MSTAGES
+#define MLB_TC_MSTAGES 10
+#endif
+constexpr int kMStages = MLB_TC_MSTAGES;  // M-slice ring (TMA -> converters), 16 KB each
+constexpr int kMPairs = kMStages / 2;  // the ring is filled and released in pairs of slices
 constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
 constexpr int kBStages = kSlots;  // factor-slice ring, in lockstep with the staging slots
 constexpr int kBStageBytes = 16384;  // fixed stride (2 r_pad x 128 B <= 16 KB)
@@ -325,9 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* sm_m = base;
   unsigned char* sm_b = base + kMStages * kMTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * kBStageBytes);
-  uint64_t* mfull = bars;                  // [kMStages]  TMA -> converters
-  uint64_t* mempty = mfull + kMStages;     // [kMStages]  converters -> TMA
-  uint64_t* ready = mempty + kMStages;     // [kSlots]    chunk ready for the MMA: 4 converter
+  uint64_t* mfull = bars;                  // [kMPairs]   TMA -> converters (a pair of slices)
+  uint64_t* mempty = mfull + kMPairs;      // [kMPairs]   converters -> TMA
+  uint64_t* ready = mempty + kMPairs;     // [kSlots]    chunk ready for the MMA: 4 converter
                                            //             arrivals (TMEM slot s written) + the
                                            //             factor slice's TMA bytes (B stage s)
   uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters + TMA
@@ -339,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kMStages; ++i) {
+    for (int i = 0; i < kMPairs; ++i) {
       mbar_init(smem_u32(&mfull[i]), 1);
-      mbar_init(smem_u32(&mempty[i]), 4);  // the 4 warps of the converting group
+      mbar_init(smem_u32(&mempty[i]), 8);  // both converter groups (4 warps each)
     }
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(smem_u32(&ready[i]), 4 + 1);  // 4 converter warps + the B producer's expect_tx
@@ -372,23 +376,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpM) {
     // ======================= TMA producer: M slices =======================
     if (lane == 0) {
-      int ms = 0;
-      uint32_t mph = 0;
+      // Slices go out in pairs (chunks g, g + 1) on one barrier, back to back:
+      // for product 1 the two 128-byte row segments of each M row are adjacent
+      // in DRAM, so issuing them together keeps the DRAM page open.
+      int g = 0, pend_tile = 0, pend_c = -1;
+      auto issue_pair = [&](int t1, int c1, int t2, int c2) {
+        const int pg = g >> 1, ps = pg % kMPairs;
+        mbar_wait(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMPairs) & 1u) ^ 1u);
+        const uint32_t fm = smem_u32(&mfull[ps]);
+        mbar_expect_tx(fm, c2 >= 0 ? 2 * kMTileBytes : kMTileBytes);
+        unsigned char* dst = sm_m + ps * 2 * kMTileBytes;
+        if (!TRANS) {
+          tma_load_2d(smem_u32(dst), &map_m, c1 * kChunk, t1 * 128, fm);
+          if (c2 >= 0) tma_load_2d(smem_u32(dst + kMTileBytes), &map_m, c2 * kChunk, t2 * 128, fm);
+        } else {
+          tma_load_2d(smem_u32(dst), &map_m, t1 * 128, c1 * kChunk, fm);
+          if (c2 >= 0) tma_load_2d(smem_u32(dst + kMTileBytes), &map_m, t2 * 128, c2 * kChunk, fm);
+        }
+        g += 2;
+      };
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
         for (int c = c_beg; c < c_end; ++c) {
-          mbar_wait(smem_u32(&mempty[ms]), mph ^ 1);
-          const uint32_t fm = smem_u32(&mfull[ms]);
-          mbar_expect_tx(fm, kMTileBytes);
-          if (!TRANS)
-            tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, c * kChunk, tile * 128, fm);
-          else
-            tma_load_2d(smem_u32(sm_m + ms * kMTileBytes), &map_m, tile * 128, c * kChunk, fm);
-          if (++ms == kMStages) ms = 0, mph ^= 1;
+          if (pend_c < 0) {
+            pend_tile = tile, pend_c = c;
+          } else {
+            issue_pair(pend_tile, pend_c, tile, c);
+            pend_c = -1;
+          }
         }
       }
+      if (pend_c >= 0) issue_pair(pend_tile, pend_c, 0, -1);
     }
   } else if (warp == kWarpB) {
     // ======================= TMA producers: factor slices (lanes 0 / 1: even / odd chunks) =======================
@@ -434,12 +454,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
       for (int c = c_beg; c < c_end; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
-        const int ms = g % kMStages, slot = g % kSlots;
-        const uint32_t mph = (uint32_t)(g / kMStages) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
-        mbar_wait(smem_u32(&mfull[ms]), mph);
+        const int pg = g >> 1, ps = pg % kMPairs, slot = g % kSlots;
+        const uint32_t mph = (uint32_t)(pg / kMPairs) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
+        mbar_wait(smem_u32(&mfull[ps]), mph);
         // the thread's 32 values of this chunk (its MMA row / TMEM lane)
         float x[32];
-        const unsigned char* tile = sm_m + ms * kMTileBytes;
+        const unsigned char* tile = sm_m + (ps * 2 + (g & 1)) * kMTileBytes;
         if (!TRANS) {
           // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
           const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
@@ -460,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // seen as ~1e-3 product errors once the M ring runs far ahead).
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&mempty[ms]));  // slice consumed: TMA may refill it
+        if (lane == 0) mbar_arrive(smem_u32(&mempty[ps]));  // slice consumed: TMA may refill the pair
         mbar_wait(smem_u32(&sdone[slot]), sphase ^ 1);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStgCol0 + slot * 64;
