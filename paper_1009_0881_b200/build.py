@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libmlnmf_b200.so")
 REPO = os.path.dirname(HERE)
 
-SOURCES = ["engine.cu", "tc_gemm.cu", "scheduler.cpp", "capi.cpp"]
+SOURCES = ["engine.cu", "tc_gemm.cu", "hals_reg.cu", "scheduler.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "hals_reg.hpp"
 #include "kernels.cuh"
 #include "nccl_shim.hpp"
 #include "nnls.cuh"
@@ -267,7 +268,10 @@ struct Engine::Impl {
     const int bd = sweep_block((int)r);
     const size_t smem = (r * r + r * bd) * 8;
     const dim3 gv((unsigned)ceil_div(L.m, bd));
-    if (kind == kHals) {
+    if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep (config-4 rank)
+      hals_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, deg, s);
+      ++e->launches_;
+    } else if (kind == kHals) {
       launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
     } else if (kind == kMu) {
       launch(k_mu_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
@@ -279,7 +283,10 @@ struct Engine::Impl {
     product_vtm<T>(l);
     T* Wp = W.as<T>();
     const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
-    if (kind == kHals) {
+    if (kind == kHals && hals_reg_supported(r)) {
+      hals_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
+      ++e->launches_;
+    } else if (kind == kHals) {
       launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
              e->n_loc_, (int)r, deg);
     } else if (kind == kMu) {

@@ -1,0 +1,130 @@
+// hals_reg.cu -- register-resident HALS sweeps at a compile-time rank
+// (hals_step, proj/src/solvers.cpp:101-141).  Kept in their own translation
+// unit: the fully unrolled r x r sweeps take minutes to compile.
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <stdexcept>
+#include <string>
+
+#include "hals_reg.hpp"
+
+namespace mlb {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T to_t(double v);
+template <>
+__device__ __forceinline__ float to_t<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ double to_t<double>(double v) { return v; }
+// reference: `s -= a * b` (solvers.cpp:118,136), unfused
+__device__ __forceinline__ double msub(double acc, double a, double b) { return __dsub_rn(acc, __dmul_rn(a, b)); }
+
+// Register-resident HALS sweeps for a compile-time rank R (the config-4 rank):
+// the factor row / column lives in R registers instead of shared memory, the
+// Gram row for update k is read as broadcast from shared memory, and both k
+// and l loops are unrolled.  Same arithmetic and operation order as k_hals_v /
+// k_hals_w (the reference's, unfused), so results are bitwise identical;
+// ~10x fewer shared-memory accesses.
+template <typename T, int R>
+__global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A, const double* __restrict__ B,
+                                                    T* __restrict__ V, size_t m, int* __restrict__ degenerate) {
+  __shared__ double Bt[R * R];  // Bt[k][l] = B[l][k]: row k is the column the update reads
+  const int t = threadIdx.x;
+  for (int e = t; e < R * R; e += blockDim.x) Bt[e] = B[(e % R) * R + e / R];
+  __syncthreads();
+  const size_t i = (size_t)blockIdx.x * blockDim.x + t;
+  const bool act = i < m;
+  double v[R];
+#pragma unroll
+  for (int l = 0; l < R; ++l) v[l] = act ? (double)V[i * R + l] : 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double bkk = Bt[k * R + k];
+    if (bkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && t == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    const double a = act ? A[i * R + k] : 0.0;
+    double num = __dadd_rn(a, __dmul_rn(v[k], bkk));
+#pragma unroll
+    for (int l = 0; l < R; ++l) num = msub(num, v[l], Bt[k * R + l]);
+    const double q = num / bkk;
+    v[k] = q > 0.0 ? q : 0.0;
+  }
+  if (act)
+#pragma unroll
+    for (int l = 0; l < R; ++l) V[i * R + l] = to_t<T>(v[l]);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ Cm, const double* __restrict__ D,
+                                                    T* __restrict__ W, size_t n, int* __restrict__ degenerate) {
+  __shared__ double Ds[R * R];
+  const int t = threadIdx.x;
+  for (int e = t; e < R * R; e += blockDim.x) Ds[e] = D[e];
+  __syncthreads();
+  const size_t j = (size_t)blockIdx.x * blockDim.x + t;
+  const bool act = j < n;
+  double w[R];
+#pragma unroll
+  for (int l = 0; l < R; ++l) w[l] = act ? (double)W[(size_t)l * n + j] : 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double dkk = Ds[k * R + k];
+    if (dkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && t == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    const double c = act ? Cm[(size_t)k * n + j] : 0.0;
+    double num = __dadd_rn(c, __dmul_rn(dkk, w[k]));
+#pragma unroll
+    for (int l = 0; l < R; ++l) num = msub(num, Ds[k * R + l], w[l]);
+    const double q = num / dkk;
+    w[k] = q > 0.0 ? q : 0.0;
+  }
+  if (act)
+#pragma unroll
+    for (int l = 0; l < R; ++l) W[(size_t)l * n + j] = to_t<T>(w[l]);
+}
+
+
+template <int R>
+void launch_v(bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
+  const dim3 g((unsigned)((m + 127) / 128));
+  if (f32)
+    k_hals_v_reg<float, R><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m, deg);
+  else
+    k_hals_v_reg<double, R><<<g, 128, 0, s>>>(A, B, static_cast<double*>(V), m, deg);
+}
+template <int R>
+void launch_w(bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
+  const dim3 g((unsigned)((n + 127) / 128));
+  if (f32)
+    k_hals_w_reg<float, R><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n, deg);
+  else
+    k_hals_w_reg<double, R><<<g, 128, 0, s>>>(C, D, static_cast<double*>(W), n, deg);
+}
+
+void check(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_reg)");
+}
+
+}  // namespace
+
+bool hals_reg_supported(size_t r) { return r == 64; }
+
+void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
+  if (r != 64) throw std::invalid_argument("hals_v_reg: unsupported rank");
+  launch_v<64>(f32, A, B, V, m, deg, s);
+  check(cudaGetLastError());
+}
+
+void hals_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
+  if (r != 64) throw std::invalid_argument("hals_w_reg: unsupported rank");
+  launch_w<64>(f32, C, D, W, n, deg, s);
+  check(cudaGetLastError());
+}
+
+}  // namespace mlb

@@ -1,0 +1,13 @@
+// hals_reg.hpp -- register-resident HALS sweeps (hals_reg.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace mlb {
+bool hals_reg_supported(size_t r);
+// V (m x r, T = f32 ? float : double) rows swept with A (m x r) and B (r x r), fp64
+void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s);
+// W (r x n) columns swept with C (r x n) and D (r x r), fp64
+void hals_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s);
+}  // namespace mlb
