@@ -39,6 +39,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -51,12 +52,25 @@ namespace mlb {
 namespace tc {
 
 #ifndef MLB_TC_MSTAGES
-#define MLB_TC_MSTAGES 10
+#define MLB_TC_MSTAGES 8
 #endif
 constexpr int kMStages = MLB_TC_MSTAGES;  // M-slice ring (TMA -> converters), 16 KB each
-constexpr int kMPairs = kMStages / 2;  // the ring is filled and released in pairs of slices
+#ifndef MLB_TC_MGROUP
+#define MLB_TC_MGROUP 2
+#endif
+constexpr int kMGroup = MLB_TC_MGROUP;       // the ring is filled and released in groups of slices
+constexpr int kMGroups = kMStages / kMGroup;
+static_assert(kMStages % kMGroup == 0, "M ring: whole groups");
 constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
-constexpr int kBStages = kSlots;  // factor-slice ring, in lockstep with the staging slots
+#ifndef MLB_TC_BSTAGES
+#define MLB_TC_BSTAGES 6
+#endif
+// factor-slice ring: deeper than the staging slots, because a slice can only be
+// refilled after the MMAs reading it complete and the refill's TMA latency
+// (~1-2k cycles) must be covered (traced: a 4-deep ring lockstepped with the
+// slots left the MMA warps waiting ~1000 cycles per chunk for B).
+constexpr int kBStages = MLB_TC_BSTAGES;
+static_assert(kBStages % 2 == 0, "B ring: even/odd chunk producers own alternate stages");
 constexpr int kBStageBytes = 16384;  // fixed stride (2 r_pad x 128 B <= 16 KB)
 constexpr int kAccStride = 128;   // TMEM columns per accumulator buffer (2 r_pad <= 128)
 constexpr int kStgCol0 = 2 * kAccStride;  // staging slots follow the two accumulators
@@ -120,6 +134,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     if (mbar_try(a, parity)) return;
     if ((i & 255) == 0 && clock64() - t0 > (1ll << 34)) __trap();
   }
+}
+__device__ __forceinline__ void lds128(uint32_t a, float& x, float& y, float& z, float& w) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a) : "memory");
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float x;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a) : "memory");
+  return x;
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
@@ -224,10 +246,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
 // (TMEM base 0, fixed strides), so the operands sit in uniform registers
 // without per-chunk R2UR traffic.  `first` clears the accumulator (window start).
 template <int S, int ACC>
-__device__ __forceinline__ void issue_chunk(uint64_t bdesc0, uint32_t id_full, uint32_t id_hi, uint32_t first) {
+__device__ __forceinline__ void issue_chunk(uint64_t bdesc, uint32_t id_full, uint32_t id_hi, uint32_t first) {
   constexpr uint32_t d = ACC * kAccStride;
   constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
-  constexpr uint64_t boff = (uint64_t)(S * kBStageBytes) >> 4;  // descriptor start-address units
+  constexpr uint64_t boff = 0;  // bdesc addresses the factor-slice stage
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -240,11 +262,23 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc0, uint32_t id_full, u
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%4], %6, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %7, %10, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %8, %10, 1;\n\t}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "r"(a_hi + 8), "r"(a_lo + 8), "l"(bdesc0 + boff), "l"(bdesc0 + boff + 2),
-      "l"(bdesc0 + boff + 4), "l"(bdesc0 + boff + 6), "r"(id_full), "r"(id_hi), "r"(a_hi + 16), "r"(a_lo + 16),
+      "r"(a_hi), "r"(a_lo), "r"(a_hi + 8), "r"(a_lo + 8), "l"(bdesc + boff), "l"(bdesc + boff + 2),
+      "l"(bdesc + boff + 4), "l"(bdesc + boff + 6), "r"(id_full), "r"(id_hi), "r"(a_hi + 16), "r"(a_lo + 16),
       "r"(first), "r"(a_hi + 24), "r"(a_lo + 24)
       : "memory");
 }
+
+// Optional event trace of CTA 0 (build with -DMLB_TC_TRACE=1; tools/tc_trace.py).
+#if MLB_TC_TRACE
+constexpr int kTraceChunks = 4096;
+__device__ long long g_tctrace[8][kTraceChunks];
+#define TCT(ev, gidx)                                                                        \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && (gidx) < kTraceChunks && (threadIdx.x & 31) == 0) g_tctrace[ev][gidx] = clock64(); \
+  } while (0)
+#else
+#define TCT(ev, gidx)
+#endif
 
 struct Params {
   int rows;        // MMA-M extent: m (product 1) or n (product 2)
@@ -279,11 +313,15 @@ __device__ __forceinline__ int own_count(int g0, int n_u, int w) {
 // other's MMAs.
 template <int W>
 __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint64_t bdesc0, uint64_t* ready,
-                                         uint64_t* sdone, uint64_t* afull, uint64_t* aempty) {
+                                         uint64_t* sdone, uint64_t* bfull, uint64_t* bempty, uint64_t* afull,
+                                         uint64_t* aempty) {
   const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
   int g = 0;
   uint32_t aph = 0;
   int lastph[2] = {-1, -1};  // parity of the last commit on slots W and W + 2
+  int lastb[kBStages / 2];   // ... and on this parity's factor-slice stages
+#pragma unroll
+  for (int k = 0; k < kBStages / 2; ++k) lastb[k] = -1;
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
     const int split = u / p.tiles;
     const int c_beg = split * p.chunks_per_split;
@@ -293,15 +331,22 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       const uint32_t sph = (uint32_t)(gg / kSlots) & 1u;
       const int wpos = j % kWindow;
       if (wpos == 0) mbar_wait(smem_u32(&aempty[W]), aph ^ 1);
+      const int bs = gg % kBStages;
       mbar_wait(smem_u32(&ready[slot]), sph);
+      mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(gg / kBStages) & 1u);
+      TCT(4, gg);
       tc_fence_after();
       const uint32_t first = wpos == 0 ? 1u : 0u;
+      const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4);
       if (slot == W)
-        issue_chunk<W, W>(bdesc0, id_full, id_hi, first);
+        issue_chunk<W, W>(bd, id_full, id_hi, first);
       else
-        issue_chunk<W + 2, W>(bdesc0, id_full, id_hi, first);
-      tc_commit(smem_u32(&sdone[slot]));  // slot and B stage reusable once these MMAs finish
+        issue_chunk<W + 2, W>(bd, id_full, id_hi, first);
+      tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
+      tc_commit(smem_u32(&bempty[bs]));    // ... and the factor-slice stage
       lastph[slot >> 1] = (int)sph;
+      lastb[bs >> 1] = (int)((gg / kBStages) & 1);
+      TCT(5, gg);
       if (wpos == kWindow - 1 || i + 2 >= n_u) {
         tc_commit(smem_u32(&afull[W]));
         aph ^= 1;
@@ -313,6 +358,8 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
   // drain: no tcgen05.commit arrival may land after the CTA exits
   for (int k = 0; k < 2; ++k)
     if (lastph[k] >= 0) mbar_wait(smem_u32(&sdone[W + 2 * k]), (uint32_t)lastph[k]);
+  for (int k = 0; k < kBStages / 2; ++k)
+    if (lastb[k] >= 0) mbar_wait(smem_u32(&bempty[2 * k + W]), (uint32_t)lastb[k]);
 }
 
 template <bool TRANS>
@@ -329,27 +376,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* sm_m = base;
   unsigned char* sm_b = base + kMStages * kMTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * kBStageBytes);
-  uint64_t* mfull = bars;                  // [kMPairs]   TMA -> converters (a pair of slices)
-  uint64_t* mempty = mfull + kMPairs;      // [kMPairs]   converters -> TMA
-  uint64_t* ready = mempty + kMPairs;     // [kSlots]    chunk ready for the MMA: 4 converter
-                                           //             arrivals (TMEM slot s written) + the
-                                           //             factor slice's TMA bytes (B stage s)
-  uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters + TMA
-                                           //             (staging slot s and B stage s free)
-  uint64_t* afull = sdone + kSlots;        // [2]         MMA warp w commit -> epilogue
+  uint64_t* mfull = bars;                  // [kMGroups]  TMA -> converters (a group of slices)
+  uint64_t* mempty = mfull + kMGroups;     // [kMGroups]  converters -> TMA
+  uint64_t* ready = mempty + kMGroups;     // [kSlots]    converters -> MMA (TMEM slot s written)
+  uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters (slot s free)
+  uint64_t* bfull = sdone + kSlots;        // [kBStages]  TMA -> MMA (factor slice)
+  uint64_t* bempty = bfull + kBStages;     // [kBStages]  MMA commit -> TMA
+  uint64_t* afull = bempty + kBStages;        // [2]         MMA warp w commit -> epilogue
   uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA warp w
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kMPairs; ++i) {
+    for (int i = 0; i < kMGroups; ++i) {
       mbar_init(smem_u32(&mfull[i]), 1);
-      mbar_init(smem_u32(&mempty[i]), 8);  // both converter groups (4 warps each)
+      mbar_init(smem_u32(&mempty[i]), 4 * kMGroup);  // 4 converter warps per slice
     }
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(smem_u32(&ready[i]), 4 + 1);  // 4 converter warps + the B producer's expect_tx
+      mbar_init(smem_u32(&ready[i]), 4);  // the 4 converter warps
       mbar_init(smem_u32(&sdone[i]), 1);
+    }
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init(smem_u32(&bfull[i]), 1);
+      mbar_init(smem_u32(&bempty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&afull[i]), 1);
@@ -376,39 +426,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpM) {
     // ======================= TMA producer: M slices =======================
     if (lane == 0) {
-      // Slices go out in pairs (chunks g, g + 1) on one barrier, back to back:
-      // for product 1 the two 128-byte row segments of each M row are adjacent
-      // in DRAM, so issuing them together keeps the DRAM page open.
-      int g = 0, pend_tile = 0, pend_c = -1;
-      auto issue_pair = [&](int t1, int c1, int t2, int c2) {
-        const int pg = g >> 1, ps = pg % kMPairs;
-        mbar_wait(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMPairs) & 1u) ^ 1u);
+      // Slices go out in groups of kMGroup consecutive chunks on one barrier,
+      // back to back: for product 1 the 128-byte row segments of consecutive
+      // chunks are adjacent in DRAM, so issuing them together keeps DRAM pages
+      // open (+2-3% over single slices).
+      int g = 0, npend = 0;
+      int pt[kMGroup], pc[kMGroup];
+      auto issue_group = [&]() {
+        const int pg = g / kMGroup, ps = pg % kMGroups;
+        mbar_wait(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMGroups) & 1u) ^ 1u);
         const uint32_t fm = smem_u32(&mfull[ps]);
-        mbar_expect_tx(fm, c2 >= 0 ? 2 * kMTileBytes : kMTileBytes);
-        unsigned char* dst = sm_m + ps * 2 * kMTileBytes;
-        if (!TRANS) {
-          tma_load_2d(smem_u32(dst), &map_m, c1 * kChunk, t1 * 128, fm);
-          if (c2 >= 0) tma_load_2d(smem_u32(dst + kMTileBytes), &map_m, c2 * kChunk, t2 * 128, fm);
-        } else {
-          tma_load_2d(smem_u32(dst), &map_m, t1 * 128, c1 * kChunk, fm);
-          if (c2 >= 0) tma_load_2d(smem_u32(dst + kMTileBytes), &map_m, t2 * 128, c2 * kChunk, fm);
+        mbar_expect_tx(fm, npend * kMTileBytes);
+        for (int k = 0; k < npend; ++k) TCT(0, g + k);
+        unsigned char* dst = sm_m + ps * kMGroup * kMTileBytes;
+        for (int k = 0; k < npend; ++k) {
+          if (!TRANS)
+            tma_load_2d(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm);
+          else
+            tma_load_2d(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm);
         }
-        g += 2;
+        g += kMGroup;
+        npend = 0;
       };
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
         for (int c = c_beg; c < c_end; ++c) {
-          if (pend_c < 0) {
-            pend_tile = tile, pend_c = c;
-          } else {
-            issue_pair(pend_tile, pend_c, tile, c);
-            pend_c = -1;
-          }
+          pt[npend] = tile, pc[npend] = c;
+          if (++npend == kMGroup) issue_group();
         }
       }
-      if (pend_c >= 0) issue_pair(pend_tile, pend_c, 0, -1);
+      if (npend > 0) issue_group();
     }
   } else if (warp == kWarpB) {
     // ======================= TMA producers: factor slices (lanes 0 / 1: even / odd chunks) =======================
@@ -423,10 +472,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
         for (int i = own_first(g, w); i < n_u; i += 2) {
           const int gg = g + i, bs = gg % kBStages;
-          mbar_wait<64>(smem_u32(&sdone[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
-          const uint32_t fb = smem_u32(&ready[bs]);
+          mbar_wait<64>(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
+          const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
           tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
+          TCT(6, gg);
         }
         g += n_u;
       }
@@ -437,9 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the uniform datapath; one elected lane issues each tcgen05 instruction.
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
     if (warp == kWarpMma0)
-      mma_role<0>(p, total_units, bdesc0, ready, sdone, afull, aempty);
+      mma_role<0>(p, total_units, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
     else
-      mma_role<1>(p, total_units, bdesc0, ready, sdone, afull, aempty);
+      mma_role<1>(p, total_units, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
   } else if (warp < kWarpEpi0) {
     // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
     // kConvGroups groups of 4 warps take alternate chunks (more chunks in
@@ -454,25 +504,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
       for (int c = c_beg; c < c_end; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
-        const int pg = g >> 1, ps = pg % kMPairs, slot = g % kSlots;
-        const uint32_t mph = (uint32_t)(pg / kMPairs) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
+        const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots;
+        const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
         mbar_wait(smem_u32(&mfull[ps]), mph);
+        if (q == 0) TCT(1, g);
         // the thread's 32 values of this chunk (its MMA row / TMEM lane)
         float x[32];
-        const unsigned char* tile = sm_m + (ps * 2 + (g & 1)) * kMTileBytes;
+        // shared-window address of the slice (explicit ld.shared: a generic
+        // pointer here compiles to slower generic LD.E)
+        const uint32_t tile = smem_u32(sm_m) + (uint32_t)((ps * kMGroup + g % kMGroup) * kMTileBytes);
         if (!TRANS) {
           // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
-          const float4* rp = reinterpret_cast<const float4*>(tile + row * 128);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 v = rp[j ^ (row & 7)];
-            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-          }
+          for (int j = 0; j < 8; ++j)
+            lds128(tile + row * 128 + ((j ^ (row & 7)) << 4), x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
         } else {
           // column `row` of a 32 x 128 (k x j) tile, no swizzle
-          const float* cp = reinterpret_cast<const float*>(tile) + row;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) x[k] = cp[k * 128];
+          for (int k = 0; k < 32; ++k) x[k] = lds32(tile + (uint32_t)((k * 128 + row) * 4));
+        }
+        // tf32 split in registers before waiting for the staging slot:
+        // hi = rna(x), lo = rna(x - hi); x - hi is exact in fp32 (bit-pattern
+        // round-to-nearest-away == cvt.rna.tf32)
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          hi[k] = (__float_as_uint(x[k]) + 0x1000u) & 0xFFFFE000u;
+          lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
         }
         // The slice was read through the generic proxy and the refill is an
         // async-proxy (TMA) write: order the two before releasing the stage
@@ -480,32 +538,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // seen as ~1e-3 product errors once the M ring runs far ahead).
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&mempty[ps]));  // slice consumed: TMA may refill the pair
+        if (lane == 0) mbar_arrive(smem_u32(&mempty[ps]));  // slice consumed: TMA may refill the group
         mbar_wait(smem_u32(&sdone[slot]), sphase ^ 1);
+        if (q == 0) TCT(2, g);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStgCol0 + slot * 64;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          // tf32 round-to-nearest(-away) on the bit pattern (== cvt.rna.tf32):
-          // hi = rna(x), lo = rna(x - hi); x - hi is exact in fp32
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float v = x[half * 16 + k];
-            hi[k] = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
-            lo[k] = (__float_as_uint(v - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
-          }
-#if !MLB_X_NOST
-          tmem_st16(ta + half * 16, hi);
-          tmem_st16(ta + 32 + half * 16, lo);
-#else
-          if (hi[0] == 0x7fffffff && lo[3] == 1) tmem_st16(ta + half * 16, hi);
-#endif
-        }
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&ready[slot]));
+        if (q == 0) TCT(3, g);
       }
     }
   } else {
@@ -697,8 +741,26 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
-    // split-K so that there are >= ~8 units per SM (balance)
-    int splits = (int)std::max<size_t>(1, cdiv((size_t)sms_ * 8, p.tiles));
+    // split-K: units (tile, K range) are dealt round-robin to the persistent
+    // CTAs, so the kernel lasts ceil(units / SMs) units.  Pick the split factor
+    // that maximises the balanced fraction units / (ceil(units / SMs) * SMs),
+    // charging each extra split its fp64 partial-output traffic (write + reduce
+    // read, 16 B per output element) against the M bytes streamed.
+    int splits = 1;
+    {
+      double best = -1.0;
+      const int smax = std::max(1, std::min(p.nchunks / 8, 64));
+      for (int sp = 1; sp <= smax; ++sp) {
+        const int cps = (int)cdiv(p.nchunks, sp);
+        const int spr = (int)cdiv(p.nchunks, cps);
+        const double units = (double)p.tiles * spr;
+        const double rounds = std::ceil(units / sms_);
+        const double balance = units / (rounds * sms_);
+        const double extra = spr > 1 ? (double)spr * rows * r * 16.0 / ((double)rows * K * 4.0) : 0.0;
+        const double score = balance / (1.0 + extra);
+        if (score > best + 1e-9) best = score, splits = sp;
+      }
+    }
     if (const char* e = getenv("MLB_TC_SPLITS")) splits = std::max(1, atoi(e));  // debug override
     splits = std::min(splits, p.nchunks);
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
@@ -723,6 +785,18 @@ class TcGemmImpl final : public TcGemm {
     if (const char* e = getenv("MLB_TC_GRID")) grid = std::max(1, std::min(grid, atoi(e)));  // debug override
     kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
     TC_CK(cudaGetLastError());
+#if MLB_TC_TRACE
+    if (const char* path = getenv("MLB_TC_TRACE_OUT")) {
+      static long long h[8][tc::kTraceChunks];
+      TC_CK(cudaStreamSynchronize(s));
+      TC_CK(cudaMemcpyFromSymbol(h, tc::g_tctrace, sizeof(h)));
+      std::string f = std::string(path) + (TRANS ? ".C" : ".A");
+      if (FILE* fp = fopen(f.c_str(), "wb")) {
+        fwrite(h, sizeof(h), 1, fp);
+        fclose(fp);
+      }
+    }
+#endif
 
     ++*launches;
     if (p.splits > 1) {
