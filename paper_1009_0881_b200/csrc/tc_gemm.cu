@@ -329,14 +329,17 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
     for (int i = own_first(g, W), j = 0; i < n_u; i += 2, ++j) {
       const int gg = g + i, slot = gg % kSlots;
       const uint32_t sph = (uint32_t)(gg / kSlots) & 1u;
-      const int wpos = j % kWindow;
-      if (wpos == 0) mbar_wait(smem_u32(&aempty[W]), aph ^ 1);
+      // accumulator 1's windows are offset by half a window (its first one
+      // is kWindow / 2 long), so the two accumulators fill -- and stall their
+      // warps for the drain -- at alternating times, not together
+      const int wpos = (j + W * (kWindow / 2)) % kWindow;
+      if (wpos == 0 || j == 0) mbar_wait(smem_u32(&aempty[W]), aph ^ 1);
       const int bs = gg % kBStages;
       mbar_wait(smem_u32(&ready[slot]), sph);
       mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(gg / kBStages) & 1u);
       TCT(4, gg);
       tc_fence_after();
-      const uint32_t first = wpos == 0 ? 1u : 0u;
+      const uint32_t first = (wpos == 0 || j == 0) ? 1u : 0u;
       const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4);
       if (slot == W)
         issue_chunk<W, W>(bd, id_full, id_hi, first);
@@ -556,7 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= epilogue: fp32 windows -> fp64 =======================
     // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32.
     // Per unit, windows are drained in a fixed order (window k of accumulator
-    // 0, then of accumulator 1), so the fp64 sums are deterministic.
+    // 1, then of accumulator 0 -- their completion order), so the fp64 sums
+    // are deterministic.
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int cb = ((warp - kWarpEpi0) >> 2) * 32;
@@ -568,13 +572,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = u % p.tiles, split = u / p.tiles;
       const int c_beg = split * p.chunks_per_split;
       const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+      const int c1 = own_count(g, n_u, 1);
       const int nw0 = (own_count(g, n_u, 0) + kWindow - 1) / kWindow;
-      const int nw1 = (own_count(g, n_u, 1) + kWindow - 1) / kWindow;
+      const int nw1 = c1 > 0 ? (c1 + kWindow / 2 + kWindow - 1) / kWindow : 0;  // first window is half length
 #pragma unroll
       for (int k = 0; k < 32; ++k) sum[k] = 0.0;
       for (int k = 0; k < max(nw0, nw1); ++k) {
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
+        for (int ww = 0; ww < 2; ++ww) {
+          const int w = 1 - ww;  // window k of accumulator 1 completes before window k of accumulator 0
           if (k >= (w ? nw1 : nw0)) continue;
           mbar_wait<256>(smem_u32(&afull[w]), aph[w]);
           tc_fence_after();
