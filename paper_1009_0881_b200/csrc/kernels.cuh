@@ -344,7 +344,7 @@ __device__ __forceinline__ void ld4_shared(const double* p, double* o) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_sqerr_tiled(const T* __restrict__ M, const T* __restrict__ V,
+__global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M, const T* __restrict__ V,
                                                      const T* __restrict__ W, size_t m, size_t n, int r,
                                                      double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -381,19 +381,23 @@ __global__ void __launch_bounds__(256) k_sqerr_tiled(const T* __restrict__ M, co
 #pragma unroll
       for (int b = 0; b < 8; ++b) acc[a][b] = fma(va[a], wb[b], acc[a][b]);
   }
+  // squared residuals: each row's 8 terms summed in T, then in fp64 (the
+  // per-element fp64 convert + FMA would make the kernel fp64-pipe bound)
   double s = 0.0;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const size_t i = i0 + (a >> 2) * 64 + ty * 4 + (a & 3);
     if (i >= m) continue;
+    T sr = T(0);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const size_t j = j0 + (b >> 2) * 64 + tx * 4 + (b & 3);
       if (j < n) {
-        const double d = (double)M[i * n + j] - (double)acc[a][b];
-        s = fma(d, d, s);
+        const T d = M[i * n + j] - acc[a][b];
+        sr = fma(d, d, sr);
       }
     }
+    s += (double)sr;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
