@@ -361,6 +361,13 @@ struct Engine::Impl {
     const size_t n = e->n_loc_;
     const size_t cb = ceil_div(n, 128);
     const size_t tiled_smem = 2 * (size_t)r * 128 * sizeof(T);
+    if (!exact() && use_tc(L.m)) {
+      // tensor-core residual (3xTF32 V W on tcgen05, fp32 residuals, fp64 sums)
+      tc->sqerr(static_cast<const T*>(L.M), static_cast<const T*>(L.V), W.as<T>(), L.m, n, (size_t)r, out, s,
+                &e->launches_);
+      allreduce_sum(out, 1);
+      return;
+    }
     if (!exact() && tiled_smem <= 200 * 1024) {
       // register-tiled residual: one fp64 partial per 128 x 128 tile
       const size_t rb = ceil_div(L.m, 128), nb = cb * rb;

@@ -647,12 +647,243 @@ __global__ void k_split_factor(const float* __restrict__ F, float* __restrict__ 
   }
 }
 
+// out[0] = sum of part[0..count) in a fixed order (one block)
+__global__ void k_sum_parts(const double* __restrict__ part, int count, double* __restrict__ out) {
+  __shared__ double ws[32];
+  double s = 0.0;
+  for (int e = threadIdx.x; e < count; e += blockDim.x) s += part[e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    out[0] = t;
+  }
+}
+
 // out[e] = sum_z part[z][e], z ascending (deterministic split-K epilogue)
 __global__ void k_split_reduce(const double* __restrict__ part, size_t count, int splits, double* __restrict__ out) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
     double s = part[e];
     for (int z = 1; z < splits; ++z) s += part[(size_t)z * count + e];
     out[e] = s;
+  }
+}
+
+
+// ----------------------------------------------------------------------------
+// Direct residual ||M - V W||_F^2 on the tensor cores (frobenius_error,
+// proj/src/matrix.cpp:37-42; the trace sample of run_solver_phase).
+// Per tile (128 columns J of M) x (64 rows I of M):
+//   P^T[j][i] = sum_k W[k][j] V[i][k]   (3xTF32: W^T_hi V_hi + W^T_hi V_lo + W^T_lo V_hi)
+// in TMEM (M_mma = 128 columns j, N = 64 rows i, K = r_pad), then the epilogue
+// sums (M[i][j] - P[i][j])^2 in fp32 per 32 and fp64 across.  Operands come
+// pre-split, K-major, row width 2 * rpa (hi | lo), rpa = r_pad rounded up to
+// whole 128-byte swizzle atoms.  A (W^T tile) stays in shared memory for all I
+// tiles of a J tile; each I tile's V slice and M tile (TMA, 4 boxes of 64 rows
+// x 128 B) stream through a 2-stage ring.  (Per-lane global loads of M ran at
+// 0.9 TB/s; the TMA-staged tile reads it at the HBM rate.)
+// ----------------------------------------------------------------------------
+constexpr int kRThreads = (2 + 8) * 32;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-9 epilogue
+constexpr int kRAtomBytes = 128 * 128;    // one 128-row x 32-fp32 SW128 box
+constexpr int kRMBytes = 64 * 128 * 4;     // M tile: 64 rows i x 128 columns j
+
+// X -> S (rows x 2 rpa): [rna(x) | rna(x - rna(x))], zero padded.  trans: X is
+// r x rows (W, row-major) and row j of S comes from column j of X.
+__global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S, int r, int rpa, size_t rows,
+                             int trans) {
+  const size_t total = (size_t)rows * rpa;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t j, k;
+    if (trans) k = e / rows, j = e % rows;  // coalesced reads of W rows
+    else j = e / rpa, k = e % rpa;
+    float hi = 0.f, lo = 0.f;
+    if ((int)k < r) {
+      const float x = trans ? X[k * rows + j] : X[j * r + k];
+      hi = __uint_as_float(tf32_rna(x));
+      lo = __uint_as_float(tf32_rna(x - hi));
+    }
+    S[j * 2 * rpa + k] = hi;
+    S[j * 2 * rpa + rpa + k] = lo;
+  }
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+struct RParams {
+  const float* M;
+  int m, n, r, rp, atoms;  // atoms = rpa / 32
+  int tj, ti;              // tile counts along n (J) and m (I)
+  double* part;            // [gridDim.x] per-CTA sums
+};
+
+__global__ void __launch_bounds__(kRThreads, 1)
+    k_tc_residual(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_v,
+                  const __grid_constant__ CUtensorMap map_m, const RParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int opa = 2 * p.atoms * kRAtomBytes;      // W^T tile: 128 j x 2 rpa (hi atoms, then lo atoms)
+  const int opb = 2 * p.atoms * kRAtomBytes / 2;  // V tile: 64 i x 2 rpa
+  const int stage = opb + kRMBytes;               // V tile + M tile (64 i x 128 j, four 32-column boxes)
+  unsigned char* sm_a = base;
+  unsigned char* sm_s = base + opa;               // 2 stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_s + 2 * stage);
+  uint64_t* afull = bars;       // A landed
+  uint64_t* aempty = bars + 1;  // MMAs of the J tile done
+  uint64_t* sfull = bars + 2;   // [2] V + M tile landed
+  uint64_t* sempty = bars + 4;  // [2] MMAs done (V) and epilogue done (M): 1 commit + 8 warps
+  uint64_t* cfull = bars + 6;   // [2] accumulator ready for the epilogue
+  uint64_t* cempty = bars + 8;  // [2] epilogue done with the accumulator
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 10);
+  __shared__ double red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(afull), 1);
+    mbar_init(smem_u32(aempty), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), 1 + 8);
+      mbar_init(smem_u32(&cfull[i]), 1);
+      mbar_init(smem_u32(&cempty[i]), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  double s64 = 0.0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int jc = 0, tc_ = 0;
+      for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
+        mbar_wait(smem_u32(aempty), ((uint32_t)jc & 1u) ^ 1u);
+        mbar_expect_tx(smem_u32(afull), (uint32_t)opa);
+        for (int h = 0; h < 2; ++h)
+          for (int a = 0; a < p.atoms; ++a)
+            tma_load_2d(smem_u32(sm_a + (h * p.atoms + a) * kRAtomBytes), &map_w, h * p.atoms * 32 + a * 32, jt * 128,
+                        smem_u32(afull));
+        for (int it = 0; it < p.ti; ++it, ++tc_) {
+          const int st = tc_ & 1;
+          unsigned char* sb = sm_s + st * stage;
+          mbar_wait(smem_u32(&sempty[st]), ((uint32_t)(tc_ >> 1) & 1u) ^ 1u);
+          mbar_expect_tx(smem_u32(&sfull[st]), (uint32_t)stage);
+          for (int h = 0; h < 2; ++h)
+            for (int a = 0; a < p.atoms; ++a)
+              tma_load_2d(smem_u32(sb + (h * p.atoms + a) * (kRAtomBytes / 2)), &map_v, h * p.atoms * 32 + a * 32,
+                          it * 64, smem_u32(&sfull[st]));
+          for (int b = 0; b < 4; ++b)  // M rows i of the tile, 32 columns j per box
+            tma_load_2d(smem_u32(sb + opb + b * (kRMBytes / 4)), &map_m, jt * 128 + b * 32, it * 64,
+                        smem_u32(&sfull[st]));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t id = idesc_tf32(64);
+    const uint64_t da = sdesc_sw128(smem_u32(sm_a)), ds = sdesc_sw128(smem_u32(sm_s));
+    const uint64_t lo_a = (uint64_t)((p.atoms * kRAtomBytes) >> 4), lo_b = (uint64_t)((p.atoms * kRAtomBytes / 2) >> 4);
+    const int ksteps = p.rp / 8;
+    int jc = 0, tc_ = 0;
+    int lasts[2] = {-1, -1};
+    int lasta = -1;
+    for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
+      mbar_wait(smem_u32(afull), (uint32_t)jc & 1u);
+      for (int it = 0; it < p.ti; ++it, ++tc_) {
+        const int st = tc_ & 1, acc = tc_ & 1;
+        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;
+        mbar_wait(smem_u32(&cempty[acc]), ph ^ 1u);
+        mbar_wait(smem_u32(&sfull[st]), ph);
+        tc_fence_after();
+        const uint32_t d = (uint32_t)(acc * 64);
+        const uint64_t dbs = ds + (uint64_t)((st * stage) >> 4);
+        for (int kk = 0; kk < ksteps; ++kk) {
+          const uint64_t oa = (uint64_t)(((kk >> 2) * kRAtomBytes + (kk & 3) * 32) >> 4);
+          const uint64_t ob = (uint64_t)(((kk >> 2) * (kRAtomBytes / 2) + (kk & 3) * 32) >> 4);
+          mma_ss(d, da + oa, dbs + ob, id, kk > 0 ? 1u : 0u);   // W_hi V_hi
+          mma_ss(d, da + oa, dbs + lo_b + ob, id, 1u);          // W_hi V_lo
+          mma_ss(d, da + lo_a + oa, dbs + ob, id, 1u);          // W_lo V_hi
+        }
+        tc_commit(smem_u32(&sempty[st]));  // V tile free (the M tile is released by the epilogue)
+        tc_commit(smem_u32(&cfull[acc]));
+        lasts[st] = (int)ph;
+        __syncwarp();
+      }
+      tc_commit(smem_u32(aempty));
+      lasta = jc & 1;
+      __syncwarp();
+    }
+    // no commit arrival may land after exit: wait for the last sempty phase of
+    // each stage (its 8 epilogue arrivals follow the commit) and for aempty
+    for (int st = 0; st < 2; ++st)
+      if (lasts[st] >= 0) mbar_wait(smem_u32(&sempty[st]), (uint32_t)lasts[st]);
+    if (lasta >= 0) mbar_wait(smem_u32(aempty), (uint32_t)lasta);
+  } else {
+    // epilogue: lane quarter q (TMEM lane = column j of M), half h (rows i of the tile)
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    int tc_ = 0;
+    for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x) {
+      const int jl = q * 32 + lane, j = jt * 128 + jl;
+      const int b = jl >> 5, jb = jl & 31;  // M box and column within it
+      for (int it = 0; it < p.ti; ++it, ++tc_) {
+        const int acc = tc_ & 1, st = tc_ & 1;
+        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;
+        mbar_wait<128>(smem_u32(&cfull[acc]), ph);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + h * 32, v);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&cempty[acc]));
+        // M[i][j] from the staged tile (SW128 rows of 32 fp32: a warp reads one
+        // 128-byte row per load, conflict-free)
+        const uint32_t mt = smem_u32(sm_s + st * stage + opb + b * (kRMBytes / 4));
+        const int i0 = it * 64 + h * 32;
+        float s32 = 0.f;
+#pragma unroll
+        for (int ii = 0; ii < 32; ++ii) {
+          const int il = h * 32 + ii;
+          const float mval = lds32(mt + il * 128 + ((((jb >> 2) ^ (il & 7)) << 4) | ((jb & 3) << 2)));
+          const float dlt = mval - __uint_as_float(v[ii]);
+          s32 = (j < p.n && i0 + ii < p.m) ? fmaf(dlt, dlt, s32) : s32;
+        }
+        s64 += (double)s32;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sempty[st]));  // M tile read
+      }
+    }
+  }
+  // per-CTA sum (fixed order: deterministic)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+  if (warp >= 2 && lane == 0) red[warp - 2] = s64;
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    p.part[blockIdx.x] = t;
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
   }
 }
 
@@ -703,6 +934,8 @@ class TcGemmImpl final : public TcGemm {
   ~TcGemmImpl() override {
     if (split_) cudaFree(split_);
     if (part_) cudaFree(part_);
+    if (rv_) cudaFree(rv_);
+    if (rw_) cudaFree(rw_);
   }
   bool active() const override { return true; }
   bool supports(size_t m, size_t n, size_t r) const override {
@@ -721,6 +954,50 @@ class TcGemmImpl final : public TcGemm {
   void vtm(const float* V, const float* M, size_t m, size_t n, size_t r, double* C, cudaStream_t s,
            long* launches) override {
     run<true>(M, V, m, n, r, C, s, launches);
+  }
+
+  void sqerr(const float* M, const float* V, const float* W, size_t m, size_t n, size_t r, double* out,
+             cudaStream_t s, long* launches) override {
+    if (!supports(m, n, r)) throw std::invalid_argument("tcgen05 residual: unsupported shape");
+    const int rp = (int)cdiv(r, 16) * 16;
+    const int rpa = (int)cdiv(rp, 32) * 32;
+    ensure(&rv_, &rv_bytes_, (size_t)m * 2 * rpa * 4);
+    ensure(&rw_, &rw_bytes_, (size_t)n * 2 * rpa * 4);
+    {
+      const unsigned gv = (unsigned)std::min<size_t>(cdiv((size_t)m * rpa, 256), 16384);
+      const unsigned gw = (unsigned)std::min<size_t>(cdiv((size_t)n * rpa, 256), 16384);
+      tc::k_split_rows<<<gv, 256, 0, s>>>(V, static_cast<float*>(rv_), (int)r, rpa, m, 0);
+      tc::k_split_rows<<<gw, 256, 0, s>>>(W, static_cast<float*>(rw_), (int)r, rpa, n, 1);
+      TC_CK(cudaGetLastError());
+      *launches += 2;
+    }
+    tc::RParams p{};
+    p.M = M;
+    p.m = (int)m;
+    p.n = (int)n;
+    p.r = (int)r;
+    p.rp = rp;
+    p.atoms = rpa / 32;
+    p.tj = (int)cdiv(n, 128);
+    p.ti = (int)cdiv(m, 64);
+    const int grid = std::min(p.tj, sms_);
+    ensure(&part_, &part_bytes_, (size_t)grid * 8);
+    p.part = static_cast<double*>(part_);
+    const CUtensorMap mw = make_map(rw_, (uint64_t)2 * rpa, n, 32, 128, true);
+    const CUtensorMap mv = make_map(rv_, (uint64_t)2 * rpa, m, 32, 64, true);
+    const CUtensorMap mm = make_map(M, n, m, 32, 64, true);
+    const size_t opa = (size_t)2 * p.atoms * tc::kRAtomBytes;
+    const size_t smem = 1024 + opa + 2 * (opa / 2 + tc::kRMBytes) + 256;
+    if (!resid_attr_) {
+      const size_t smax = 1024 + 4 * tc::kRAtomBytes + 2 * (2 * tc::kRAtomBytes + tc::kRMBytes) + 256;
+      TC_CK(cudaFuncSetAttribute(tc::k_tc_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      resid_attr_ = true;
+    }
+    tc::k_tc_residual<<<grid, tc::kRThreads, smem, s>>>(mw, mv, mm, p);
+    TC_CK(cudaGetLastError());
+    tc::k_sum_parts<<<1, 256, 0, s>>>(static_cast<const double*>(part_), grid, out);
+    TC_CK(cudaGetLastError());
+    *launches += 2;
   }
 
  private:
@@ -828,6 +1105,10 @@ class TcGemmImpl final : public TcGemm {
   void* part_ = nullptr;
   size_t part_bytes_ = 0;
   bool attr_set_[2] = {false, false};
+  void* rv_ = nullptr;  // residual operands: V and W^T split into [hi | lo] rows
+  void* rw_ = nullptr;
+  size_t rv_bytes_ = 0, rw_bytes_ = 0;
+  bool resid_attr_ = false;
 };
 
 }  // namespace

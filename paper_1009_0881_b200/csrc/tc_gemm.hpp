@@ -19,6 +19,11 @@ class TcGemm {
                    long* launches) = 0;
   virtual void vtm(const float* V, const float* M, size_t m, size_t n, size_t r, double* C, cudaStream_t s,
                    long* launches) = 0;
+  // ||M - V W||_F^2 into the device scalar out[0] (3xTF32 V W, fp32 residuals
+  // summed in fp64); same shape support as the products
+  virtual void sqerr(const float* M, const float* V, const float* W, size_t m, size_t n, size_t r, double* out,
+                     cudaStream_t s, long* launches) = 0;
+  void sqerr(const double*, const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
   // fp64 storage never takes the tensor path (kept for the templated engine)
   void mwt(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
   void vtm(const double*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
