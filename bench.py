@@ -46,6 +46,20 @@ def env_int(k, d):
         return d
 
 
+TRAFFIC_SRC = "profiles/r01_traffic_config4.json (ncu dram__bytes_read+write per launch, 1 GPU)"
+
+
+def traffic_for(kernel, world):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of this
+    workload (profiles/); None if absent or not the 1-GPU configuration."""
+    p = os.path.join(REPO, "profiles", "r01_traffic_config4.json")
+    if world != 1 or not os.path.exists(p):
+        return None
+    with open(p) as f:
+        k = json.load(f)["kernels"].get(kernel)
+    return k["traffic_bytes"] if k else None
+
+
 def peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -289,7 +303,8 @@ def run_b200(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": dom, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic_for(dom, world), "kernel": dom,
+                     "peak_source": peak_src, "traffic_source": TRAFFIC_SRC,
                      "algorithmic_bytes_per_launch": bytes_per_pass,
                      "avg_ms": {"A = M W^T": mwt_ms, "C = V^T M": vtm_ms},
                      "step_frac_in_products": (mwt_ms + vtm_ms) / (ms_max / args.steps)},
