@@ -288,6 +288,7 @@ def run_b200(args):
         s.close()
 
     ttt = time_to_target(P, local, gemm) if (args.ttt and world == 1) else None
+    small = small_configs(P, local, args.cpu_baseline) if (args.small and world == 1) else None
 
     if rank != 0:
         return
@@ -315,6 +316,8 @@ def run_b200(args):
         line["e2e"] = e2e
     if ttt:
         line["time_to_target"] = ttt
+    if small:
+        line["small_configs"] = small
     if args.cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
@@ -342,6 +345,46 @@ def run_e2e(P, host, local, gemm, iters, norm):
             "call": f"mlnmf_session_set_data + mlnmf_session_run_configuration(levels=1, hals, none, r=64, "
                     f"work:{iters}, trace_every=0) + mlnmf_session_get_factors; pinned host fp32",
             "iters_per_call": steps, "wall_s": wall, "final_rel_error": float(tr.error[-1]) / norm}
+
+
+def small_configs(P, local, with_cpu):
+    """BASELINE configs 0-3 (L2-resident, launch/latency bound):
+    HALS single-level sweeps/s on the device (fp32 storage, SIMT fp64-accumulate
+    products, data generated on the device, trace_every=0, 100 sweeps), next to
+    the reference's own hals_step (oracle/_ref, fp64, OpenMP on all host cores)
+    timed on the same host for 3 steps."""
+    out = {}
+    ref = None
+    if with_cpu:
+        import oracle
+        if oracle.Reference.available():
+            ref, restated = oracle.Reference(), oracle.Restated()
+    for cfg in (0, 1, 2, 3):
+        c = P.GEN_CONFIGS[cfg]
+        with P.Session(device=local, dtype=P.F32) as s:
+            s.generate(cfg, seed=0)
+            s.run_configuration(1, "hals", "none", c["r"], 0, 5.0, 0)  # warm-up (graphs, buffers)
+            s.sync()
+            t0 = time.perf_counter()
+            tr = s.run_configuration(1, "hals", "none", c["r"], 0, 100.0, 0)
+            s.sync()
+            wall = time.perf_counter() - t0
+        steps = int(tr.phase_steps.sum())
+        e = {"shape": f"{c['h']}x{c['w']} (m={c['h'] * c['w']}) x n={c['n']}, r={c['r']}",
+             "gpu_it_s": steps / wall, "gpu_ms_per_step": wall / steps * 1e3}
+        if ref is not None:
+            M = oracle.generate_config(cfg, restated=restated)
+            V, W = ref.random_init(M.shape[0], M.shape[1], c["r"], 0)
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                V, W, _ = ref.hals_step(M, V, W)
+                ts.append(time.perf_counter() - t0)
+            e["cpu_ref_ms_per_step"] = float(np.median(ts)) * 1e3
+            e["cpu_cores"] = os.cpu_count() or 1
+            e["speedup"] = e["cpu_ref_ms_per_step"] / e["gpu_ms_per_step"]
+        out[f"config{cfg}"] = e
+    return out
 
 
 def time_to_target(P, local, gemm):
@@ -376,6 +419,7 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-ttt", dest="ttt", action="store_false")
+    ap.add_argument("--no-small", dest="small", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

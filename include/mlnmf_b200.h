@@ -133,6 +133,14 @@ int mlnmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* V_out
  * X is (h*w) x ncols (restrict) or (ceil(h/2)*ceil(w/2)) x ncols (prolong). */
 int mlnmf_restrict_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
 int mlnmf_prolong_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
+/* run_bench's runs loop (proj/include/mlnmf/bench.hpp:34, proj/src/bench.cpp:28-84):
+ * final_errors[i] = run_configuration(M, grid, level_count, kind, cycle, rank,
+ * base_seed + i, budget, trace_every = 0).trace.final_error() for i < runs,
+ * batched over `workers` concurrent device sessions (0 = 8).  opt: storage and
+ * precision of the sessions (NULL = the one-shot defaults); single rank. */
+int mlnmf_run_seeds(const mlnmf_options* opt, const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                    size_t level_count, int kind, int cycle, size_t rank, uint64_t base_seed, size_t runs,
+                    int budget_mode, double budget_amount, size_t workers, double* final_errors);
 /* Dry run of the host scheduler (no device work): the phase allocations,
  * steps per phase and the (work_units, level) stamps of every trace sample a
  * work-unit-budget run_configuration on an h x w grid with n columns would

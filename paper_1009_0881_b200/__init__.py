@@ -188,6 +188,8 @@ _proto("mlnmf_run_configuration", C.c_int, _dp, _sz, _sz, _sz, _sz, _sz, C.c_int
        C.c_int, C.c_double, _sz, _dp, _dp, C.POINTER(_vp))
 _proto("mlnmf_run_cycle", C.c_int, _dp, _sz, _sz, _sz, _sz, _sz, _sz, _dp, _dp, _sz, C.c_int, C.c_int, C.c_int,
        C.c_double, _sz, _dp, _dp, C.POINTER(_vp))
+_proto("mlnmf_run_seeds", C.c_int, C.POINTER(_Options), _dp, _sz, _sz, _sz, _sz, _sz, C.c_int, C.c_int, _sz,
+       C.c_uint64, _sz, C.c_int, C.c_double, _sz, _dp)
 _proto("mlnmf_run_solver", C.c_int, _dp, _sz, _sz, _dp, _dp, _sz, C.c_int, C.c_int, C.c_double, _sz, _dp, _dp,
        C.POINTER(_vp))
 _proto("mlnmf_mu_step", C.c_int, _dp, _sz, _sz, _dp, _dp, _sz)
@@ -280,9 +282,13 @@ def _take_trace(tp: int) -> RunTrace:
 # ---------------------------------------------------------------------------
 # default-session options of the one-shot calls
 # ---------------------------------------------------------------------------
+_default_opts = [0, F64, 0, GEMM_AUTO, ERROR_AUTO, 1, 0, None]
+
+
 def set_default_options(device=0, dtype=F64, exact=False, gemm_path=GEMM_AUTO, error_mode=ERROR_AUTO):
     o = _Options(device, dtype, int(bool(exact)), gemm_path, error_mode, 1, 0, None)
     _check(_lib.mlnmf_set_default_options(C.byref(o)))
+    _default_opts[:] = [device, dtype, int(bool(exact)), gemm_path, error_mode, 1, 0, None]
 
 
 # ---------------------------------------------------------------------------
@@ -308,6 +314,90 @@ def run_configuration(M, grid: ImageGrid, level_count: int, kind, cycle, rank: i
                                       C.byref(tp))
     _check(rc)
     return MultilevelResult(V, W, _take_trace(tp.value))
+
+
+# ---------------------------------------------------------------------------
+# run_bench (proj/include/mlnmf/bench.hpp:15-45, proj/src/bench.cpp:28-84)
+# ---------------------------------------------------------------------------
+@dataclass
+class BenchConfig:
+    algorithms: list = field(default_factory=lambda: ["hals"])
+    cycles: list = field(default_factory=lambda: ["none"])
+    level_counts: list = field(default_factory=lambda: [1])
+    rank: int = 1
+    runs: int = 1
+    budget: object = None
+    base_seed: int = 0
+
+
+@dataclass
+class BenchEntry:
+    algorithm: str
+    cycle: str
+    levels: int
+    runs: int = 0
+    mean: float = 0.0
+    stddev: float = 0.0
+    min: float = 0.0
+    max: float = 0.0
+    skipped: bool = False
+    note: str = ""
+    errors: Optional[np.ndarray] = None
+
+
+def run_seeds(M, grid: ImageGrid, level_count: int, kind, cycle, rank: int, base_seed: int, runs: int, budget,
+              workers: int = 8, dtype=None, exact=None) -> np.ndarray:
+    """Final errors of run_configuration(..., seed = base_seed + i, trace_every = 0)
+    for i < runs, batched over `workers` concurrent device sessions."""
+    M = _f64(M)
+    m, n = M.shape
+    mode, amount = _budget(budget)
+    o = _Options(*_default_opts)
+    if dtype is not None:
+        o.dtype = dtype
+    if exact is not None:
+        o.exact = int(bool(exact))
+    out = np.zeros(runs)
+    _check(_lib.mlnmf_run_seeds(C.byref(o), _d(M), m, n, grid.height, grid.width, level_count, _kind(kind),
+                                _cycle(cycle), rank, base_seed, runs, mode, amount, workers, _d(out)))
+    return out
+
+
+def run_bench(M, grid: Optional[ImageGrid], cfg: BenchConfig, workers: int = 8, dtype=None, exact=None):
+    """run_bench (bench.cpp:28-84): for every algorithm x cycle x level count,
+    `runs` seeded run_configuration calls (trace_every = 0), summarised by the
+    mean / sample stddev / min / max of the final error; the same skip rules.
+    The runs of one entry execute concurrently on `workers` device sessions."""
+    if cfg.runs < 1:
+        raise ValueError("run_bench: runs >= 1")
+    M = _f64(M)
+    entries = []
+    for algo in cfg.algorithms:
+        for cycle in cfg.cycles:
+            for levels in cfg.level_counts:
+                e = BenchEntry(str(algo), str(cycle), int(levels))
+                if _cycle(cycle) == CycleKind.kSingleLevel and levels != 1:
+                    e.skipped, e.note = True, "single-level runs use exactly one level"
+                    entries.append(e)
+                    continue
+                if levels > 1 and grid is None:
+                    e.skipped, e.note = True, "dataset has no pixel grid"
+                    entries.append(e)
+                    continue
+                g = grid if grid is not None else ImageGrid(M.shape[0], 1)
+                try:
+                    errs = run_seeds(M, g, levels, algo, cycle, cfg.rank, cfg.base_seed, cfg.runs, cfg.budget,
+                                     workers, dtype, exact)
+                except ValueError as ex:
+                    e.skipped, e.note = True, str(ex)
+                    entries.append(e)
+                    continue
+                e.runs = len(errs)
+                e.mean = float(errs.sum() / len(errs))
+                e.stddev = float(np.sqrt(((errs - e.mean) ** 2).sum() / (len(errs) - 1))) if len(errs) > 1 else 0.0
+                e.min, e.max, e.errors = float(errs.min()), float(errs.max()), errs
+                entries.append(e)
+    return entries
 
 
 @dataclass

@@ -9,6 +9,7 @@
 #include <tuple>
 #include <vector>
 #include <algorithm>
+#include <thread>
 
 #include "../../include/mlnmf_b200.h"
 #include "engine.hpp"
@@ -193,6 +194,57 @@ int mlnmf_run_cycle(const double* M, size_t m, size_t n, size_t grid_h, size_t g
     run_cycle(e, levels, r, to_kind(kind), to_cycle(cycle), budget_mode, amount, trace_every, t);
     e.get_factors(0, V_out, W_out, MLNMF_F64);
     emit_trace(std::move(t), trace_out);
+  });
+}
+
+// run_bench's inner loop (proj/src/bench.cpp:28-84), batched: seeds
+// base_seed .. base_seed + runs - 1 of run_configuration(trace_every = 0) on
+// one M.  `workers` host threads each own a device session (own stream, own
+// copy of M) and take seeds round-robin, so independent runs overlap on the
+// GPU; every seed's result is the same as a lone run's (each run is
+// deterministic and touches only its own session).
+int mlnmf_run_seeds(const mlnmf_options* opt, const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                    size_t level_count, int kind, int cycle, size_t rank, uint64_t base_seed, size_t runs,
+                    int budget_mode, double amount, size_t workers, double* final_errors) {
+  return guard([&] {
+    if (!M || !final_errors) throw std::invalid_argument("run_seeds: null buffer");
+    if (runs < 1) throw std::invalid_argument("run_bench: runs >= 1");
+    if (level_count < 1) throw std::invalid_argument("run_configuration: need at least one level");
+    mlnmf_options o = opt ? *opt : g_default;
+    o.world = 1;
+    o.rank = 0;
+    o.nccl_id = nullptr;
+    const Kind k = to_kind(kind);
+    const Cycle c = to_cycle(cycle);
+    const size_t nw = std::max<size_t>(1, std::min(workers ? workers : 8, runs));
+    std::vector<std::string> errs(nw);
+    std::vector<int> codes(nw, MLNMF_OK);
+    auto body = [&](size_t w) {
+      codes[w] = guard([&] {
+        Engine e(to_opts(&o));
+        e.set_data(M, MLNMF_F64, false, m, n, n, 0, grid_h, grid_w, false);
+        for (size_t i = w; i < runs; i += nw) {
+          RunTrace t;
+          run_configuration(e, level_count, k, c, rank, base_seed + i, budget_mode, amount, 0, t);
+          final_errors[i] = t.samples.back().error;
+        }
+      });
+      if (codes[w] != MLNMF_OK) errs[w] = g_err;
+    };
+    std::vector<std::thread> th;
+    for (size_t w = 1; w < nw; ++w) th.emplace_back(body, w);
+    body(0);
+    for (auto& t : th) t.join();
+    for (size_t w = 0; w < nw; ++w)
+      if (codes[w] != MLNMF_OK) {
+        g_err = errs[w];
+        switch (codes[w]) {
+          case MLNMF_ERR_INVALID: throw std::invalid_argument(errs[w]);
+          case MLNMF_ERR_NNLS_CAP: throw NnlsCapExceeded(errs[w]);
+          case MLNMF_ERR_DATA: throw DataError(errs[w]);
+          default: throw std::runtime_error(errs[w]);
+        }
+      }
   });
 }
 

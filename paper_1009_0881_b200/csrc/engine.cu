@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <map>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -34,8 +37,25 @@ namespace mlb {
                                __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")");       \
   } while (0)
 
+// Device-allocation epoch: bumped by every (re)allocation of engine or
+// tensor-path buffers.  A captured step graph is valid only for the epoch it
+// was captured in (its kernels hold raw buffer pointers).
+std::atomic<uint64_t> g_dev_epoch{1};
+
 namespace {
 constexpr int kTargetBlocks = 2 * 148;
+
+template <typename T>
+cudaError_t dev_malloc(T** p, size_t b) {
+  g_dev_epoch.fetch_add(1);
+  return cudaMalloc(reinterpret_cast<void**>(p), b);
+}
+void dev_free(void* p) {
+  if (p) {
+    g_dev_epoch.fetch_add(1);
+    cudaFree(p);
+  }
+}
 constexpr size_t kSmemMax = 227 * 1024;
 
 size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
@@ -45,13 +65,13 @@ struct DevBuf {
   size_t bytes = 0;
   void ensure(size_t b) {
     if (b <= bytes) return;
-    if (p) CK(cudaFree(p));
+    dev_free(p);
     p = nullptr;
-    CK(cudaMalloc(&p, b));
+    CK(dev_malloc(&p, b));
     bytes = b;
   }
   void release() {
-    if (p) cudaFree(p);
+    dev_free(p);
     p = nullptr;
     bytes = 0;
   }
@@ -92,8 +112,21 @@ struct Engine::Impl {
   std::vector<cudaEvent_t> ev_pool;
   std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
   TcGemm* tc = nullptr;
+  // captured steady-state steps (HALS / MU, single rank): key level * 4 + kind
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t epoch = 0;
+    long nlaunch = 0;
+    bool warm = false;
+  };
+  std::map<size_t, StepGraph> graphs;
+  bool graphs_on = std::getenv("MLNMF_NO_GRAPHS") == nullptr;
 
   explicit Impl(Engine* eng) : e(eng) {}
+  ~Impl() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  }
 
   size_t esz() const { return e->opt_.dtype == 0 ? 4 : 8; }
   bool exact() const { return e->opt_.exact != 0; }
@@ -133,7 +166,7 @@ struct Engine::Impl {
   int splits_for(size_t tiles, size_t K) const {
     if (exact()) return 1;
     size_t sp = ceil_div(kTargetBlocks, tiles);
-    sp = std::min(sp, ceil_div(K, 256));
+    sp = std::min(sp, ceil_div(K, 64));  // >= 2 K-steps of 32 per split
     return (int)std::max<size_t>(sp, 1);
   }
 
@@ -481,9 +514,9 @@ Engine::~Engine() {
   if (!impl_) return;
   cudaStreamSynchronize(impl_->s);
   for (auto& L : lv_) {
-    cudaFree(L.M);
-    cudaFree(L.V);
-    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+    dev_free(L.M);
+    dev_free(L.V);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   for (DevBuf* b : {&impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
                     &impl_->samples, &impl_->counts, &impl_->flags, &impl_->tstart, &impl_->stage})
@@ -526,8 +559,8 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   if (m == 0 || n_loc == 0) throw std::invalid_argument("Matrix: dimensions must be positive");
   if (h * w != m) throw std::invalid_argument("GridHierarchy: grid does not match matrix rows");
   for (auto& L : lv_) {
-    cudaFree(L.M), cudaFree(L.V);
-    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+    dev_free(L.M), dev_free(L.V);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();
   n_loc_ = n_loc;
@@ -535,7 +568,7 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   col0_ = col0;
   Level L0{h, w, m};
   const size_t count = m * n_loc, es = impl_->esz();
-  CK(cudaMalloc(&L0.M, count * es));
+  CK(dev_malloc(&L0.M, count * es));
   lv_.push_back(L0);
   cudaStream_t s = impl_->s;
   const size_t hs = host_dtype == 0 ? 4 : 8;
@@ -571,15 +604,15 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
   const size_t m = g.h * g.w;
   // allocate level 0
   for (auto& L : lv_) {
-    cudaFree(L.M), cudaFree(L.V);
-    cudaFree(L.Rp), cudaFree(L.Ri), cudaFree(L.Rw), cudaFree(L.Pp), cudaFree(L.Pi), cudaFree(L.Pw);
+    dev_free(L.M), dev_free(L.V);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();
   n_loc_ = n_loc;
   n_total_ = n_total;
   col0_ = col0;
   Level L0{g.h, g.w, m};
-  CK(cudaMalloc(&L0.M, m * n_loc * impl_->esz()));
+  CK(dev_malloc(&L0.M, m * n_loc * impl_->esz()));
   lv_.push_back(L0);
   cudaStream_t s = impl_->s;
   const int r = (int)g.r;
@@ -634,9 +667,9 @@ void Engine::ensure_levels(size_t L) {
     if (cur.h < 2 || cur.w < 2) throw std::invalid_argument("GridHierarchy: too many levels for this grid");
     HostCsr R = build_restriction(cur.h, cur.w), P = build_prolongation(cur.h, cur.w);
     auto up = [&](const HostCsr& op, int** p, int** i, double** w) {
-      CK(cudaMalloc(p, op.rowptr.size() * 4));
-      CK(cudaMalloc(i, op.idx.size() * 4));
-      CK(cudaMalloc(w, op.wt.size() * 8));
+      CK(dev_malloc(p, op.rowptr.size() * 4));
+      CK(dev_malloc(i, op.idx.size() * 4));
+      CK(dev_malloc(w, op.wt.size() * 8));
       CK(cudaMemcpy(*p, op.rowptr.data(), op.rowptr.size() * 4, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(*i, op.idx.data(), op.idx.size() * 4, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(*w, op.wt.data(), op.wt.size() * 8, cudaMemcpyHostToDevice));
@@ -645,7 +678,7 @@ void Engine::ensure_levels(size_t L) {
     up(P, &cur.Pp, &cur.Pi, &cur.Pw);
     Level nx{(cur.h + 1) / 2, (cur.w + 1) / 2, 0};
     nx.m = nx.h * nx.w;
-    CK(cudaMalloc(&nx.M, nx.m * n_loc_ * es));
+    CK(dev_malloc(&nx.M, nx.m * n_loc_ * es));
     const size_t colblocks = ceil_div(n_loc_, 256);
     if (opt_.dtype == 0)
       impl_->launch(k_csr_apply<float>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
@@ -655,7 +688,7 @@ void Engine::ensure_levels(size_t L) {
       impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
                     (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M), nx.m,
                     n_loc_, colblocks);
-    if (r_ > 0) CK(cudaMalloc(&nx.V, nx.m * r_ * es));
+    if (r_ > 0) CK(dev_malloc(&nx.V, nx.m * r_ * es));
     lv_.push_back(nx);
   }
   CK(cudaStreamSynchronize(impl_->s));
@@ -695,13 +728,13 @@ void Engine::set_factors(size_t l, const void* V, const void* W, int host_dtype,
   const size_t es = impl_->esz();
   if (r != r_) {
     for (auto& L : lv_) {
-      cudaFree(L.V);
+      dev_free(L.V);
       L.V = nullptr;
     }
     r_ = r;
   }
   for (auto& L : lv_)
-    if (!L.V) CK(cudaMalloc(&L.V, L.m * r * es));
+    if (!L.V) CK(dev_malloc(&L.V, L.m * r * es));
   impl_->W.ensure(r * n_loc_ * es);
   impl_->AB.ensure((lv_[0].m * r + r * r) * 8);
   impl_->Cb.ensure(r * n_loc_ * 8);
@@ -796,6 +829,58 @@ void Engine::step(size_t l, Kind kind) {
   if (l >= lv_.size()) throw std::invalid_argument("step: level not built");
   if (r_ == 0) throw std::invalid_argument("step: factors not initialised");
   if (impl_->CD_valid && impl_->CD_level != l) impl_->CD_valid = false;
+  Impl& im = *impl_;
+  // Steady-state HALS / MU steps replay a captured CUDA graph: the step is a
+  // fixed sequence of ~10 small launches, launch-bound on the L2-resident
+  // configs.  (ANLS appends NNLS counts at moving offsets; multi-rank steps
+  // hold NCCL calls; profiling records events: those run eagerly.)
+  const bool graphable = im.graphs_on && kind != kAnls && opt_.world <= 1 && !profiling_;
+  if (graphable) {
+    Impl::StepGraph& g = im.graphs[l * 4 + (size_t)kind];
+    if (!g.exec || g.epoch != g_dev_epoch.load()) {
+      if (!g.warm) {  // one eager step first: buffers reach their steady-state sizes
+        g.warm = true;
+        im.B_valid = false;
+        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        else im.step_t<double>(l, kind);
+        return;
+      }
+      if (g.exec) cudaGraphExecDestroy(g.exec), g.exec = nullptr;
+      const uint64_t ep = g_dev_epoch.load();
+      const long l0 = launches_;
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(im.s, cudaStreamCaptureModeRelaxed));
+      im.B_valid = false;  // the captured step always recomputes B = W W^T
+      try {
+        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        else im.step_t<double>(l, kind);
+      } catch (...) {
+        cudaStreamEndCapture(im.s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      CK(cudaStreamEndCapture(im.s, &graph));
+      g.nlaunch = launches_ - l0;
+      launches_ = l0;
+      if (g_dev_epoch.load() != ep) {  // an allocation happened during capture: run eagerly, recapture next time
+        cudaGraphDestroy(graph);
+        g.warm = false;
+        im.B_valid = false;
+        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        else im.step_t<double>(l, kind);
+        return;
+      }
+      CK(cudaGraphInstantiate(&g.exec, graph, 0));
+      cudaGraphDestroy(graph);
+      g.epoch = ep;
+    }
+    CK(cudaGraphLaunch(g.exec, im.s));
+    launches_ += g.nlaunch;
+    im.B_valid = false;
+    im.CD_valid = true;
+    im.CD_level = l;
+    return;
+  }
   if (opt_.dtype == 0) impl_->step_t<float>(l, kind);
   else impl_->step_t<double>(l, kind);
 }

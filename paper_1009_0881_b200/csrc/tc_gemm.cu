@@ -1092,6 +1092,7 @@ class TcGemmImpl final : public TcGemm {
 
   static void ensure(void** p, size_t* have, size_t need) {
     if (need <= *have) return;
+    g_dev_epoch.fetch_add(1);  // invalidates captured step graphs holding the old pointer
     if (*p) TC_CK(cudaFree(*p));
     *p = nullptr;
     TC_CK(cudaMalloc(p, need));

@@ -2,10 +2,15 @@
 // M-streaming products at fp32 storage (tc_gemm.cu):
 //   A (m x r, fp64) = M (m x n) W^T      and      C (r x n, fp64) = V^T M.
 #pragma once
+#include <atomic>
 #include <cstddef>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace mlb {
+
+// device-allocation epoch (engine.cu): bumped on every buffer (re)allocation
+extern std::atomic<uint64_t> g_dev_epoch;
 
 class TcGemm {
  public:

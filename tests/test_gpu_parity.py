@@ -345,3 +345,25 @@ def test_rank64_hals_exact_bitwise(P, restated):
         P.set_default_options(exact=False)
     check_trace(res.trace, to, 0.0, exact=True)
     assert np.array_equal(res.V, Vo) and np.array_equal(res.W, Wo)
+
+
+def test_run_bench_acceptance8_batched(P):
+    """run_bench (bench.cpp:28-84) batched over concurrent device sessions
+    reproduces the reference's acceptance-criterion-8 runs seed by seed:
+    synth 65x65, n=40, r=8, work:300, seeds 100..119 (fixture from the
+    unmodified reference), fp64 exact mode -> identical final errors, and the
+    published means (acceptance.cpp:359-386)."""
+    import os
+    A = np.load(os.path.join(os.path.dirname(__file__), "golden", "acceptance8.npz"))
+    cfg = P.BenchConfig(algorithms=["mu", "hals"], cycles=["none", "fmg"], level_counts=[1, 3], rank=8, runs=20,
+                        budget=300.0, base_seed=100)
+    entries = P.run_bench(A["M"], P.ImageGrid(65, 65), cfg, workers=6, dtype=P.F64, exact=True)
+    got = {(e.algorithm, e.cycle, e.levels): e for e in entries}
+    assert got[("mu", "none", 3)].skipped and got[("hals", "fmg", 1)].skipped is False
+    expect = {"mu_none": 9.691148, "mu_fmg": 8.924942, "hals_none": 8.251099, "hals_fmg": 8.091289}
+    for k, mean in expect.items():
+        algo, cyc = k.split("_")
+        e = got[(algo, cyc, 1 if cyc == "none" else 3)]
+        assert not e.skipped and e.runs == 20
+        assert np.array_equal(e.errors, A[k]), k
+        assert round(e.mean, 6) == mean
