@@ -62,6 +62,9 @@ constexpr int kMGroup = MLB_TC_MGROUP;       // the ring is filled and released 
 constexpr int kMGroups = kMStages / kMGroup;
 static_assert(kMStages % kMGroup == 0, "M ring: whole groups");
 constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
+#ifndef MLB_TC_BSINGLE
+#define MLB_TC_BSINGLE 1  // one thread issues every factor slice in stream order
+#endif
 #ifndef MLB_TC_BSTAGES
 #define MLB_TC_BSTAGES 6
 #endif
@@ -70,7 +73,11 @@ constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
 // (~1-2k cycles) must be covered (traced: a 4-deep ring lockstepped with the
 // slots left the MMA warps waiting ~1000 cycles per chunk for B).
 constexpr int kBStages = MLB_TC_BSTAGES;
-static_assert(kBStages % 2 == 0, "B ring: even/odd chunk producers own alternate stages");
+#ifndef MLB_TC_BPREFETCH
+#define MLB_TC_BPREFETCH 0
+#endif
+constexpr int kBPrefetch = MLB_TC_BPREFETCH;  // factor slices prefetched into L2 this many chunks ahead
+static_assert(MLB_TC_BSINGLE || kBStages % 2 == 0, "B ring: even/odd chunk producers own alternate stages");
 constexpr int kBStageBytes = 16384;  // fixed stride (2 r_pad x 128 B <= 16 KB)
 constexpr int kAccStride = 128;   // TMEM columns per accumulator buffer (2 r_pad <= 128)
 constexpr int kStgCol0 = 2 * kAccStride;  // staging slots follow the two accumulators
@@ -142,6 +149,11 @@ __device__ __forceinline__ float lds32(uint32_t a) {
   float x;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a) : "memory");
   return x;
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
@@ -319,9 +331,9 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
   int g = 0;
   uint32_t aph = 0;
   int lastph[2] = {-1, -1};  // parity of the last commit on slots W and W + 2
-  int lastb[kBStages / 2];   // ... and on this parity's factor-slice stages
+  int lastb[kBStages];       // ... and on the factor-slice stages this warp used
 #pragma unroll
-  for (int k = 0; k < kBStages / 2; ++k) lastb[k] = -1;
+  for (int k = 0; k < kBStages; ++k) lastb[k] = -1;
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
     const int split = u / p.tiles;
     const int c_beg = split * p.chunks_per_split;
@@ -348,7 +360,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
       tc_commit(smem_u32(&bempty[bs]));    // ... and the factor-slice stage
       lastph[slot >> 1] = (int)sph;
-      lastb[bs >> 1] = (int)((gg / kBStages) & 1);
+      lastb[bs] = (int)((gg / kBStages) & 1);
       TCT(5, gg);
       if (wpos == kWindow - 1 || i + 2 >= n_u) {
         tc_commit(smem_u32(&afull[W]));
@@ -361,8 +373,8 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
   // drain: no tcgen05.commit arrival may land after the CTA exits
   for (int k = 0; k < 2; ++k)
     if (lastph[k] >= 0) mbar_wait(smem_u32(&sdone[W + 2 * k]), (uint32_t)lastph[k]);
-  for (int k = 0; k < kBStages / 2; ++k)
-    if (lastb[k] >= 0) mbar_wait(smem_u32(&bempty[2 * k + W]), (uint32_t)lastb[k]);
+  for (int k = 0; k < kBStages; ++k)
+    if (lastb[k] >= 0) mbar_wait(smem_u32(&bempty[k]), (uint32_t)lastb[k]);
 }
 
 template <bool TRANS>
@@ -466,6 +478,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= TMA producers: factor slices (lanes 0 / 1: even / odd chunks) =======================
     // Own warp: the B ring (freed only when a chunk's MMAs complete) must not
     // throttle the M stream, and one parity's stall must not block the other.
+#if MLB_TC_BSINGLE
+    if (lane == 0) {
+      // one thread, all chunks in stream order, spin without sleeping
+      int g = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int split = u / p.tiles;
+        const int c_beg = split * p.chunks_per_split;
+        const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+        for (int i = 0; i < n_u; ++i) {
+          const int gg = g + i, bs = gg % kBStages;
+          mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
+          const uint32_t fb = smem_u32(&bfull[bs]);
+          mbar_expect_tx(fb, b_bytes);
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
+          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
+          TCT(6, gg);
+        }
+        g += n_u;
+      }
+    }
+#else
     const int w = lane;
     if (lane < 2) {
       int g = 0;
@@ -479,11 +512,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
           tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
+          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
         g += n_u;
       }
     }
+#endif
   } else if (warp == kWarpMma0 || warp == kWarpMma1) {
     // ======================= MMA issuers (one per parity) =======================
     // The whole warp runs the (warp-uniform) loop so every MMA operand stays in
