@@ -391,14 +391,15 @@ def time_to_target(P, local, gemm):
     """Time-to-target relative error: target = the
     single-level (cycle none) final relative error at work:20; report the
     elapsed time of the first finest-level sample at or below it for none and
-    FMG (5 levels), traced every 2 steps."""
+    NI / VC / FMG (5 levels), traced every 2 steps."""
     out = {}
     with P.Session(device=local, dtype=P.F32, gemm_path=gemm) as s:
         s.generate(CFG, seed=0)
         norm = float(np.sqrt(s.norm2(0)))
         runs = {"none": s.run_configuration(1, "hals", "none", RANK, 0, 20.0, 2)}
         target = float(runs["none"].error[-1]) / norm
-        runs["fmg"] = s.run_configuration(LEVELS, "hals", "fmg", RANK, 0, 20.0, 2)
+        for cyc in ("ni", "vc", "fmg"):
+            runs[cyc] = s.run_configuration(LEVELS, "hals", cyc, RANK, 0, 20.0, 2)
         out["target_rel_error"] = target
         for cyc, tr in runs.items():
             rel = tr.error / norm

@@ -367,3 +367,19 @@ def test_run_bench_acceptance8_batched(P):
         assert not e.skipped and e.runs == 20
         assert np.array_equal(e.errors, A[k]), k
         assert round(e.mean, 6) == mean
+
+
+@pytest.mark.parametrize("cycle", ["none", "ni"])
+def test_wall_clock_budget(P, cfg0, cycle):
+    """Budget::Mode::kWallClockSeconds (solvers.cpp:318-320,340): phases run
+    until their share of the wall-clock budget is spent; the trace spans the
+    budget, allocations sum to it, and the error decreases."""
+    T = 0.3
+    res = P.run_configuration(cfg0, P.ImageGrid(32, 32), 3, "hals", cycle, 20, 0,
+                              P.Budget(P.BudgetMode.kWallClockSeconds, T), 0)
+    tr = res.trace
+    assert int(tr.phase_steps.sum()) > 10
+    assert abs(float(tr.alloc_amount.sum()) - T) < 1e-12 * max(1.0, T) + 1e-12
+    assert tr.elapsed_s[-1] >= 0.9 * T
+    assert tr.error[-1] < tr.error[0]
+    assert tr.level[-1] == 1
