@@ -61,7 +61,20 @@ constexpr int kMStages = MLB_TC_MSTAGES;  // M-slice ring (TMA -> converters), 1
 constexpr int kMGroup = MLB_TC_MGROUP;       // the ring is filled and released in groups of slices
 constexpr int kMGroups = kMStages / kMGroup;
 static_assert(kMStages % kMGroup == 0, "M ring: whole groups");
-constexpr int kSlots = 4;         // TMEM staging slots (hi|lo, 64 columns each)
+#ifndef MLB_TC_K3
+#define MLB_TC_K3 1
+#endif
+// K3 form: D[:, 0:r) += [A_hi A_lo A_hi] . [F_hi F_hi F_lo]^T as one r-column
+// accumulation (12 N = r MMAs per chunk); else the stacked form
+// D[:, 0:2r) += A_hi [F_hi;F_lo]^T, D[:, 0:r) += A_lo F_hi^T (2r columns).
+constexpr bool kK3 = MLB_TC_K3 != 0;
+#ifndef MLB_TC_ACCBUFS
+#define MLB_TC_ACCBUFS 2
+#endif
+// accumulator buffers per MMA warp: with 2, a warp starts its next window
+// while the epilogue drains the previous one (K3 form only: 4 x r_pad columns)
+constexpr int kAccBufs = kK3 ? MLB_TC_ACCBUFS : 1;
+constexpr int kSlots = kK3 ? (512 - 2 * kAccBufs * 64) / 64 : 4;  // TMEM staging slots (hi|lo, 64 columns each)
 #ifndef MLB_TC_BSINGLE
 #define MLB_TC_BSINGLE 1  // one thread issues every factor slice in stream order
 #endif
@@ -79,12 +92,12 @@ constexpr int kBStages = MLB_TC_BSTAGES;
 constexpr int kBPrefetch = MLB_TC_BPREFETCH;  // factor slices prefetched into L2 this many chunks ahead
 static_assert(MLB_TC_BSINGLE || kBStages % 2 == 0, "B ring: even/odd chunk producers own alternate stages");
 constexpr int kBStageBytes = 16384;  // fixed stride (2 r_pad x 128 B <= 16 KB)
-constexpr int kAccStride = 128;   // TMEM columns per accumulator buffer (2 r_pad <= 128)
-constexpr int kStgCol0 = 2 * kAccStride;  // staging slots follow the two accumulators
-static_assert(kStgCol0 + kSlots * 64 == 512, "TMEM map: 2 accumulators + staging = 512 columns");
+constexpr int kAccStride = kK3 ? 64 : 128;  // TMEM columns per accumulator (r_pad or 2 r_pad)
+constexpr int kStgCol0 = 2 * kAccBufs * kAccStride;  // staging slots follow the accumulators
+static_assert(kStgCol0 + kSlots * 64 == 512, "TMEM map: accumulators + staging = 512 columns");
 constexpr int kChunk = 32;        // K elements per pipeline chunk (128 B rows)
 #ifndef MLB_TC_WINDOW
-#define MLB_TC_WINDOW 8
+#define MLB_TC_WINDOW 6
 #endif
 constexpr int kWindow = MLB_TC_WINDOW;  // chunks per fp32 accumulation window
 constexpr int kConvGroups = 2;    // converter groups of 4 warps (alternate chunks)
@@ -159,6 +172,26 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+// TMA load with an L2 cache-policy hint (createpolicy): the M stream is read
+// once (evict_first) and must not push out the factor slices, which every CTA
+// of the split re-reads (evict_last).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -280,6 +313,38 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc, uint32_t id_full, ui
       : "memory");
 }
 
+// K3 chunk: the accumulator holds only the r output columns; the three 3xTF32
+// terms are one K = 96 accumulation, A = [A_hi A_lo A_hi] from the TMEM slot
+// (A_hi re-read, not stored twice), B = [F_hi F_hi F_lo] from the factor slice
+// (rows 0..r_pad of the stage, then rows r_pad..2 r_pad).  Half the TMEM
+// columns of the stacked form, so 6 staging slots fit and the epilogue drains
+// half as much.
+template <int S, int ACC>
+__device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first) {
+  constexpr uint32_t d = ACC * kAccStride;
+  constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.u32 p, %12, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %4, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %5, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %6, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%16], %4, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%17], %5, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%18], %6, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %7, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %8, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %9, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %10, %11, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2),
+      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24),
+      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24)
+      : "memory");
+}
+
 // Optional event trace of CTA 0 (build with -DMLB_TC_TRACE=1; tools/tc_trace.py).
 #if MLB_TC_TRACE
 constexpr int kTraceChunks = 4096;
@@ -301,6 +366,7 @@ struct Params {
   int splits;      // split-K factor
   int chunks_per_split;
   int nchunks;     // ceil(kdim / 32)
+  int rotate;      // rotate each tile's chunk order (product 1)
   double* part;    // [splits][...] fp64 partial outputs
 };
 
@@ -313,6 +379,19 @@ struct Params {
 // staging slot and B stage.  Within a unit, the chunks of parity w are
 // i = i0(w), i0(w) + 2, ... with i0(w) = (w - g0) & 1.
 __device__ __forceinline__ int own_first(int g0, int w) { return (w - g0) & 1; }
+
+// Chunk order within a unit is rotated per tile: for product 1 concurrent CTAs
+// work on different 128-row tiles, and rows n * 4 bytes apart (1 MiB at
+// config 4) at the same column offset land on the same DRAM channels
+// (partition camping).  Starting each tile at a different chunk spreads the
+// concurrent row segments over the address space.  Both producers use the
+// same order; everything downstream follows the stream position.
+__device__ __forceinline__ int unit_chunk(const Params& p, int tile, int c_beg, int n_u, int i) {
+  if (!p.rotate) return c_beg + i;
+  const int rot = (int)(((long long)tile * 97) % n_u);
+  const int k = i + rot;
+  return c_beg + (k >= n_u ? k - n_u : k);
+}
 __device__ __forceinline__ int own_count(int g0, int n_u, int w) {
   const int i0 = own_first(g0, w);
   return n_u > i0 ? (n_u - i0 + 1) >> 1 : 0;
@@ -329,8 +408,10 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
                                          uint64_t* aempty) {
   const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
   int g = 0;
-  uint32_t aph = 0;
-  int lastph[2] = {-1, -1};  // parity of the last commit on slots W and W + 2
+  int wc = 0;  // windows this warp has opened (all units): buffer wc % kAccBufs
+  int lastph[kSlots / 2];    // parity of the last commit on this warp's slots W, W + 2, ...
+#pragma unroll
+  for (int k = 0; k < kSlots / 2; ++k) lastph[k] = -1;
   int lastb[kBStages];       // ... and on the factor-slice stages this warp used
 #pragma unroll
   for (int k = 0; k < kBStages; ++k) lastb[k] = -1;
@@ -345,7 +426,8 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       // is kWindow / 2 long), so the two accumulators fill -- and stall their
       // warps for the drain -- at alternating times, not together
       const int wpos = (j + W * (kWindow / 2)) % kWindow;
-      if (wpos == 0 || j == 0) mbar_wait(smem_u32(&aempty[W]), aph ^ 1);
+      const int abuf = wc % kAccBufs, abar = W * kAccBufs + abuf;
+      if (wpos == 0 || j == 0) mbar_wait(smem_u32(&aempty[abar]), ((uint32_t)(wc / kAccBufs) & 1u) ^ 1u);
       const int bs = gg % kBStages;
       mbar_wait(smem_u32(&ready[slot]), sph);
       mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(gg / kBStages) & 1u);
@@ -353,25 +435,41 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       tc_fence_after();
       const uint32_t first = (wpos == 0 || j == 0) ? 1u : 0u;
       const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4);
-      if (slot == W)
-        issue_chunk<W, W>(bd, id_full, id_hi, first);
-      else
-        issue_chunk<W + 2, W>(bd, id_full, id_hi, first);
+      TCT(7, gg);  // issue start (after the waits and the fence)
+      if constexpr (kK3) {
+        const uint64_t bd_lo = bd + ((uint64_t)(p.rp * 128) >> 4);  // F_lo rows of the stage
+        constexpr int A0 = W * kAccBufs, A1 = W * kAccBufs + (kAccBufs > 1 ? 1 : 0);
+        const int sidx = slot >> 1;  // this warp's slots are W, W + 2, ...
+        if (abuf == 0) {
+          if (sidx == 0) issue_chunk3<W, A0>(bd, bd_lo, id_hi, first);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0>(bd, bd_lo, id_hi, first);
+          else issue_chunk3<(W + 4) % kSlots, A0>(bd, bd_lo, id_hi, first);
+        } else {
+          if (sidx == 0) issue_chunk3<W, A1>(bd, bd_lo, id_hi, first);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1>(bd, bd_lo, id_hi, first);
+          else issue_chunk3<(W + 4) % kSlots, A1>(bd, bd_lo, id_hi, first);
+        }
+      } else {
+        if (slot == W)
+          issue_chunk<W, W>(bd, id_full, id_hi, first);
+        else
+          issue_chunk<(W + 2) % kSlots, W>(bd, id_full, id_hi, first);
+      }
       tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
       tc_commit(smem_u32(&bempty[bs]));    // ... and the factor-slice stage
       lastph[slot >> 1] = (int)sph;
       lastb[bs] = (int)((gg / kBStages) & 1);
       TCT(5, gg);
       if (wpos == kWindow - 1 || i + 2 >= n_u) {
-        tc_commit(smem_u32(&afull[W]));
-        aph ^= 1;
+        tc_commit(smem_u32(&afull[abar]));
+        ++wc;
       }
       __syncwarp();
     }
     g += n_u;
   }
   // drain: no tcgen05.commit arrival may land after the CTA exits
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < kSlots / 2; ++k)
     if (lastph[k] >= 0) mbar_wait(smem_u32(&sdone[W + 2 * k]), (uint32_t)lastph[k]);
   for (int k = 0; k < kBStages; ++k)
     if (lastb[k] >= 0) mbar_wait(smem_u32(&bempty[k]), (uint32_t)lastb[k]);
@@ -397,9 +495,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters (slot s free)
   uint64_t* bfull = sdone + kSlots;        // [kBStages]  TMA -> MMA (factor slice)
   uint64_t* bempty = bfull + kBStages;     // [kBStages]  MMA commit -> TMA
-  uint64_t* afull = bempty + kBStages;        // [2]         MMA warp w commit -> epilogue
-  uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA warp w
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2);
+  uint64_t* afull = bempty + kBStages;     // [2 x kAccBufs] MMA warp w commit -> epilogue
+  uint64_t* aempty = afull + 2 * kAccBufs; // [2 x kAccBufs] epilogue -> MMA warp w
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2 * kAccBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -416,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&bfull[i]), 1);
       mbar_init(smem_u32(&bempty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2 * kAccBufs; ++i) {
       mbar_init(smem_u32(&afull[i]), 1);
       mbar_init(smem_u32(&aempty[i]), 8);
     }
@@ -447,6 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // open (+2-3% over single slices).
       int g = 0, npend = 0;
       int pt[kMGroup], pc[kMGroup];
+      const uint64_t pol_m = l2_policy_evict_first();
       auto issue_group = [&]() {
         const int pg = g / kMGroup, ps = pg % kMGroups;
         mbar_wait(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMGroups) & 1u) ^ 1u);
@@ -456,9 +555,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* dst = sm_m + ps * kMGroup * kMTileBytes;
         for (int k = 0; k < npend; ++k) {
           if (!TRANS)
-            tma_load_2d(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm);
+            tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm, pol_m);
           else
-            tma_load_2d(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm);
+            tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm, pol_m);
         }
         g += kMGroup;
         npend = 0;
@@ -467,8 +566,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-        for (int c = c_beg; c < c_end; ++c) {
-          pt[npend] = tile, pc[npend] = c;
+        for (int i = 0; i < c_end - c_beg; ++i) {
+          pt[npend] = tile, pc[npend] = unit_chunk(p, tile, c_beg, c_end - c_beg, i);
           if (++npend == kMGroup) issue_group();
         }
       }
@@ -481,9 +580,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if MLB_TC_BSINGLE
     if (lane == 0) {
       // one thread, all chunks in stream order, spin without sleeping
+      const uint64_t pol_b = l2_policy_evict_last();
       int g = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int split = u / p.tiles;
+        const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
         for (int i = 0; i < n_u; ++i) {
@@ -491,7 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
+          tma_load_2d_hint(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, tile, c_beg, n_u, i) * kChunk, 0,
+                           fb, pol_b);
           if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
@@ -503,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane < 2) {
       int g = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int split = u / p.tiles;
+        const int tile = u % p.tiles, split = u / p.tiles;
         const int c_beg = split * p.chunks_per_split;
         const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
         for (int i = own_first(g, w); i < n_u; i += 2) {
@@ -511,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait<64>(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, (c_beg + i) * kChunk, 0, fb);
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, tile, c_beg, n_u, i) * kChunk, 0, fb);
           if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
@@ -600,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const int cb = ((warp - kWarpEpi0) >> 2) * 32;
     const bool live = cb < p.rp;
-    uint32_t aph[2] = {0, 0};
+    int wcnt[2] = {0, 0};  // windows drained per accumulator warp (all units)
     int g = 0;
     double sum[32];
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
@@ -617,12 +718,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ww = 0; ww < 2; ++ww) {
           const int w = 1 - ww;  // window k of accumulator 1 completes before window k of accumulator 0
           if (k >= (w ? nw1 : nw0)) continue;
-          mbar_wait<256>(smem_u32(&afull[w]), aph[w]);
+          const int ab = wcnt[w] % kAccBufs, abar = w * kAccBufs + ab;
+          mbar_wait<256>(smem_u32(&afull[abar]), (uint32_t)(wcnt[w] / kAccBufs) & 1u);
           tc_fence_after();
           if (live) {
-            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + w * kAccStride + cb;
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + abar * kAccStride + cb;
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {  // main part, then the F_lo part of the stacked accumulator, 16 cols each
+            for (int h = 0; h < (kK3 ? 2 : 4); ++h) {  // 16 cols each (stacked form: then the F_lo part)
               uint32_t v[16];
               tmem_ld16(ta + (h >> 1) * p.rp + (h & 1) * 16, v);
               tmem_wait_ld();
@@ -632,8 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&aempty[w]));
-          aph[w] ^= 1;
+          if (lane == 0) mbar_arrive(smem_u32(&aempty[abar]));
+          ++wcnt[w];
         }
       }
       g += n_u;
@@ -1059,6 +1161,10 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
+    // rotate for product 1 when M rows are >= 1 MiB apart (measured: +3.5 % at
+    // n = 262144; at 256 KiB strides it costs the L2 sharing of factor slices)
+    p.rotate = (!TRANS && n * 4 >= ((size_t)1 << 20)) ? 1 : 0;
+    if (const char* e = getenv("MLB_TC_ROTATE")) p.rotate = atoi(e);  // debug override
     // split-K: units (tile, K range) are dealt round-robin to the persistent
     // CTAs, so the kernel lasts ceil(units / SMs) units.  Pick the split factor
     // that maximises the balanced fraction units / (ceil(units / SMs) * SMs),
