@@ -151,13 +151,16 @@ struct Engine::Impl {
   }
 
   // ---------------- collectives ----------------
+  // collectives run whenever a communicator exists: world > 1, or a 1-rank
+  // communicator requested by passing an NCCL id with world = 1 (exercises the
+  // NCCL path on one GPU)
   void allreduce_sum(double* p, size_t count) {
-    if (e->opt_.world <= 1) return;
+    if (!comm) return;
     auto& api = NcclApi::get();
     nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclSum, comm, s), "allreduce");
   }
   void allreduce_max(double* p, size_t count) {
-    if (e->opt_.world <= 1) return;
+    if (!comm) return;
     auto& api = NcclApi::get();
     nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclMax, comm, s), "allreduce max");
   }
@@ -289,7 +292,7 @@ struct Engine::Impl {
     const bool needB = !B_valid;
     if (needB) gram_W<T>();
     product_mwt<T>(l);
-    if (e->opt_.world > 1) {
+    if (comm) {
       if (needB && L.m == e->lv_[0].m) {
         allreduce_sum(A(), L.m * r + r * r);  // A|B contiguous: one collective
       } else {
@@ -502,7 +505,7 @@ Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
   impl_->scal.ensure(64);
   impl_->tstart.ensure(8);
   impl_->tc = make_tc_gemm(o.dtype == 0 && o.gemm != 1, o.gemm == 2);
-  if (o.world > 1) {
+  if (o.world > 1 || o.has_nccl_id) {
     if (!o.has_nccl_id) throw std::invalid_argument("world > 1 needs an NCCL unique id");
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_id, sizeof(id));
@@ -834,7 +837,7 @@ void Engine::step(size_t l, Kind kind) {
   // fixed sequence of ~10 small launches, launch-bound on the L2-resident
   // configs.  (ANLS appends NNLS counts at moving offsets; multi-rank steps
   // hold NCCL calls; profiling records events: those run eagerly.)
-  const bool graphable = im.graphs_on && kind != kAnls && opt_.world <= 1 && !profiling_;
+  const bool graphable = im.graphs_on && kind != kAnls && !im.comm && !profiling_;
   if (graphable) {
     Impl::StepGraph& g = im.graphs[l * 4 + (size_t)kind];
     if (!g.exec || g.epoch != g_dev_epoch.load()) {

@@ -5,35 +5,37 @@
 //   product 2 (TRANS = true):   C^T (n x r) = M^T (n x m) . V      (solvers.cpp:91,124,273)
 //
 // Both stream M from HBM exactly once.  MMA operand roles (M = 128 rows of the
-// MMA, N = 2 r_pad, K = 8 per tcgen05.mma, kind::tf32):
+// MMA, N = r_pad, K = 8 per tcgen05.mma, kind::tf32):
 //   A operand: a 128 x 32 slice of M (product 1) or of M^T (product 2), split
 //              by the converter warps into tf32 hi = rna(x) and lo = rna(x - hi)
-//              and written straight into TMEM (tcgen05.st) -- no shared-memory
-//              round trip, so the MMA's A reads never touch shared memory.
+//              and written straight into a TMEM staging slot (tcgen05.st).
 //   B operand: [F_hi ; F_lo] (2 r_pad x 32, K-major, SWIZZLE_128B) where F is
 //              W (product 1) or V^T (product 2), pre-split once per step by a
-//              tiny kernel and brought in by TMA next to the M slice.
-// Per K-step two MMAs:  D[:, 0:2r) += A_hi [F_hi;F_lo]^T   (N = 2 r_pad)
-//                       D[:, 0:r)  += A_lo  F_hi^T          (N = r_pad)
-// so D[:, 0:r) + D[:, r:2r) = A_hi F_hi + A_hi F_lo + A_lo F_hi (3xTF32).
+//              small kernel and brought in by TMA.
+// K3 form (default): per 32-K chunk, 12 MMAs of N = r_pad accumulate
+//   D[:, 0:r) += [A_hi A_lo A_hi] . [F_hi F_hi F_lo]^T = A_hi F_hi + A_lo F_hi + A_hi F_lo
+// (3xTF32) into an r-column accumulator; A_hi is re-read from the slot, F_hi /
+// F_lo are rows 0..r_pad / r_pad..2 r_pad of the factor stage.  (The stacked
+// form, 4 MMAs of N = 2 r_pad + 4 of N = r_pad into 2 r_pad columns, is kept
+// behind MLB_TC_K3=0.)
 // fp32 TMEM accumulation is limited to windows of kWindow chunks; the
-// epilogue warps drain each window into fp64 registers (double-buffered
-// accumulators), and write fp64 split-K partials that a deterministic reduce
-// sums in fixed order.
-// Why windows: the tensor core's fp32 accumulate truncates, so on the
-// all-nonnegative NMF operands the error is a one-sided bias that grows
-// linearly with the accumulation length: measured ~2.4e-7 relative per
-// 32-K chunk of window (tools/tc_check.py: window 64 -> 1.6e-5, 8 -> 1.9e-6,
-// 4 -> 8.7e-7, 1 -> 2.0e-7 on uniform [0,1) data; profiles/README.md).
-// kWindow = 8 keeps the products ~2e-6 of fp64 at ~4% throughput cost.
+// epilogue warps drain each window into fp64 registers and write fp64 split-K
+// partials that a deterministic reduce sums in fixed order.
+// Why windows: the tensor core's fp32 accumulate truncates toward zero, so on
+// the all-nonnegative NMF operands the error is a one-sided bias that grows
+// linearly with the accumulation length (per chunk ~2.4e-7 relative in the
+// stacked form, ~3e-7 in K3; tools/tc_check.py: window 64 -> 1.6e-5, 8 ->
+// 1.9e-6, 1 -> 2.0e-7).  kWindow = 6 keeps the products ~2e-6 of fp64.
 //
-// Warp roles (640 threads, one persistent CTA per SM, 512 TMEM columns):
-//   warp 0: TMA producer (M slices)
-//   warps 1, 2: MMA issuers for even / odd chunks, each into its own fp32
-//               accumulator (TMEM columns 0 / 128); warp 1 allocates TMEM
+// Warp roles (640 threads, one persistent CTA per SM, 512 TMEM columns =
+// 2 MMA warps x 2 accumulator buffers x r_pad + 4 staging slots x 64):
+//   warp 0: TMA producer (M slices, issued and released in pairs)
+//   warps 1, 2: MMA issuers for even / odd chunks, each into its own pair of
+//               accumulator buffers (windows alternate buffers, so a warp
+//               never waits for a drain); warp 1 allocates TMEM
 //   warps 3-10: converters (two groups of 4: even / odd chunks)
-//   warps 11-18: epilogue (lane quarter x column half), drains both accumulators
-//   warp 19: TMA producers (factor slices; lane 0 even, lane 1 odd chunks)
+//   warps 11-18: epilogue (lane quarter x column half), drains all windows
+//   warp 19: TMA producer (factor slices, one thread, stream order)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

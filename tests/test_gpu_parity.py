@@ -383,3 +383,21 @@ def test_wall_clock_budget(P, cfg0, cycle):
     assert tr.elapsed_s[-1] >= 0.9 * T
     assert tr.error[-1] < tr.error[0]
     assert tr.level[-1] == 1
+
+
+def test_nccl_single_rank_path(P, cfg0):
+    """The collective path (NCCL communicator, in-place allreduce of [A | B],
+    error partials, norms) on a 1-rank communicator: bit-identical to the
+    communicator-free run, through a 3-level FMG on fp32 and fp64 storage."""
+    nid = P.nccl_unique_id()
+    for dt in (P.F32, P.F64):
+        with P.Session(dtype=dt) as s:
+            s.set_data(cfg0, P.ImageGrid(32, 32))
+            t0 = s.run_configuration(3, "hals", "fmg", 20, 0, 20.0, 1)
+            V0, W0 = s.get_factors()
+        with P.Session(dtype=dt, world=1, rank=0, nccl_id=nid) as s:
+            s.set_data(cfg0, P.ImageGrid(32, 32))
+            t1 = s.run_configuration(3, "hals", "fmg", 20, 0, 20.0, 1)
+            V1, W1 = s.get_factors()
+        assert np.array_equal(t0.error, t1.error)
+        assert np.array_equal(V0, V1) and np.array_equal(W0, W1)
