@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +26,11 @@ struct NcclApi {
     static NcclApi api;
     static bool loaded = false;
     if (!loaded) {
+      // Single-node framework: bootstrap over loopback unless the user chose an
+      // interface.  (On the GPU pool's boxes NCCL's default interface pick
+      // fails its bootstrap -- "remote process exited or there was a network
+      // error" -- while NVLink/P2P carries the data either way.)
+      setenv("NCCL_SOCKET_IFNAME", "lo", 0);
       void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
 #ifdef MLB_NCCL_PATH
       if (!h) h = dlopen(MLB_NCCL_PATH, RTLD_NOW | RTLD_GLOBAL);

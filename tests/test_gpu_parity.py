@@ -389,8 +389,8 @@ def test_nccl_single_rank_path(P, cfg0):
     """The collective path (NCCL communicator, in-place allreduce of [A | B],
     error partials, norms) on a 1-rank communicator: bit-identical to the
     communicator-free run, through a 3-level FMG on fp32 and fp64 storage."""
-    nid = P.nccl_unique_id()
     for dt in (P.F32, P.F64):
+        nid = P.nccl_unique_id()  # one id per communicator
         with P.Session(dtype=dt) as s:
             s.set_data(cfg0, P.ImageGrid(32, 32))
             t0 = s.run_configuration(3, "hals", "fmg", 20, 0, 20.0, 1)
