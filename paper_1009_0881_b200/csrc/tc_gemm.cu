@@ -368,7 +368,8 @@ struct Params {
   int splits;      // split-K factor
   int chunks_per_split;
   int nchunks;     // ceil(kdim / 32)
-  int rotate;      // rotate each tile's chunk order (product 1)
+  int interleave;  // unit order: interleaved phases of one tile (see unit_of)
+  int rotate;      // blocked order: rotate each tile's chunk order
   double* part;    // [splits][...] fp64 partial outputs
 };
 
@@ -381,22 +382,49 @@ struct Params {
 // staging slot and B stage.  Within a unit, the chunks of parity w are
 // i = i0(w), i0(w) + 2, ... with i0(w) = (w - g0) & 1.
 __device__ __forceinline__ int own_first(int g0, int w) { return (w - g0) & 1; }
-
-// Chunk order within a unit is rotated per tile: for product 1 concurrent CTAs
-// work on different 128-row tiles, and rows n * 4 bytes apart (1 MiB at
-// config 4) at the same column offset land on the same DRAM channels
-// (partition camping).  Starting each tile at a different chunk spreads the
-// concurrent row segments over the address space.  Both producers use the
-// same order; everything downstream follows the stream position.
-__device__ __forceinline__ int unit_chunk(const Params& p, int tile, int c_beg, int n_u, int i) {
-  if (!p.rotate) return c_beg + i;
-  const int rot = (int)(((long long)tile * 97) % n_u);
-  const int k = i + rot;
-  return c_beg + (k >= n_u ? k - n_u : k);
-}
 __device__ __forceinline__ int own_count(int g0, int n_u, int w) {
   const int i0 = own_first(g0, w);
   return n_u > i0 ? (n_u - i0 + 1) >> 1 : 0;
+}
+
+// Work units.  Blocked order (product 2, and product 1 at small strides):
+// unit u = (tile u % tiles, K range u / tiles), chunks c_beg .. c_beg + n - 1;
+// concurrent CTAs hold consecutive tiles (for product 2 adjacent column blocks
+// of the same M rows).  Interleaved order (product 1 at >= 1 MiB row strides):
+// unit u = (tile u / S, phase u % S), chunks phase, phase + S, ...; the S CTAs
+// that run a tile concurrently fetch neighbouring 128-byte segments of the
+// same rows.  (With whole-tile K ranges per CTA, 148 concurrent tiles at the
+// same column offset hit the same DRAM channels: a pure TMA stream in that
+// order tops out at ~4.7 TB/s against 7.4 TB/s with all CTAs on one tile --
+// tools/stream_probe.cu -- but in the product kernel the interleaved order
+// measured slower, so it is opt-in.)
+struct Unit {
+  int tile, split, n;
+};
+__device__ __forceinline__ Unit unit_of(const Params& p, int u) {
+  Unit x;
+  if (p.interleave) {
+    x.tile = u / p.splits;
+    x.split = u % p.splits;
+    x.n = (p.nchunks - x.split + p.splits - 1) / p.splits;
+  } else {
+    x.tile = u % p.tiles;
+    x.split = u / p.tiles;
+    const int c_beg = x.split * p.chunks_per_split;
+    x.n = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+  }
+  return x;
+}
+// chunk index of the i-th chunk of unit x.  With `rotate`, a blocked unit
+// starts at a tile-dependent chunk (concurrent tiles then sit at different
+// column offsets; +2-3 % for product 1 at 1 MiB row strides).
+__device__ __forceinline__ int unit_chunk(const Params& p, const Unit& x, int i) {
+  if (p.interleave) return x.split + i * p.splits;
+  if (p.rotate) {
+    const int k = i + (int)(((long long)x.tile * 97) % x.n);
+    i = k >= x.n ? k - x.n : k;
+  }
+  return x.split * p.chunks_per_split + i;
 }
 
 // MMA issuer for the chunks of parity W into accumulator W.  Two such warps
@@ -418,9 +446,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
 #pragma unroll
   for (int k = 0; k < kBStages; ++k) lastb[k] = -1;
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-    const int split = u / p.tiles;
-    const int c_beg = split * p.chunks_per_split;
-    const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+    const int n_u = unit_of(p, u).n;
     for (int i = own_first(g, W), j = 0; i < n_u; i += 2, ++j) {
       const int gg = g + i, slot = gg % kSlots;
       const uint32_t sph = (uint32_t)(gg / kSlots) & 1u;
@@ -565,11 +591,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         npend = 0;
       };
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int tile = u % p.tiles, split = u / p.tiles;
-        const int c_beg = split * p.chunks_per_split;
-        const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-        for (int i = 0; i < c_end - c_beg; ++i) {
-          pt[npend] = tile, pc[npend] = unit_chunk(p, tile, c_beg, c_end - c_beg, i);
+        const Unit x = unit_of(p, u);
+        for (int i = 0; i < x.n; ++i) {
+          pt[npend] = x.tile, pc[npend] = unit_chunk(p, x, i);
           if (++npend == kMGroup) issue_group();
         }
       }
@@ -585,17 +609,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = l2_policy_evict_last();
       int g = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int tile = u % p.tiles, split = u / p.tiles;
-        const int c_beg = split * p.chunks_per_split;
-        const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+        const Unit x = unit_of(p, u);
+        const int n_u = x.n;
         for (int i = 0; i < n_u; ++i) {
           const int gg = g + i, bs = gg % kBStages;
           mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d_hint(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, tile, c_beg, n_u, i) * kChunk, 0,
-                           fb, pol_b);
-          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
+          tma_load_2d_hint(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, x, i) * kChunk, 0, fb, pol_b);
+          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, unit_chunk(p, x, i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
         g += n_u;
@@ -606,16 +628,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane < 2) {
       int g = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int tile = u % p.tiles, split = u / p.tiles;
-        const int c_beg = split * p.chunks_per_split;
-        const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+        const Unit x = unit_of(p, u);
+        const int n_u = x.n;
         for (int i = own_first(g, w); i < n_u; i += 2) {
           const int gg = g + i, bs = gg % kBStages;
           mbar_wait<64>(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, b_bytes);
-          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, tile, c_beg, n_u, i) * kChunk, 0, fb);
-          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, (c_beg + i + kBPrefetch) * kChunk, 0);
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, x, i) * kChunk, 0, fb);
+          if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, unit_chunk(p, x, i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
         g += n_u;
@@ -640,10 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
     int g = 0;                       // global chunk sequence number
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int split = u / p.tiles;
-      const int c_beg = split * p.chunks_per_split;
-      const int c_end = min(c_beg + p.chunks_per_split, p.nchunks);
-      for (int c = c_beg; c < c_end; ++c, ++g) {
+      const int n_u = unit_of(p, u).n;
+      for (int c = 0; c < n_u; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
         const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots;
         const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
@@ -707,9 +726,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int g = 0;
     double sum[32];
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int tile = u % p.tiles, split = u / p.tiles;
-      const int c_beg = split * p.chunks_per_split;
-      const int n_u = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
+      const Unit x = unit_of(p, u);
+      const int tile = x.tile, split = x.split, n_u = x.n;
       const int c1 = own_count(g, n_u, 1);
       const int nw0 = (own_count(g, n_u, 0) + kWindow - 1) / kWindow;
       const int nw1 = c1 > 0 ? (c1 + kWindow / 2 + kWindow - 1) / kWindow : 0;  // first window is half length
@@ -1163,10 +1181,14 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
-    // rotate for product 1 when M rows are >= 1 MiB apart (measured: +3.5 % at
-    // n = 262144; at 256 KiB strides it costs the L2 sharing of factor slices)
+    // unit order (see unit_of): blocked, rotated for product 1 when M rows are
+    // >= 1 MiB apart.  The interleaved order measured slower in the kernel
+    // (its pure-stream advantage is lost to factor-slice and pairing effects)
+    // and stays opt-in.
+    p.interleave = 0;
     p.rotate = (!TRANS && n * 4 >= ((size_t)1 << 20)) ? 1 : 0;
-    if (const char* e = getenv("MLB_TC_ROTATE")) p.rotate = atoi(e);  // debug override
+    if (const char* e = getenv("MLB_TC_INTERLEAVE")) p.interleave = atoi(e);  // debug override
+    if (const char* e = getenv("MLB_TC_ROTATE")) p.rotate = atoi(e);          // debug override
     // split-K: units (tile, K range) are dealt round-robin to the persistent
     // CTAs, so the kernel lasts ceil(units / SMs) units.  Pick the split factor
     // that maximises the balanced fraction units / (ceil(units / SMs) * SMs),
@@ -1176,7 +1198,7 @@ class TcGemmImpl final : public TcGemm {
     {
       double best = -1.0;
       const int smax = std::max(1, std::min(p.nchunks / 8, 64));
-      for (int sp = 1; sp <= smax; ++sp) {
+      for (int sp = p.interleave ? std::min(4, smax) : 1; sp <= smax; ++sp) {
         const int cps = (int)cdiv(p.nchunks, sp);
         const int spr = (int)cdiv(p.nchunks, cps);
         const double units = (double)p.tiles * spr;
@@ -1190,7 +1212,7 @@ class TcGemmImpl final : public TcGemm {
     if (const char* e = getenv("MLB_TC_SPLITS")) splits = std::max(1, atoi(e));  // debug override
     splits = std::min(splits, p.nchunks);
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
-    p.splits = (int)cdiv(p.nchunks, p.chunks_per_split);
+    p.splits = p.interleave ? splits : (int)cdiv(p.nchunks, p.chunks_per_split);
     const size_t out_count = rows * r;
     double* dst = out;
     if (p.splits > 1) {

@@ -17,7 +17,7 @@ __device__ __forceinline__ bool tryw(uint32_t a, uint32_t ph) {
 __device__ __forceinline__ void wait(uint32_t a, uint32_t ph) { while (!tryw(a, ph)) {} }
 
 template <int STAGES, int BYTES>
-__global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtensorMap map, int ntiles_outer, int nchunks, int rowmode) {
+__global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtensorMap map, int ntiles_outer, int nchunks, int rowmode, int rot) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -29,14 +29,26 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
-  const long total = (long)ntiles_outer * nchunks;
+  const long total = (long)ntiles_outer * nchunks + (rowmode == 2 ? 148L * 8192 : 0);  // mode 2 breaks by unit count
   if (warp == 0 && lane == 0) {
     int s = 0; uint32_t ph = 0;
     for (long u = blockIdx.x; u < total; u += gridDim.x) {
-      const int t = (int)(u / nchunks), c = (int)(u % nchunks);
+      int t, c;
+      if (rowmode == 2) {  // product-kernel order: units (tile, split) dealt round-robin, 13 splits
+        const int splits = 13, cps = (nchunks + splits - 1) / splits;
+        const long k = (u - blockIdx.x) / gridDim.x;   // k-th chunk of this CTA
+        const long unit = blockIdx.x + (k / cps) * gridDim.x;
+        if (unit >= (long)ntiles_outer * splits) break;
+        const int tt = (int)(unit % ntiles_outer), sp = (int)(unit / ntiles_outer);
+        const int i = (int)(k % cps);
+        const int ii = rot ? (int)((i + (long)tt * 97) % cps) : i;
+        t = tt; c = sp * cps + ii;
+      } else {
+        t = (int)(u / nchunks); c = (int)(u % nchunks);
+      }
       wait(su(&empty[s]), ph ^ 1);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[s])), "r"(BYTES));
-      const int c0 = rowmode ? c * 32 : t * 128, c1 = rowmode ? t * 128 : c * 32;
+      const int c0 = rowmode ? c * 32 : t * 128, c1 = rowmode ? t * 128 : c * 32;  // mode 2 = row boxes
       asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                    ::"r"(su(sm + s * BYTES)), "l"((uint64_t)&map), "r"(c0), "r"(c1), "r"(su(&full[s])) : "memory");
       if (++s == STAGES) s = 0, ph ^= 1;
@@ -44,6 +56,11 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
   } else if (warp == 1 && lane == 0) {
     int s = 0; uint32_t ph = 0;
     for (long u = blockIdx.x; u < total; u += gridDim.x) {
+      if (rowmode == 2) {
+        const int splits = 13, cps = (nchunks + splits - 1) / splits;
+        const long k = (u - blockIdx.x) / gridDim.x;
+        if (blockIdx.x + (k / cps) * gridDim.x >= (long)ntiles_outer * splits) break;
+      }
       wait(su(&full[s]), ph);
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su(&empty[s])));
       if (++s == STAGES) s = 0, ph ^= 1;
@@ -56,23 +73,32 @@ int main() {
   float* M; cudaMalloc(&M, m * n * 4); cudaMemset(M, 0, m * n * 4);
   PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
-  for (int mode = 1; mode >= 0; --mode) {  // 1: 128 rows x 32 cols (product A), 0: 32 rows x 128 cols (product C)
+  for (int mode = 3; mode >= 2; --mode) {  // 1: 128 rows x 32 cols (product A), 0: 32 rows x 128 cols (product C)
     CUtensorMap map;
     cuuint64_t dims[2] = {n, m}; cuuint64_t str[1] = {n * 4};
-    cuuint32_t box[2] = {mode ? 32u : 128u, mode ? 128u : 32u}; cuuint32_t es[2] = {1, 1};
+    cuuint32_t box[2] = {mode ? 32u : 128u, mode ? 128u : 32u}; cuuint32_t es[2] = {1, 1};  // mode 2: row boxes too
     enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, M, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         mode ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const int outer = mode ? (int)(m / 128) : (int)(n / 128), nch = mode ? (int)(n / 32) : (int)(m / 32);
-    auto k = k_stream<12, 16384>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384 + 1024);
-    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int rep = 0; rep < 3; ++rep) {
-      cudaEventRecord(a);
-      k<<<148, 64, 12 * 16384 + 1024>>>(map, outer, nch, mode);
-      cudaEventRecord(b); cudaEventSynchronize(b);
-      float ms; cudaEventElapsedTime(&ms, a, b);
-      printf("%s: %.3f ms  %.0f GB/s  (%s)\n", mode ? "128x32 boxes (A)" : "32x128 boxes (C)", ms, m * n * 4 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
-    }
+    const int outer = mode ? (int)(m / 128) : (int)(n / 128), nch = mode ? (int)(n / 32) : (int)(m / 32);  // modes 1-3: row boxes
+    auto run = [&](auto kern, int stages) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, stages * 16384 + 1024);
+      cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+      float best = 1e9f;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        kern<<<148, 64, stages * 16384 + 1024>>>(map, outer, nch, mode >= 2 ? 2 : mode, mode == 3);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        best = ms < best ? ms : best;
+      }
+      printf("%s stages %2d (%3d KB in flight): %.3f ms  %.0f GB/s  (%s)\n", mode == 3 ? "128x32 per-CTA tiles, rotated" : mode == 2 ? "128x32 per-CTA tiles (A order)" : mode ? "128x32 boxes (A)" : "32x128 boxes (C)", stages,
+             stages * 16, best, m * n * 4 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+    };
+    run(k_stream<4, 16384>, 4);
+    run(k_stream<6, 16384>, 6);
+    run(k_stream<8, 16384>, 8);
+    run(k_stream<10, 16384>, 10);
+    run(k_stream<12, 16384>, 12);
   }
   return 0;
 }
