@@ -403,13 +403,15 @@ struct Unit {
 };
 __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   Unit x;
-  if (p.interleave) {
+  if (p.interleave == 1) {
     x.tile = u / p.splits;
     x.split = u % p.splits;
     x.n = (p.nchunks - x.split + p.splits - 1) / p.splits;
   } else {
-    x.tile = u % p.tiles;
-    x.split = u / p.tiles;
+    // 0: split-major (concurrent CTAs on consecutive tiles, same K range);
+    // 2: tile-major (the splits of one tile run concurrently)
+    x.tile = p.interleave == 2 ? u / p.splits : u % p.tiles;
+    x.split = p.interleave == 2 ? u % p.splits : u / p.tiles;
     const int c_beg = x.split * p.chunks_per_split;
     x.n = min(c_beg + p.chunks_per_split, p.nchunks) - c_beg;
   }
@@ -419,7 +421,7 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
 // starts at a tile-dependent chunk (concurrent tiles then sit at different
 // column offsets; +2-3 % for product 1 at 1 MiB row strides).
 __device__ __forceinline__ int unit_chunk(const Params& p, const Unit& x, int i) {
-  if (p.interleave) return x.split + i * p.splits;
+  if (p.interleave == 1) return x.split + i * p.splits;
   if (p.rotate) {
     const int k = i + (int)(((long long)x.tile * 97) % x.n);
     i = k >= x.n ? k - x.n : k;
@@ -1181,12 +1183,12 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
-    // unit order (see unit_of): blocked, rotated for product 1 when M rows are
-    // >= 1 MiB apart.  The interleaved order measured slower in the kernel
-    // (its pure-stream advantage is lost to factor-slice and pairing effects)
-    // and stays opt-in.
+    // unit order (see unit_of): split-major blocked.  The interleaved (1) and
+    // tile-major (2) orders read M in DRAM-friendlier patterns
+    // (tools/stream_probe.cu) but lose the cross-CTA L2 sharing of factor
+    // slices and measured slower in the kernel; they stay opt-in.
     p.interleave = 0;
-    p.rotate = (!TRANS && n * 4 >= ((size_t)1 << 20)) ? 1 : 0;
+    p.rotate = 0;  // measured within noise (+-2 %) at config 4; opt-in
     if (const char* e = getenv("MLB_TC_INTERLEAVE")) p.interleave = atoi(e);  // debug override
     if (const char* e = getenv("MLB_TC_ROTATE")) p.rotate = atoi(e);          // debug override
     // split-K: units (tile, K range) are dealt round-robin to the persistent
@@ -1198,7 +1200,7 @@ class TcGemmImpl final : public TcGemm {
     {
       double best = -1.0;
       const int smax = std::max(1, std::min(p.nchunks / 8, 64));
-      for (int sp = p.interleave ? std::min(4, smax) : 1; sp <= smax; ++sp) {
+      for (int sp = p.interleave == 1 ? std::min(4, smax) : 1; sp <= smax; ++sp) {
         const int cps = (int)cdiv(p.nchunks, sp);
         const int spr = (int)cdiv(p.nchunks, cps);
         const double units = (double)p.tiles * spr;
@@ -1212,7 +1214,7 @@ class TcGemmImpl final : public TcGemm {
     if (const char* e = getenv("MLB_TC_SPLITS")) splits = std::max(1, atoi(e));  // debug override
     splits = std::min(splits, p.nchunks);
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
-    p.splits = p.interleave ? splits : (int)cdiv(p.nchunks, p.chunks_per_split);
+    p.splits = p.interleave == 1 ? splits : (int)cdiv(p.nchunks, p.chunks_per_split);
     const size_t out_count = rows * r;
     double* dst = out;
     if (p.splits > 1) {

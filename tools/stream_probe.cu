@@ -39,9 +39,10 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
         const long k = (u - blockIdx.x) / gridDim.x;   // k-th chunk of this CTA
         const long unit = blockIdx.x + (k / cps) * gridDim.x;
         if (unit >= (long)ntiles_outer * splits) break;
-        const int tt = (int)(unit % ntiles_outer), sp = (int)(unit / ntiles_outer);
+        const int tt = rot == 2 ? (int)(unit / splits) : (int)(unit % ntiles_outer);
+        const int sp = rot == 2 ? (int)(unit % splits) : (int)(unit / ntiles_outer);
         const int i = (int)(k % cps);
-        const int ii = rot ? (int)((i + (long)tt * 97) % cps) : i;
+        const int ii = rot == 1 ? (int)((i + (long)tt * 97) % cps) : i;
         t = tt; c = sp * cps + ii;
       } else {
         t = (int)(u / nchunks); c = (int)(u % nchunks);
@@ -73,7 +74,7 @@ int main() {
   float* M; cudaMalloc(&M, m * n * 4); cudaMemset(M, 0, m * n * 4);
   PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
-  for (int mode = 3; mode >= 2; --mode) {  // 1: 128 rows x 32 cols (product A), 0: 32 rows x 128 cols (product C)
+  for (int mode = 4; mode >= 2; mode -= 2) {  // 1: 128 rows x 32 cols (product A), 0: 32 rows x 128 cols (product C)
     CUtensorMap map;
     cuuint64_t dims[2] = {n, m}; cuuint64_t str[1] = {n * 4};
     cuuint32_t box[2] = {mode ? 32u : 128u, mode ? 128u : 32u}; cuuint32_t es[2] = {1, 1};  // mode 2: row boxes too
@@ -86,12 +87,12 @@ int main() {
       float best = 1e9f;
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(a);
-        kern<<<148, 64, stages * 16384 + 1024>>>(map, outer, nch, mode >= 2 ? 2 : mode, mode == 3);
+        kern<<<148, 64, stages * 16384 + 1024>>>(map, outer, nch, mode >= 2 ? 2 : mode, mode == 3 ? 1 : mode == 4 ? 2 : 0);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         best = ms < best ? ms : best;
       }
-      printf("%s stages %2d (%3d KB in flight): %.3f ms  %.0f GB/s  (%s)\n", mode == 3 ? "128x32 per-CTA tiles, rotated" : mode == 2 ? "128x32 per-CTA tiles (A order)" : mode ? "128x32 boxes (A)" : "32x128 boxes (C)", stages,
+      printf("%s stages %2d (%3d KB in flight): %.3f ms  %.0f GB/s  (%s)\n", mode == 4 ? "128x32 tile-major blocked (13 K ranges/tile)" : mode == 3 ? "128x32 per-CTA tiles, rotated" : mode == 2 ? "128x32 per-CTA tiles (A order)" : mode ? "128x32 boxes (A)" : "32x128 boxes (C)", stages,
              stages * 16, best, m * n * 4 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
     run(k_stream<4, 16384>, 4);
