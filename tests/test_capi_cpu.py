@@ -175,3 +175,20 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(root, f), errors="ignore").read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "mlnmf_oracle" not in src and "libmlnmf_ref" not in src, f
+
+
+def test_run_bench_skip_rules_without_device(P):
+    """run_bench (bench.cpp:41-57): a single-level cycle with levels != 1 and a
+    multilevel request without a pixel grid are skipped with the reference's
+    notes, before any device work."""
+    import numpy as np
+    M = np.ones((16, 5))
+    cfg = P.BenchConfig(algorithms=["hals"], cycles=["none"], level_counts=[2, 3], rank=2, runs=3, budget=10.0)
+    entries = P.run_bench(M, P.ImageGrid(4, 4), cfg)
+    assert [e.skipped for e in entries] == [True, True]
+    assert all(e.note == "single-level runs use exactly one level" for e in entries)
+    cfg = P.BenchConfig(algorithms=["mu"], cycles=["fmg"], level_counts=[2], rank=2, runs=3, budget=10.0)
+    entries = P.run_bench(M, None, cfg)
+    assert entries[0].skipped and entries[0].note == "dataset has no pixel grid"
+    with pytest.raises(ValueError):
+        P.run_bench(M, None, P.BenchConfig(runs=0))
