@@ -90,6 +90,53 @@ __global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ C
 }
 
 
+// MU (solvers.cpp:79-99) at a compile-time rank, same unfused arithmetic and
+// order as k_mu_v / k_mu_w: V(i,:) *= A(i,:) / max(V(i,:) B, 1e-16) with the
+// row's old values (Jacobi within the half) held in registers.
+__device__ __forceinline__ double mu_floor(double v) { return v < 1e-16 ? 1e-16 : v; }
+
+template <typename T, int R>
+__global__ void __launch_bounds__(128) k_mu_v_reg(const double* __restrict__ A, const double* __restrict__ B,
+                                                  T* __restrict__ V, size_t m) {
+  __shared__ double Bt[R * R];  // Bt[j][p] = B[p][j]
+  const int t = threadIdx.x;
+  for (int e = t; e < R * R; e += blockDim.x) Bt[e] = B[(e % R) * R + e / R];
+  __syncthreads();
+  const size_t i = (size_t)blockIdx.x * blockDim.x + t;
+  if (i >= m) return;
+  double v[R];
+#pragma unroll
+  for (int l = 0; l < R; ++l) v[l] = (double)V[i * R + l];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) s = __dadd_rn(s, __dmul_rn(v[q], Bt[j * R + q]));
+    V[i * R + j] = to_t<T>(__dmul_rn(v[j], A[i * R + j] / mu_floor(s)));
+  }
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(128) k_mu_w_reg(const double* __restrict__ Cm, const double* __restrict__ D,
+                                                  T* __restrict__ W, size_t n) {
+  __shared__ double Ds[R * R];
+  const int t = threadIdx.x;
+  for (int e = t; e < R * R; e += blockDim.x) Ds[e] = D[e];
+  __syncthreads();
+  const size_t j = (size_t)blockIdx.x * blockDim.x + t;
+  if (j >= n) return;
+  double w[R];
+#pragma unroll
+  for (int l = 0; l < R; ++l) w[l] = (double)W[(size_t)l * n + j];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) s = __dadd_rn(s, __dmul_rn(Ds[k * R + q], w[q]));
+    W[(size_t)k * n + j] = to_t<T>(__dmul_rn(w[k], Cm[(size_t)k * n + j] / mu_floor(s)));
+  }
+}
+
 template <int R>
 void launch_v(bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
   const dim3 g((unsigned)((m + 127) / 128));
@@ -114,6 +161,22 @@ void check(cudaError_t e) {
 }  // namespace
 
 bool hals_reg_supported(size_t r) { return r == 64; }
+
+void mu_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, cudaStream_t s) {
+  if (r != 64) throw std::invalid_argument("mu_v_reg: unsupported rank");
+  const dim3 g((unsigned)((m + 127) / 128));
+  if (f32) k_mu_v_reg<float, 64><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m);
+  else k_mu_v_reg<double, 64><<<g, 128, 0, s>>>(A, B, static_cast<double*>(V), m);
+  check(cudaGetLastError());
+}
+
+void mu_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, cudaStream_t s) {
+  if (r != 64) throw std::invalid_argument("mu_w_reg: unsupported rank");
+  const dim3 g((unsigned)((n + 127) / 128));
+  if (f32) k_mu_w_reg<float, 64><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n);
+  else k_mu_w_reg<double, 64><<<g, 128, 0, s>>>(C, D, static_cast<double*>(W), n);
+  check(cudaGetLastError());
+}
 
 void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
   if (r != 64) throw std::invalid_argument("hals_v_reg: unsupported rank");

@@ -333,14 +333,15 @@ def test_sharded_slices_generate_consistently(P, restated):
     assert np.array_equal(full[:, 16:40], part)
 
 
-def test_rank64_hals_exact_bitwise(P, restated):
-    """r = 64 takes the register-resident HALS sweep kernels (hals_reg.cu):
+@pytest.mark.parametrize("kind", ["hals", "mu"])
+def test_rank64_hals_exact_bitwise(P, restated, kind):
+    """r = 64 takes the register-resident HALS / MU kernels (hals_reg.cu):
     fp64 exact mode stays bit-identical to the oracle through a 3-level FMG."""
     M = oracle.generate_config(0, n=300, restated=restated)
     P.set_default_options(exact=True)
     try:
-        Vo, Wo, to = restated.run_configuration(M, 32, 32, 3, "hals", "fmg", 64, 3, 6.0, 1)
-        res = P.run_configuration(M, P.ImageGrid(32, 32), 3, "hals", "fmg", 64, 3, 6.0, 1)
+        Vo, Wo, to = restated.run_configuration(M, 32, 32, 3, kind, "fmg", 64, 3, 6.0, 1)
+        res = P.run_configuration(M, P.ImageGrid(32, 32), 3, kind, "fmg", 64, 3, 6.0, 1)
     finally:
         P.set_default_options(exact=False)
     check_trace(res.trace, to, 0.0, exact=True)
