@@ -583,7 +583,27 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   const size_t hs = host_dtype == 0 ? 4 : 8;
   const cudaMemcpyKind kind = is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if ((size_t)hs == es) {
-    CK(cudaMemcpyAsync(L0.M, M, count * es, kind, s));
+    const size_t bytes = count * es;
+    if (kind == cudaMemcpyHostToDevice && bytes >= ((size_t)1 << 30)) {
+      // large uploads: 256 MiB pieces alternating over the engine stream and a
+      // second stream, so two copy engines pull from host memory at once
+      cudaStream_t s2 = nullptr;
+      cudaEvent_t done = nullptr;
+      CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      const size_t piece = (size_t)256 << 20;
+      size_t k = 0;
+      for (size_t off = 0; off < bytes; off += piece, ++k)
+        CK(cudaMemcpyAsync(static_cast<char*>(L0.M) + off, static_cast<const char*>(M) + off,
+                           std::min(piece, bytes - off), kind, (k & 1) ? s2 : s));
+      CK(cudaEventRecord(done, s2));
+      CK(cudaStreamWaitEvent(s, done, 0));
+      CK(cudaStreamSynchronize(s));
+      cudaEventDestroy(done);
+      cudaStreamDestroy(s2);
+    } else {
+      CK(cudaMemcpyAsync(L0.M, M, bytes, kind, s));
+    }
   } else {
     // convert through a staging buffer in chunks
     const size_t chunk = std::min<size_t>(count, (size_t)64 << 20);
