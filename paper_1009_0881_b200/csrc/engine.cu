@@ -43,7 +43,8 @@ namespace mlb {
 std::atomic<uint64_t> g_dev_epoch{1};
 
 namespace {
-constexpr int kTargetBlocks = 2 * 148;
+constexpr int kTargetBlocks = 8 * 148;  // split-K target: ~8 blocks per SM (latency-bound K loops)
+
 
 template <typename T>
 cudaError_t dev_malloc(T** p, size_t b) {
@@ -192,8 +193,7 @@ struct Engine::Impl {
       launch(k_gemm_abt<T, false>, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst);
     if (spr > 1) {
       const size_t cnt = rows * ny;
-      launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0,
-             (const double*)part.as<double>(), cnt, spr, out);
+      reduce_splits(part.as<double>(), cnt, spr, out);
     }
   }
 
@@ -216,9 +216,17 @@ struct Engine::Impl {
       launch(k_gemm_atb<T, false>, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst);
     if (spr > 1) {
       const size_t cnt = r * ncols;
-      launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0,
-             (const double*)part.as<double>(), cnt, spr, out);
+      reduce_splits(part.as<double>(), cnt, spr, out);
     }
+  }
+
+  // out[e] = sum over spr split partials (deterministic; wide form for many splits)
+  void reduce_splits(const double* prt, size_t cnt, int spr, double* out) {
+    if (spr >= 16 && cnt <= ((size_t)1 << 16))
+      launch(k_reduce_splits_wide, dim3((unsigned)ceil_div(cnt, 32)), dim3(256), 0, prt, cnt, spr, out);
+    else
+      launch(k_reduce_splits, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0, prt, cnt, spr,
+             out);
   }
 
   double* A() { return AB.as<double>(); }
@@ -277,6 +285,14 @@ struct Engine::Impl {
   }
 
   // ---------------- row/column sweeps ----------------
+  // Non-exact HALS sweeps over few rows / columns use a warp per row (warp-
+  // shuffle dot products): one thread per column leaves the GPU idle there
+  // (config 3's W half: n = 165).  With many rows the thread-per-row kernels
+  // win (measured: config 3's V half 0.58 -> 0.82 ms/step and config 4's step
+  // +2 ms with warps).  Exact mode keeps the reference's sequential order.
+  bool warp_sweeps(size_t r, size_t count) const {
+    return !exact() && r <= 64 && count < 16384 && std::getenv("MLNMF_THREAD_SWEEPS") == nullptr;
+  }
   int sweep_block(int r) const {
     for (int bd : {128, 64, 32})
       if ((size_t)r * r * 8 + (size_t)r * bd * 8 <= kSmemMax) return bd;
@@ -304,7 +320,10 @@ struct Engine::Impl {
     const int bd = sweep_block((int)r);
     const size_t smem = (r * r + r * bd) * 8;
     const dim3 gv((unsigned)ceil_div(L.m, bd));
-    if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep (config-4 rank)
+    if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
+      launch(k_hals_v_warp<T>, dim3((unsigned)ceil_div(L.m, 8)), dim3(256), r * r * 8, (const double*)A(),
+             (const double*)B(), V, L.m, (int)r, deg);
+    } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
       hals_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, deg, s);
       ++e->launches_;
     } else if (kind == kHals) {
@@ -322,7 +341,10 @@ struct Engine::Impl {
     product_vtm<T>(l);
     T* Wp = W.as<T>();
     const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
-    if (kind == kHals && hals_reg_supported(r)) {
+    if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
+      launch(k_hals_w_warp<T>, dim3((unsigned)ceil_div(e->n_loc_, 8)), dim3(256), r * r * 8,
+             (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_, (int)r, deg);
+    } else if (kind == kHals && hals_reg_supported(r)) {
       hals_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
       ++e->launches_;
     } else if (kind == kHals) {

@@ -179,6 +179,27 @@ __global__ void k_reduce_splits(const double* __restrict__ part, size_t count, i
   }
 }
 
+// Same sum with the splits spread over 8 thread groups (many splits, few
+// outputs: r x r Grams over long K): block = 32 consecutive outputs x 8
+// groups; group q sums splits q, q + 8, ...; the 8 partials are added in
+// group order.  Deterministic; a different association than k_reduce_splits.
+__global__ void __launch_bounds__(256) k_reduce_splits_wide(const double* __restrict__ part, size_t count,
+                                                            int splits, double* __restrict__ out) {
+  __shared__ double ps[8][33];
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const size_t e = (size_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < count)
+    for (int z = q; z < splits; z += 8) s += part[(size_t)z * count + e];
+  ps[q][lane] = s;
+  __syncthreads();
+  if (q == 0 && e < count) {
+    double t = ps[0][lane];
+    for (int g = 1; g < 8; ++g) t += ps[g][lane];
+    out[e] = t;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // HALS sweeps (solvers.cpp:101-141).  One thread per row of V (resp. column
 // of W); the r x r Gram in shared memory; the thread's row/column held in
@@ -240,6 +261,92 @@ __global__ void k_hals_w(const double* __restrict__ Cm, const double* __restrict
   }
   if (act)
     for (int l = 0; l < r; ++l) W[(size_t)l * n + j] = to_t<T>(ws[l * bd + t]);
+}
+
+// Warp-per-row / warp-per-column HALS sweeps for few rows / columns (non-exact
+// runs on the small configs, where one thread per column leaves the GPU idle:
+// config 3 has n = 165).  Lanes hold elements l and l + 32 (r <= 64); each of
+// the r sequential updates is a warp-wide dot product (shuffle reduction) --
+// a different association than the reference's sequential sum, so exact mode
+// keeps the thread-per-row kernels.
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// rows of V (m x r): x_k <- max(0, (A_ik + x_k G_kk - sum_l x_l G_lk) / G_kk)
+template <typename T>
+__global__ void __launch_bounds__(256) k_hals_v_warp(const double* __restrict__ A, const double* __restrict__ G,
+                                                     T* __restrict__ V, size_t m, int r, int* __restrict__ degenerate) {
+  extern __shared__ double Gs[];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = G[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const bool act = i < m;
+  double x0 = (act && lane < r) ? (double)V[i * r + lane] : 0.0;
+  double x1 = (act && lane + 32 < r) ? (double)V[i * r + lane + 32] : 0.0;
+  for (int k = 0; k < r; ++k) {
+    const double gkk = Gs[k * r + k];
+    if (gkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    double part = 0.0;
+    if (lane < r) part = x0 * Gs[lane * r + k];
+    if (lane + 32 < r) part = fma(x1, Gs[(lane + 32) * r + k], part);
+    const double dot = warp_allsum(part);
+    const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+    const double a = act ? A[i * r + k] : 0.0;
+    const double q = (a + xk * gkk - dot) / gkk;
+    const double nk = q > 0.0 ? q : 0.0;
+    if (lane == (k & 31)) {
+      if (k < 32) x0 = nk;
+      else x1 = nk;
+    }
+  }
+  if (act) {
+    if (lane < r) V[i * r + lane] = to_t<T>(x0);
+    if (lane + 32 < r) V[i * r + lane + 32] = to_t<T>(x1);
+  }
+}
+
+// columns of W (r x n): the same update with C (r x n) and D (r x r)
+template <typename T>
+__global__ void __launch_bounds__(256) k_hals_w_warp(const double* __restrict__ Cm, const double* __restrict__ D,
+                                                     T* __restrict__ W, size_t n, int r, int* __restrict__ degenerate) {
+  extern __shared__ double Ds[];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) Ds[e] = D[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const size_t j = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const bool act = j < n;
+  double x0 = (act && lane < r) ? (double)W[(size_t)lane * n + j] : 0.0;
+  double x1 = (act && lane + 32 < r) ? (double)W[(size_t)(lane + 32) * n + j] : 0.0;
+  for (int k = 0; k < r; ++k) {
+    const double dkk = Ds[k * r + k];
+    if (dkk <= 0.0) {
+      if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(degenerate, 1);
+      continue;
+    }
+    double part = 0.0;
+    if (lane < r) part = Ds[k * r + lane] * x0;
+    if (lane + 32 < r) part = fma(Ds[k * r + lane + 32], x1, part);
+    const double dot = warp_allsum(part);
+    const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+    const double c = act ? Cm[(size_t)k * n + j] : 0.0;
+    const double q = (c + dkk * xk - dot) / dkk;
+    const double nk = q > 0.0 ? q : 0.0;
+    if (lane == (k & 31)) {
+      if (k < 32) x0 = nk;
+      else x1 = nk;
+    }
+  }
+  if (act) {
+    if (lane < r) W[(size_t)lane * n + j] = to_t<T>(x0);
+    if (lane + 32 < r) W[(size_t)(lane + 32) * n + j] = to_t<T>(x1);
+  }
 }
 
 // ---------------------------------------------------------------------------
