@@ -328,7 +328,7 @@ struct Engine::Impl {
       ++e->launches_;
     } else if (kind == kHals) {
       launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
-    } else if (kind == kMu && hals_reg_supported(r)) {
+    } else if (kind == kMu && mu_reg_supported(r)) {
       mu_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, s);
       ++e->launches_;
     } else if (kind == kMu) {
@@ -350,7 +350,7 @@ struct Engine::Impl {
     } else if (kind == kHals) {
       launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
              e->n_loc_, (int)r, deg);
-    } else if (kind == kMu && hals_reg_supported(r)) {
+    } else if (kind == kMu && mu_reg_supported(r)) {
       mu_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, s);
       ++e->launches_;
     } else if (kind == kMu) {

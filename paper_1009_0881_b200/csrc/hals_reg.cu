@@ -160,7 +160,9 @@ void check(cudaError_t e) {
 
 }  // namespace
 
-bool hals_reg_supported(size_t r) { return r == 64; }
+// compiled ranks: the config-4 rank and the configs-1/3 rank (HALS); MU at 64
+bool hals_reg_supported(size_t r) { return r == 64 || r == 49; }
+bool mu_reg_supported(size_t r) { return r == 64; }
 
 void mu_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, cudaStream_t s) {
   if (r != 64) throw std::invalid_argument("mu_v_reg: unsupported rank");
@@ -179,14 +181,16 @@ void mu_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, siz
 }
 
 void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
-  if (r != 64) throw std::invalid_argument("hals_v_reg: unsupported rank");
-  launch_v<64>(f32, A, B, V, m, deg, s);
+  if (r == 64) launch_v<64>(f32, A, B, V, m, deg, s);
+  else if (r == 49) launch_v<49>(f32, A, B, V, m, deg, s);
+  else throw std::invalid_argument("hals_v_reg: unsupported rank");
   check(cudaGetLastError());
 }
 
 void hals_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
-  if (r != 64) throw std::invalid_argument("hals_w_reg: unsupported rank");
-  launch_w<64>(f32, C, D, W, n, deg, s);
+  if (r == 64) launch_w<64>(f32, C, D, W, n, deg, s);
+  else if (r == 49) launch_w<49>(f32, C, D, W, n, deg, s);
+  else throw std::invalid_argument("hals_w_reg: unsupported rank");
   check(cudaGetLastError());
 }
 

@@ -6,6 +6,7 @@
 
 namespace mlb {
 bool hals_reg_supported(size_t r);
+bool mu_reg_supported(size_t r);
 // V (m x r, T = f32 ? float : double) rows swept with A (m x r) and B (r x r), fp64
 void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s);
 // W (r x n) columns swept with C (r x n) and D (r x r), fp64
