@@ -196,6 +196,13 @@ __device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t mbar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // warp-wide call; one elected lane commits
@@ -370,6 +377,8 @@ struct Params {
   int nchunks;     // ceil(kdim / 32)
   int interleave;  // unit order: interleaved phases of one tile (see unit_of)
   int rotate;      // blocked order: rotate each tile's chunk order
+  int wide;        // product 1: a chunk pair is one 3-D TMA box of 128 rows x 256 B
+                   // (smem [row][half][32]); chunks_per_split even, n % 64 == 0
   double* part;    // [splits][...] fp64 partial outputs
 };
 
@@ -583,11 +592,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(fm, npend * kMTileBytes);
         for (int k = 0; k < npend; ++k) TCT(0, g + k);
         unsigned char* dst = sm_m + ps * kMGroup * kMTileBytes;
-        for (int k = 0; k < npend; ++k) {
-          if (!TRANS)
-            tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm, pol_m);
-          else
-            tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm, pol_m);
+        if (!TRANS && p.wide) {
+          // pair (c, c + 1), c even, same tile: each row's 256 contiguous bytes
+          // in one request stream (a 2-D box per chunk fetches 128 B per row
+          // and DRAM serves that pattern at ~4.6 TB/s; 256 B rows ~7 TB/s --
+          // tools/stream_probe.cu)
+          tma_load_3d_hint(smem_u32(dst), &map_m, 0, pc[0], pt[0] * 128, fm, pol_m);
+        } else {
+          for (int k = 0; k < npend; ++k) {
+            if (!TRANS)
+              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm, pol_m);
+            else
+              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm, pol_m);
+          }
         }
         g += kMGroup;
         npend = 0;
@@ -675,7 +692,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         // shared-window address of the slice (explicit ld.shared: a generic
         // pointer here compiles to slower generic LD.E)
         const uint32_t tile = smem_u32(sm_m) + (uint32_t)((ps * kMGroup + g % kMGroup) * kMTileBytes);
-        if (!TRANS) {
+        if (!TRANS && p.wide) {
+          // pair buffer [row][half][32] (SWIZZLE_128B per 128-byte line):
+          // this chunk's row is line 2 row + h; 16-byte piece jj at
+          // jj ^ (line & 7).  Lanes 4..7 of each quarter-warp walk the pieces
+          // in a flipped order (jj = j ^ 1), so the 8 lanes of a wavefront hit
+          // 8 distinct bank groups.
+          const uint32_t pairb = smem_u32(sm_m) + (uint32_t)(ps * kMGroup * kMTileBytes);
+          const uint32_t line = 2u * (uint32_t)row + (uint32_t)(g & 1);
+          const int flip = (lane >> 2) & 1;
+          float y[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            lds128(pairb + line * 128 + ((((uint32_t)(j ^ flip)) ^ (line & 7)) << 4), y[4 * j], y[4 * j + 1],
+                   y[4 * j + 2], y[4 * j + 3]);
+          // y holds piece j ^ flip in slot j: swap adjacent pieces back when flipped
+#pragma unroll
+          for (int k = 0; k < 32; ++k) x[k] = flip ? y[k ^ 4] : y[k];
+        } else if (!TRANS) {
           // row `row` of a 128 x 32 SWIZZLE_128B tile: 16-byte chunk j at j ^ (row & 7)
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -1081,6 +1115,22 @@ CUtensorMap make_map(const void* ptr, uint64_t inner, uint64_t outer, uint32_t b
   return m;
 }
 
+// 3-D view of a row-major fp32 matrix (n % 64 == 0): (32 columns, n / 32
+// column blocks, m rows), box (32, 2, 128): one 128-row x 256-byte slab, laid
+// out [row][block][32] with the 128-byte swizzle.
+CUtensorMap make_map3_rows(const void* ptr, uint64_t n, uint64_t m) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {32, n / 32, m};
+  cuuint64_t strides[2] = {128, n * 4};
+  cuuint32_t box[3] = {32, 2, 128};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+  return map;
+}
+
 size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
 
 class TcGemmImpl final : public TcGemm {
@@ -1183,6 +1233,8 @@ class TcGemmImpl final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
+    p.wide = (!TRANS && tc::kMGroup == 2 && n % 64 == 0) ? 1 : 0;
+    if (const char* e = getenv("MLB_TC_WIDE")) p.wide = p.wide && atoi(e);  // debug override
     // unit order (see unit_of): split-major blocked.  The interleaved (1) and
     // tile-major (2) orders read M in DRAM-friendlier patterns
     // (tools/stream_probe.cu) but lose the cross-CTA L2 sharing of factor
@@ -1201,7 +1253,8 @@ class TcGemmImpl final : public TcGemm {
       double best = -1.0;
       const int smax = std::max(1, std::min(p.nchunks / 8, 64));
       for (int sp = p.interleave == 1 ? std::min(4, smax) : 1; sp <= smax; ++sp) {
-        const int cps = (int)cdiv(p.nchunks, sp);
+        int cps = (int)cdiv(p.nchunks, sp);
+        if (p.wide) cps += cps & 1;  // whole chunk pairs per unit
         const int spr = (int)cdiv(p.nchunks, cps);
         const double units = (double)p.tiles * spr;
         const double rounds = std::ceil(units / sms_);
@@ -1214,6 +1267,10 @@ class TcGemmImpl final : public TcGemm {
     if (const char* e = getenv("MLB_TC_SPLITS")) splits = std::max(1, atoi(e));  // debug override
     splits = std::min(splits, p.nchunks);
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
+    if (p.wide) {
+      p.chunks_per_split += p.chunks_per_split & 1;
+      p.interleave = 0, p.rotate = 0;  // pairs must stay (c even, c + 1)
+    }
     p.splits = p.interleave == 1 ? splits : (int)cdiv(p.nchunks, p.chunks_per_split);
     const size_t out_count = rows * r;
     double* dst = out;
@@ -1222,7 +1279,9 @@ class TcGemmImpl final : public TcGemm {
       dst = static_cast<double*>(part_);
     }
     p.part = dst;
-    const CUtensorMap mm = TRANS ? make_map(M, n, m, 128, tc::kChunk, false) : make_map(M, n, m, tc::kChunk, 128, true);
+    const CUtensorMap mm = TRANS    ? make_map(M, n, m, 128, tc::kChunk, false)
+                           : p.wide ? make_map3_rows(M, n, m)
+                                    : make_map(M, n, m, tc::kChunk, 128, true);
     const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, 2 * rp, true);
     const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
     auto kern = tc::k_tc_product<TRANS>;
