@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // chunks are adjacent in DRAM, so issuing them together keeps DRAM pages
       // open (+2-3% over single slices).
       int g = 0, npend = 0;
-      int pt[kMGroup], pc[kMGroup];
+      int pt[kMGroup] = {}, pc[kMGroup] = {};
       const uint64_t pol_m = l2_policy_evict_first();
       auto issue_group = [&]() {
         const int pg = g / kMGroup, ps = pg % kMGroups;
