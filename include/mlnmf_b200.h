@@ -133,6 +133,15 @@ int mlnmf_random_init(size_t m, size_t n, size_t r, uint64_t seed, double* V_out
  * X is (h*w) x ncols (restrict) or (ceil(h/2)*ceil(w/2)) x ncols (prolong). */
 int mlnmf_restrict_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
 int mlnmf_prolong_columns(size_t grid_h, size_t grid_w, const double* X, size_t ncols, double* Y);
+/* smoothness (transfer.hpp:75-76, transfer.cpp:128-141) with R, P =
+ * build_restriction / build_prolongation(grid h x w): M is (h*w) x n.
+ * MLNMF_ERR_INVALID for the zero matrix. */
+int mlnmf_smoothness(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w, double* out);
+/* initialization_bound (transfer.hpp:85-87, transfer.cpp:143-153):
+ * lhs = ||M - P(V_coarse) W||_F, rhs = s_M ||M||_F + ||P||_F ||R(M) - V_coarse W||_F;
+ * V_coarse is (ceil(h/2)*ceil(w/2)) x r, W is r x n. */
+int mlnmf_initialization_bound(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                               const double* V_coarse, const double* W, size_t r, double* lhs, double* rhs);
 /* run_bench's runs loop (proj/include/mlnmf/bench.hpp:34, proj/src/bench.cpp:28-84):
  * final_errors[i] = run_configuration(M, grid, level_count, kind, cycle, rank,
  * base_seed + i, budget, trace_every = 0).trace.final_error() for i < runs,
@@ -177,6 +186,14 @@ int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps);
 int mlnmf_session_sync(mlnmf_session* s);
 int mlnmf_session_error(mlnmf_session* s, double* out); /* ||M - VW||_F at level 0, all ranks */
 int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out); /* ||M_level||_F^2, all ranks */
+/* Diagnostics over the resident pyramid, all ranks (transfer.cpp:128-153):
+ * s_M of level `level`, and both sides of the initialization bound for
+ * V_coarse (level+1 rows x r) and this rank's W columns (r x n_local).  The
+ * bound call leaves V_coarse at level+1, P V_coarse at `level` and W as the
+ * session's factors. */
+int mlnmf_session_smoothness(mlnmf_session* s, size_t level, double* out);
+int mlnmf_session_initialization_bound(mlnmf_session* s, size_t level, const void* V_coarse, const void* W_local,
+                                       int host_dtype, size_t r, double* lhs, double* rhs);
 /* The two M-streaming products at level 0 with the current factors, through
  * the active implementation: A = M W^T (m x r) and C = V^T M (r x n_local),
  * fp64 host buffers (either may be NULL).  Note: A is this rank's partial

@@ -148,6 +148,20 @@ class _Common:
         self._check(self._fn("nnls_active_set")(_d(G), _d(h), _d(x0), _sz(r), _d(x), C.byref(it)))
         return x, it.value
 
+    # ---- diagnostics (transfer.cpp:128-153) ----
+    def smoothness(self, M, h, w):
+        M = _f64(M)
+        out = C.c_double()
+        self._check(self._fn("smoothness")(_d(M), _sz(h), _sz(w), _sz(M.shape[1]), C.byref(out)))
+        return out.value
+
+    def initialization_bound(self, M, h, w, Vc, W):
+        M = _f64(M); Vc = _f64(Vc); W = _f64(W)
+        lhs = C.c_double(); rhs = C.c_double()
+        self._check(self._fn("initialization_bound")(_d(M), _sz(h), _sz(w), _sz(M.shape[1]), _d(Vc), _d(W),
+                                                     _sz(Vc.shape[1]), C.byref(lhs), C.byref(rhs)))
+        return lhs.value, rhs.value
+
 
 class Restated(_Common):
     """The serial C restatement (oracle/mlnmf_oracle.c)."""

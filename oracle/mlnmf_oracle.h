@@ -58,6 +58,10 @@ orc_op* orc_build_restriction(size_t h, size_t w);
 orc_op* orc_build_prolongation(size_t h, size_t w);
 void orc_op_apply(const orc_op* op, const double* X, size_t ncols, double* Y);
 void orc_op_free(orc_op* op);
+double orc_op_frobenius_norm(const orc_op* op);
+int orc_smoothness(const double* M, size_t h, size_t w, size_t n, double* out);
+int orc_initialization_bound(const double* M, size_t h, size_t w, size_t n, const double* Vc,
+                             const double* W, size_t r, double* lhs, double* rhs);
 
 void orc_mu_step(const double* M, double* V, double* W, size_t m, size_t n, size_t r);
 void orc_hals_step(const double* M, double* V, double* W, size_t m, size_t n, size_t r, int* degenerate);

@@ -126,6 +126,24 @@ int ref_operator_dense(size_t h, size_t w, int which, double* out) {
   });
 }
 
+int ref_smoothness(const double* M, size_t h, size_t w, size_t n, double* out) {
+  return guard([&] {
+    *out = smoothness(mat(M, h * w, n), build_restriction({h, w}), build_prolongation({h, w}));
+  });
+}
+
+int ref_initialization_bound(const double* M, size_t h, size_t w, size_t n, const double* Vc,
+                             const double* W, size_t r, double* lhs, double* rhs) {
+  return guard([&] {
+    const ImageGrid c = coarsen_grid({h, w});
+    const BoundCheck b = initialization_bound(mat(M, h * w, n), build_restriction({h, w}),
+                                              build_prolongation({h, w}), mat(Vc, c.pixels(), r),
+                                              mat(W, r, n));
+    *lhs = b.lhs;
+    *rhs = b.rhs;
+  });
+}
+
 int ref_apply_operator(size_t h, size_t w, int which, const double* X,
                        size_t ncols, double* Y) {
   return guard([&] {

@@ -18,7 +18,7 @@ import ctypes as C
 import enum
 import os
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import NamedTuple, Optional
 
 import numpy as np
 
@@ -200,6 +200,8 @@ _proto("mlnmf_frobenius_error", C.c_int, _dp, _dp, _dp, _sz, _sz, _sz, _dp)
 _proto("mlnmf_random_init", C.c_int, _sz, _sz, _sz, C.c_uint64, _dp, _dp)
 _proto("mlnmf_restrict_columns", C.c_int, _sz, _sz, _dp, _sz, _dp)
 _proto("mlnmf_prolong_columns", C.c_int, _sz, _sz, _dp, _sz, _dp)
+_proto("mlnmf_smoothness", C.c_int, _dp, _sz, _sz, _sz, _sz, _dp)
+_proto("mlnmf_initialization_bound", C.c_int, _dp, _sz, _sz, _sz, _sz, _dp, _dp, _sz, _dp, _dp)
 _proto("mlnmf_session_create", C.c_int, C.POINTER(_Options), C.POINTER(_vp))
 _proto("mlnmf_session_destroy", None, _vp)
 _proto("mlnmf_session_set_data", C.c_int, _vp, _vp, C.c_int, _sz, _sz, _sz, _sz, _sz, _sz)
@@ -214,6 +216,8 @@ _proto("mlnmf_session_steps", C.c_int, _vp, C.c_int, _sz)
 _proto("mlnmf_session_sync", C.c_int, _vp)
 _proto("mlnmf_session_error", C.c_int, _vp, _dp)
 _proto("mlnmf_session_norm2", C.c_int, _vp, _sz, _dp)
+_proto("mlnmf_session_smoothness", C.c_int, _vp, _sz, _dp)
+_proto("mlnmf_session_initialization_bound", C.c_int, _vp, _sz, _vp, _vp, C.c_int, _sz, _dp, _dp)
 _proto("mlnmf_session_export_data", C.c_int, _vp, _vp, C.c_int)
 _proto("mlnmf_session_products", C.c_int, _vp, _dp, _dp)
 _proto("mlnmf_session_set_profiling", C.c_int, _vp, C.c_int)
@@ -582,6 +586,37 @@ def prolong_columns(grid: ImageGrid, X):
     return Y
 
 
+def smoothness(M, grid: ImageGrid) -> float:
+    """smoothness(M, build_restriction(grid), build_prolongation(grid))
+    (transfer.hpp:75-76): ||M - P R M||_F / ||M||_F, on the device."""
+    M = _f64(M)
+    if M.ndim == 1:
+        M = M[:, None]
+    if M.shape[0] != grid.pixels():
+        raise ValueError("TransferOperator::apply: dimension mismatch")
+    out = C.c_double()
+    _check(_lib.mlnmf_smoothness(_d(M), M.shape[0], M.shape[1], grid.height, grid.width, C.byref(out)))
+    return out.value
+
+
+class BoundCheck(NamedTuple):  # transfer.hpp:78-81
+    lhs: float  # ||M - P(V')W||_F
+    rhs: float  # s_M ||M||_F + ||P||_F ||R(M) - V'W||_F
+
+
+def initialization_bound(M, grid: ImageGrid, V_coarse, W) -> BoundCheck:
+    """initialization_bound(M, R, P, V_coarse, W) with R, P built on `grid`
+    (transfer.hpp:85-87, transfer.cpp:143-153), on the device."""
+    M, Vc, W = _f64(M), _f64(V_coarse), _f64(W)
+    c = coarsen_grid(grid)
+    if M.shape[0] != grid.pixels() or Vc.shape[0] != c.pixels() or W.shape != (Vc.shape[1], M.shape[1]):
+        raise ValueError("initialization_bound: dimension mismatch")
+    lhs, rhs = C.c_double(), C.c_double()
+    _check(_lib.mlnmf_initialization_bound(_d(M), M.shape[0], M.shape[1], grid.height, grid.width, _d(Vc), _d(W),
+                                           Vc.shape[1], C.byref(lhs), C.byref(rhs)))
+    return BoundCheck(lhs.value, rhs.value)
+
+
 def iteration_cost(m: int, n: int, r: int, kind) -> float:
     """iteration_cost with CostParams::with_default_sr (cost_model.hpp:36)."""
     return _lib.mlnmf_iteration_cost(m, n, r, _kind(kind))
@@ -673,6 +708,7 @@ class Session:
         _check(_lib.mlnmf_session_set_data(self._h, M_local.ctypes.data, hd, m, nl, n_total, col0, grid.height,
                                            grid.width))
         self.m, self.n_local, self.n_total, self.col0 = m, nl, n_total, col0
+        self.grid = grid
 
     def set_data_ptr(self, ptr: int, host_dtype: int, m: int, n_local: int, grid: ImageGrid, n_total=None, col0=0):
         """set_data from a raw host pointer (e.g. pinned memory)."""
@@ -680,6 +716,7 @@ class Session:
         _check(_lib.mlnmf_session_set_data(self._h, ptr, host_dtype, m, n_local, n_total, col0, grid.height,
                                            grid.width))
         self.m, self.n_local, self.n_total, self.col0 = m, n_local, n_total, col0
+        self.grid = grid
 
     def generate(self, cfg: int, seed: int = 0, n_total=None, col0=0, n_local=None, r=None):
         c = GEN_CONFIGS[cfg]
@@ -689,7 +726,8 @@ class Session:
                        c["noise"][0], c["noise"][1], seed, c["scale_to_unit"])
         _check(_lib.mlnmf_session_generate(self._h, C.byref(g), n_total, col0, n_local))
         self.m, self.n_local, self.n_total, self.col0 = c["h"] * c["w"], n_local, n_total, col0
-        return ImageGrid(c["h"], c["w"])
+        self.grid = ImageGrid(c["h"], c["w"])
+        return self.grid
 
     def run_configuration(self, level_count, kind, cycle, rank, seed, budget, trace_every=1) -> RunTrace:
         mode, amount = _budget(budget)
@@ -742,6 +780,29 @@ class Session:
         out = C.c_double()
         _check(_lib.mlnmf_session_norm2(self._h, level, C.byref(out)))
         return out.value
+
+    def smoothness(self, level: int = 0) -> float:
+        """s_M of the resident level-`level` data over all ranks (transfer.cpp:128-141)."""
+        out = C.c_double()
+        _check(_lib.mlnmf_session_smoothness(self._h, level, C.byref(out)))
+        return out.value
+
+    def initialization_bound(self, V_coarse, W_local, level: int = 0) -> BoundCheck:
+        """Both sides of the coarse-initialization bound at `level` over all ranks
+        (transfer.cpp:143-153); V_coarse has level+1's rows, W_local this rank's
+        columns.  Leaves V_coarse / P V_coarse / W as the session's factors."""
+        g = self.grid
+        for _ in range(level + 1):
+            g = coarsen_grid(g)
+        Vc = np.ascontiguousarray(V_coarse, dtype=np.float64)
+        W = np.ascontiguousarray(W_local, dtype=np.float64)
+        if Vc.ndim != 2 or Vc.shape[0] != g.pixels() or W.shape != (Vc.shape[1], self.n_local):
+            raise ValueError("initialization_bound: dimension mismatch")
+        lhs, rhs = C.c_double(), C.c_double()
+        _check(_lib.mlnmf_session_initialization_bound(self._h, level, Vc.ctypes.data, W.ctypes.data, F64,
+                                                       Vc.shape[1], C.byref(lhs), C.byref(rhs)))
+        self.r = Vc.shape[1]
+        return BoundCheck(lhs.value, rhs.value)
 
     def products(self):
         """(A, C) = (M W^T, V^T M) at level 0 with the current factors, through

@@ -162,6 +162,25 @@ int mlnmf_plan_configuration(size_t grid_h, size_t grid_w, size_t n, size_t leve
   });
 }
 
+int mlnmf_smoothness(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w, double* out) {
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, 1);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, grid_h, grid_w, false);
+    *out = e.smoothness(0);
+  });
+}
+
+int mlnmf_initialization_bound(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w,
+                               const double* V_coarse, const double* W, size_t r, double* lhs, double* rhs) {
+  return guard([&] {
+    Engine& e = default_engine();
+    check_dims(m, n, r);
+    e.set_data(M, MLNMF_F64, false, m, n, n, 0, grid_h, grid_w, false);
+    e.initialization_bound(0, V_coarse, W, MLNMF_F64, r, lhs, rhs);
+  });
+}
+
 // ---------------------------------------------------------------------------
 int mlnmf_run_configuration(const double* M, size_t m, size_t n, size_t grid_h, size_t grid_w, size_t level_count,
                             int kind, int cycle, size_t rank, uint64_t seed, int budget_mode, double amount,
@@ -407,6 +426,15 @@ int mlnmf_session_error(mlnmf_session* s, double* out) {
 
 int mlnmf_session_norm2(mlnmf_session* s, size_t level, double* out) {
   return guard([&] { *out = s->e->norm2(level); });
+}
+
+int mlnmf_session_smoothness(mlnmf_session* s, size_t level, double* out) {
+  return guard([&] { *out = s->e->smoothness(level); });
+}
+
+int mlnmf_session_initialization_bound(mlnmf_session* s, size_t level, const void* V_coarse, const void* W_local,
+                                       int host_dtype, size_t r, double* lhs, double* rhs) {
+  return guard([&] { s->e->initialization_bound(level, V_coarse, W_local, host_dtype, r, lhs, rhs); });
 }
 
 int mlnmf_session_products(mlnmf_session* s, double* A, double* C) {

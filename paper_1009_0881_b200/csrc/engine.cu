@@ -727,6 +727,9 @@ void Engine::ensure_levels(size_t L) {
     };
     up(R, &cur.Rp, &cur.Ri, &cur.Rw);
     up(P, &cur.Pp, &cur.Pi, &cur.Pw);
+    double pf = 0.0;
+    for (double x : P.wt) pf += x * x;
+    cur.p_fro = std::sqrt(pf);
     Level nx{(cur.h + 1) / 2, (cur.w + 1) / 2, 0};
     nx.m = nx.h * nx.w;
     CK(dev_malloc(&nx.M, nx.m * n_loc_ * es));
@@ -756,6 +759,41 @@ double Engine::norm2(size_t l) {
     CK(cudaStreamSynchronize(impl_->s));
   }
   return L.norm2;
+}
+
+double Engine::smoothness(size_t l) {
+  ensure_levels(l + 2);
+  const double nrm2 = norm2(l);
+  if (!(nrm2 > 0.0)) throw std::invalid_argument("smoothness: undefined for the zero matrix");
+  const Level &F = lv_[l], &Cl = lv_[l + 1];
+  const size_t cb = ceil_div(n_loc_, 256);
+  const size_t ry = std::max<size_t>(1, std::min(F.m, ceil_div(kTargetBlocks, cb)));
+  impl_->part.ensure(cb * ry * 8);
+  double* part = impl_->part.as<double>();
+  double* sc = impl_->scal.as<double>();
+  if (opt_.dtype == 0)
+    impl_->launch(k_csr_residual<float>, dim3((unsigned)cb, (unsigned)ry), dim3(256), 0, (const int*)F.Pp,
+                  (const int*)F.Pi, (const double*)F.Pw, (const float*)Cl.M, (const float*)F.M, F.m, n_loc_, part);
+  else
+    impl_->launch(k_csr_residual<double>, dim3((unsigned)cb, (unsigned)ry), dim3(256), 0, (const int*)F.Pp,
+                  (const int*)F.Pi, (const double*)F.Pw, (const double*)Cl.M, (const double*)F.M, F.m, n_loc_, part);
+  impl_->launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part, cb * ry, sc + 5, 0);
+  impl_->allreduce_sum(sc + 5, 1);
+  double s = 0;
+  CK(cudaMemcpyAsync(&s, sc + 5, 8, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+  return std::sqrt(s) / std::sqrt(nrm2);
+}
+
+void Engine::initialization_bound(size_t l, const void* V_coarse, const void* W, int host_dtype, size_t r,
+                                  double* lhs, double* rhs) {
+  ensure_levels(l + 2);
+  set_factors(l + 1, V_coarse, W, host_dtype, r);
+  prolong_V(l);
+  *lhs = frobenius_error(l);
+  const double coarse_err = frobenius_error(l + 1);
+  const double sM = smoothness(l);
+  *rhs = sM * std::sqrt(norm2(l)) + lv_[l].p_fro * coarse_err;
 }
 
 void Engine::init_random(size_t r, uint64_t seed) {

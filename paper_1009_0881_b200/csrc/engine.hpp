@@ -109,6 +109,13 @@ class Engine {
 
   // ---- standalone kernels for the step-level C-ABI ----
   double frobenius_error(size_t l);  // sync
+  // diagnostics (transfer.cpp:128-153) over the resident pyramid, all ranks:
+  // s_M = ||M_l - P R M_l||_F / ||M_l||_F, and both sides of the coarse-
+  // initialization bound for V_coarse at level l+1 and W (overwrites the
+  // session's V at levels l, l+1 and W)
+  double smoothness(size_t l);
+  void initialization_bound(size_t l, const void* V_coarse, const void* W, int host_dtype, size_t r, double* lhs,
+                            double* rhs);
   void apply_transfer(size_t h, size_t w, int which, const double* X, size_t ncols, double* Y);
   void nnls_single(const double* G, const double* h, const double* x0, size_t r, double* x, int* iterations);
   void random_init_host(size_t m, size_t n, size_t r, uint64_t seed, double* V, double* W);
@@ -130,6 +137,7 @@ class Engine {
     void* M = nullptr;  // T[m x n_loc]
     void* V = nullptr;  // T[m x r]
     double norm2 = -1;
+    double p_fro = 0;  // ||P||_F of P: next -> this (TransferOperator::frobenius_norm)
     // R: this level -> next; P: next -> this (device CSR)
     int *Rp = nullptr, *Ri = nullptr, *Pp = nullptr, *Pi = nullptr;
     double *Rw = nullptr, *Pw = nullptr;

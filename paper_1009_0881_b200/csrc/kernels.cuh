@@ -612,6 +612,36 @@ __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restric
   Y[o * ncols + c] = to_t<T>(y);
 }
 
+// smoothness numerator, transfer.cpp:133-139: sum_ij (M_f - P M_c)_ij^2 with
+// M_c = R M_f (the next level's resident data), P applied on the fly in the
+// reference's entry order, so P R M is never stored.  Grid (colblocks, ry):
+// column-coalesced, rows strided by ry; one fp64 partial per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) k_csr_residual(const int* __restrict__ rowptr, const int* __restrict__ idx,
+                                                      const double* __restrict__ wt, const T* __restrict__ Mc,
+                                                      const T* __restrict__ Mf, size_t rows, size_t ncols,
+                                                      double* __restrict__ part) {
+  __shared__ double ws[8];
+  const size_t c = (size_t)blockIdx.x * 256 + threadIdx.x;
+  double s = 0.0;
+  if (c < ncols)
+    for (size_t o = blockIdx.y; o < rows; o += gridDim.y) {
+      const int eb = rowptr[o], ee = rowptr[o + 1];
+      double y = 0.0;
+      for (int e = eb; e < ee; ++e) y = __dadd_rn(y, __dmul_rn(wt[e], (double)Mc[(size_t)idx[e] * ncols + c]));
+      const double d = (double)Mf[o * ncols + c] - y;
+      s = fma(d, d, s);
+    }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // random_init (matrix.cpp:51-60) on the device: V row-major first, then W,
 // one SplitMix64 stream.  W is this rank's column slice [col0, col0+n_loc)

@@ -110,5 +110,34 @@ def main():
     print({k: float(v.mean()) for k, v in finals.items()})
 
 
+def diagnostics():
+    """smoothness / initialization_bound (transfer.cpp:128-153) on the
+    reference's own test shapes (test_transfer.cpp:155-220, acceptance.cpp:390-408)
+    plus larger odd grids; -> tests/golden/diagnostics.npz."""
+    ref = oracle.Reference()
+    rng = np.random.default_rng(1009)
+    out = {}
+    cb = np.array([[(i + j) % 2 for j in range(3)] for i in range(3)], np.float64)
+    cases = [("ones", 3, 3, np.ones((9, 4))), ("checker", 3, 3, cb.T.reshape(9, 1))]
+    for (h, w, n) in [(8, 7, 5), (19, 17, 3), (64, 64, 16), (33, 65, 7), (2, 2, 1)]:
+        cases.append((f"rand_{h}x{w}", h, w, rng.random((h * w, n))))
+    for name, h, w, M in cases:
+        out[f"s_{name}_M"] = M
+        out[f"s_{name}_hw"] = np.array([h, w])
+        out[f"s_{name}_s"] = np.array(ref.smoothness(M, h, w))
+    # acceptance criterion 9 shape draws: h, w in [2, 13], n in [1, 6], r in [1, 3]
+    for t in range(40):
+        h, w = int(rng.integers(2, 14)), int(rng.integers(2, 14))
+        n, r = int(rng.integers(1, 7)), int(rng.integers(1, 4))
+        hc, wc = (h + 1) // 2, (w + 1) // 2
+        M, Vc, W = rng.random((h * w, n)), rng.random((hc * wc, r)), rng.random((r, n))
+        out[f"b{t}_M"], out[f"b{t}_Vc"], out[f"b{t}_W"], out[f"b{t}_hw"] = M, Vc, W, np.array([h, w])
+        out[f"b{t}_lr"] = np.array(ref.initialization_bound(M, h, w, Vc, W))
+    out["n_bound"] = np.array(40)
+    np.savez_compressed(os.path.join(HERE, "diagnostics.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if "diagnostics" not in sys.argv[1:]:
+        main()
+    diagnostics()

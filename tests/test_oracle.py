@@ -44,6 +44,35 @@ def test_transfer_apply_golden(restated):
     assert np.array_equal(restated.apply_operator(19, 17, 1, G["apply_Xc"]), G["apply_P"])
 
 
+D = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "diagnostics.npz"))
+SMOOTH_CASES = sorted({k[2:-2] for k in D.files if k.startswith("s_") and k.endswith("_s")})
+
+
+@pytest.mark.parametrize("name", SMOOTH_CASES)
+def test_smoothness_golden(restated, name):
+    h, w = (int(x) for x in D[f"s_{name}_hw"])
+    assert restated.smoothness(D[f"s_{name}_M"], h, w) == float(D[f"s_{name}_s"])
+
+
+def test_initialization_bound_golden(restated):
+    for t in range(int(D["n_bound"])):
+        h, w = (int(x) for x in D[f"b{t}_hw"])
+        lhs, rhs = restated.initialization_bound(D[f"b{t}_M"], h, w, D[f"b{t}_Vc"], D[f"b{t}_W"])
+        assert (lhs, rhs) == tuple(D[f"b{t}_lr"]), t
+        assert lhs <= rhs * (1 + 1e-9)  # acceptance.cpp:405
+
+
+def test_diagnostics_known_answers(restated):
+    # test_transfer.cpp:155-160, 200-218
+    assert restated.smoothness(np.ones((9, 4)), 3, 3) == pytest.approx(0.0, abs=1e-15)
+    with pytest.raises(oracle.OracleError):
+        restated.smoothness(np.zeros((9, 4)), 3, 3)
+    C_ = np.full((9, 3), 0.5)
+    Cc = restated.apply_operator(3, 3, 0, C_)
+    lhs, rhs = restated.initialization_bound(C_, 3, 3, Cc[:, :1], np.ones((1, 3)))
+    assert lhs == pytest.approx(0.0, abs=1e-12) and rhs >= lhs
+
+
 @pytest.mark.parametrize("i", [0, 1, 2])
 def test_single_steps_golden(restated, i):
     M, V0, W0 = G[f"step{i}_M"], G[f"step{i}_V0"], G[f"step{i}_W0"]
