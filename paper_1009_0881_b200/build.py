@@ -20,6 +20,8 @@ REPO = os.path.dirname(HERE)
 
 SOURCES = ["engine.cu", "tc_gemm.cu", "hals_reg.cu", "scheduler.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CLI_SOURCES = ["cli_main.cpp", "host_io.cpp"]
+CLI = os.path.join(OUT_DIR, "mlnmf_b200")  # the CLI executable (reference: tools/mlnmf_main.cpp)
 
 
 def _nccl_paths():
@@ -89,6 +91,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([nvcc] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl", "-lpthread", "-lrt"])
+    # the CLI front-end (host C++ over the C-ABI); no -march and no fp
+    # contraction, so the synth generator rounds like the reference build
+    cli_src = [os.path.join(CSRC, s) for s in CLI_SOURCES]
+    if force or _stale(CLI, cli_src + _deps(cli_src[0]) + [LIB]):
+        run([os.environ.get("MLB_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"), "-std=c++20", "-O2", "-ffp-contract=off", "-Wall",
+             f"-I{os.path.join(REPO, 'include')}", f"-I{CSRC}", "-o", CLI] + cli_src +
+            [f"-L{OUT_DIR}", "-lmlnmf_b200", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 
