@@ -278,11 +278,13 @@ def run_b200(args):
     tc = s.tc_active
 
     e2e = None
-    if args.e2e and world == 1:
+    if args.e2e:
         host = torch.empty((M_ROWS, n_loc), dtype=torch.float32, pin_memory=True)
         s.export_data(host.data_ptr())
         s.close()
-        e2e = run_e2e(P, host, local, gemm, args.e2e_iters, norm)
+        # a fresh communicator for the e2e session (one NCCL id per communicator)
+        nid2 = bcast_obj(P.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+        e2e = run_e2e(P, host, local, gemm, args.e2e_iters, norm, world, rank, nid2, col0)
         del host
     else:
         s.close()
@@ -323,27 +325,31 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
 
 
-def run_e2e(P, host, local, gemm, iters, norm):
+def run_e2e(P, host, local, gemm, iters, norm, world=1, rank=0, nccl_id=None, col0=0):
     """One reference-facing solve through the C-ABI from pinned host memory:
-    set_data (H2D of M) + run_configuration(levels=1, HALS, none, r=64,
-    work:iters) + get_factors (D2H of V, W), wall-clock timed."""
+    set_data (H2D of this rank's columns of M) + run_configuration(levels=1,
+    HALS, none, r=64, work:iters) + get_factors (D2H of V and this rank's W
+    columns), wall-clock timed between barriers, max over ranks.  Byte counts
+    are whole-job (all ranks)."""
     import torch
     m, nl = host.shape
     Vh = torch.empty((m, RANK), dtype=torch.float32, pin_memory=True)
     Wh = torch.empty((RANK, nl), dtype=torch.float32, pin_memory=True)
     torch.cuda.synchronize()
-    se = P.Session(device=local, dtype=P.F32, gemm_path=gemm)
+    se = P.Session(device=local, dtype=P.F32, gemm_path=gemm, world=world, rank=rank, nccl_id=nccl_id)
+    barrier(world)
     t0 = time.perf_counter()
-    se.set_data_ptr(host.data_ptr(), P.F32, m, nl, P.ImageGrid(256, 256))
+    se.set_data_ptr(host.data_ptr(), P.F32, m, nl, P.ImageGrid(256, 256), n_total=N_TOTAL, col0=col0)
     tr = se.run_configuration(1, "hals", "none", RANK, 0, float(iters), 0)
     se.get_factors_ptr(Vh.data_ptr(), Wh.data_ptr(), P.F32)
-    wall = time.perf_counter() - t0
+    wall = allreduce_max(time.perf_counter() - t0, world)
     se.close()
     steps = int(tr.phase_steps.sum())
-    return {"value": steps / wall, "unit": UNIT, "h2d_bytes_per_step": m * nl * 4 / steps,
-            "d2h_bytes_per_step": (m * RANK + RANK * nl) * 4 / steps,
+    return {"value": steps / wall, "unit": UNIT, "h2d_bytes_per_step": m * N_TOTAL * 4 / steps,
+            "d2h_bytes_per_step": (world * m * RANK + RANK * N_TOTAL) * 4 / steps,
             "call": f"mlnmf_session_set_data + mlnmf_session_run_configuration(levels=1, hals, none, r=64, "
-                    f"work:{iters}, trace_every=0) + mlnmf_session_get_factors; pinned host fp32",
+                    f"work:{iters}, trace_every=0) + mlnmf_session_get_factors; pinned host fp32, "
+                    f"{world} rank(s), wall time max over ranks",
             "iters_per_call": steps, "wall_s": wall, "final_rel_error": float(tr.error[-1]) / norm}
 
 

@@ -872,14 +872,46 @@ __global__ void k_split_reduce(const double* __restrict__ part, size_t count, in
 // Per tile (128 columns J of M) x (64 rows I of M):
 //   P^T[j][i] = sum_k W[k][j] V[i][k]   (3xTF32: W^T_hi V_hi + W^T_hi V_lo + W^T_lo V_hi)
 // in TMEM (M_mma = 128 columns j, N = 64 rows i, K = r_pad), then the epilogue
-// sums (M[i][j] - P[i][j])^2 in fp32 per 32 and fp64 across.  Operands come
-// pre-split, K-major, row width 2 * rpa (hi | lo), rpa = r_pad rounded up to
-// whole 128-byte swizzle atoms.  A (W^T tile) stays in shared memory for all I
-// tiles of a J tile; each I tile's V slice and M tile (TMA, 4 boxes of 64 rows
-// x 128 B) stream through a 2-stage ring.  (Per-lane global loads of M ran at
-// 0.9 TB/s; the TMA-staged tile reads it at the HBM rate.)
+// sums (M[i][j] - P[i][j])^2 in fp32 per 32 and fp64
+// across.  Operands come pre-split, K-major, row width 2 * rpa (hi | lo),
+// rpa = r_pad rounded up to whole 128-byte swizzle atoms.  The A operand
+// (W^T tile) is loaded once per J tile into a TMEM buffer (TS form, default)
+// or kept in shared memory (SS form, MLB_TC_RES_TS=0); each I tile's V slice
+// and M tile (TMA, 4 boxes of 64 rows x 128 B) stream through separate rings,
+// released by the MMA commit and by the epilogue respectively.  Config-4
+// slice (n = 65536): SS 4.9 ms -> TS + separate rings 3.8 ms (4.5 TB/s).
+// (Per-lane global loads of M ran at 0.9 TB/s; the TMA-staged tile reads it
+// at the HBM rate.)
 // ----------------------------------------------------------------------------
-constexpr int kRThreads = (2 + 8) * 32;  // warp 0 TMA, warp 1 TMEM alloc + MMA, warps 2-9 epilogue
+constexpr int kRThreads = (2 + 8 + 1) * 32;  // warp 0 TMA (V, A), warp 1 TMEM alloc + MMA, warps 2-9 epilogue, warp 10 TMA (M)
+#ifndef MLB_TC_RES_TS
+#define MLB_TC_RES_TS 1
+#endif
+// TS form: the epilogue warps copy each J tile's W^T hi|lo into a TMEM A
+// buffer (double-buffered across J tiles), so the 3 x r/8 MMAs per tile read
+// only the V slices from shared memory (the SS form read both operands:
+// ~4.5 KB of shared memory traffic per KB of M, above the 128 B/clk port;
+// tools/mma_probe2.cu: SS at N = 64 runs at 2/3 of the TS rate).
+constexpr bool kResTS = MLB_TC_RES_TS != 0;
+constexpr int kResAcol0 = 256;                    // TMEM A buffers at columns 256 / 384
+// V slices and M tiles stream through separate rings: a V stage is released
+// by the MMA commit, an M stage by the epilogue.  TS: the W^T tile goes
+// global -> registers -> TMEM (no shared-memory landing zone), which leaves
+// room for a deeper M ring (the DRAM stream; V comes from L2).
+#ifndef MLB_TC_RES_VS
+#define MLB_TC_RES_VS 2
+#endif
+constexpr int kRVS = kResTS ? MLB_TC_RES_VS : 2;
+#ifndef MLB_TC_RES_MS
+#define MLB_TC_RES_MS 4
+#endif
+constexpr int kRMS = kResTS ? MLB_TC_RES_MS : 2;
+#ifndef MLB_TC_RES_ACC
+#define MLB_TC_RES_ACC 2
+#endif
+constexpr int kRAcc = kResTS ? MLB_TC_RES_ACC : 2;  // accumulator buffers (64 columns each, below the A buffers)
+static_assert(kRAcc * 64 <= 256, "residual TMEM map: accumulators in columns 0..255");
+constexpr int kResTmemCols = kResTS ? 512 : 128;  // accumulators at columns 0 / 64
 constexpr int kRAtomBytes = 128 * 128;    // one 128-row x 32-fp32 SW128 box
 constexpr int kRMBytes = 64 * 128 * 4;     // M tile: 64 rows i x 128 columns j
 
@@ -915,6 +947,7 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdes
 
 struct RParams {
   const float* M;
+  const float* wsplit;     // (TS) W^T split rows: n x 2 rpa, [hi | lo]
   int m, n, r, rp, atoms;  // atoms = rpa / 32
   int tj, ti;              // tile counts along n (J) and m (I)
   double* part;            // [gridDim.x] per-CTA sums
@@ -927,25 +960,39 @@ __global__ void __launch_bounds__(kRThreads, 1)
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int opa = 2 * p.atoms * kRAtomBytes;      // W^T tile: 128 j x 2 rpa (hi atoms, then lo atoms)
   const int opb = 2 * p.atoms * kRAtomBytes / 2;  // V tile: 64 i x 2 rpa
-  const int stage = opb + kRMBytes;               // V tile + M tile (64 i x 128 j, four 32-column boxes)
   unsigned char* sm_a = base;
-  unsigned char* sm_s = base + opa;               // 2 stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_s + 2 * stage);
-  uint64_t* afull = bars;       // A landed
-  uint64_t* aempty = bars + 1;  // MMAs of the J tile done
-  uint64_t* sfull = bars + 2;   // [2] V + M tile landed
-  uint64_t* sempty = bars + 4;  // [2] MMAs done (V) and epilogue done (M): 1 commit + 8 warps
-  uint64_t* cfull = bars + 6;   // [2] accumulator ready for the epilogue
-  uint64_t* cempty = bars + 8;  // [2] epilogue done with the accumulator
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 10);
+  unsigned char* sm_v = kResTS ? base : base + opa;  // kRVS V stages of opb bytes
+  unsigned char* sm_m = sm_v + kRVS * opb;           // kRMS M stages (64 i x 128 j, four 32-column boxes)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_m + kRMS * kRMBytes);
+  uint64_t* afull = bars;            // (SS) A landed
+  uint64_t* aempty = bars + 1;       // (SS) MMAs of the J tile done
+  uint64_t* vfull = bars + 2;        // [kRVS] V slice landed
+  uint64_t* vempty = vfull + kRVS;   // [kRVS] MMAs reading it done (commit)
+  uint64_t* mfull = vempty + kRVS;   // [kRMS] M tile landed
+  uint64_t* mempty = mfull + kRMS;   // [kRMS] epilogue done with it (8 warps)
+  uint64_t* cfull = mempty + kRMS;   // [kRAcc] accumulator ready for the epilogue
+  uint64_t* cempty = cfull + kRAcc;  // [kRAcc] epilogue done with the accumulator
+  uint64_t* aready = cempty + kRAcc;     // [2] (TS) W^T tile stored in TMEM A buffer b: 8 epilogue warps
+  uint64_t* tfree = aready + 2;      // [2] (TS) MMAs of the J tile in TMEM A buffer b done
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfree + 2);
   __shared__ double red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(afull), 1);
     mbar_init(smem_u32(aempty), 1);
+    for (int i = 0; i < kRVS; ++i) {
+      mbar_init(smem_u32(&vfull[i]), 1);
+      mbar_init(smem_u32(&vempty[i]), 1);
+    }
+    for (int i = 0; i < kRMS; ++i) {
+      mbar_init(smem_u32(&mfull[i]), 1);
+      mbar_init(smem_u32(&mempty[i]), 8);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&sfull[i]), 1);
-      mbar_init(smem_u32(&sempty[i]), 1 + 8);
+      mbar_init(smem_u32(&aready[i]), 8);
+      mbar_init(smem_u32(&tfree[i]), 1);
+    }
+    for (int i = 0; i < kRAcc; ++i) {
       mbar_init(smem_u32(&cfull[i]), 1);
       mbar_init(smem_u32(&cempty[i]), 8);
     }
@@ -953,7 +1000,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(128)
+                 "r"(kResTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -967,76 +1014,137 @@ __global__ void __launch_bounds__(kRThreads, 1)
     if (lane == 0) {
       int jc = 0, tc_ = 0;
       for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
-        mbar_wait(smem_u32(aempty), ((uint32_t)jc & 1u) ^ 1u);
-        mbar_expect_tx(smem_u32(afull), (uint32_t)opa);
-        for (int h = 0; h < 2; ++h)
-          for (int a = 0; a < p.atoms; ++a)
-            tma_load_2d(smem_u32(sm_a + (h * p.atoms + a) * kRAtomBytes), &map_w, h * p.atoms * 32 + a * 32, jt * 128,
-                        smem_u32(afull));
+        if (!kResTS) {
+          mbar_wait(smem_u32(aempty), ((uint32_t)jc & 1u) ^ 1u);
+          mbar_expect_tx(smem_u32(afull), (uint32_t)opa);
+          for (int h = 0; h < 2; ++h)
+            for (int a = 0; a < p.atoms; ++a)
+              tma_load_2d(smem_u32(sm_a + (h * p.atoms + a) * kRAtomBytes), &map_w, h * p.atoms * 32 + a * 32,
+                          jt * 128, smem_u32(afull));
+        }
         for (int it = 0; it < p.ti; ++it, ++tc_) {
-          const int st = tc_ & 1;
-          unsigned char* sb = sm_s + st * stage;
-          mbar_wait(smem_u32(&sempty[st]), ((uint32_t)(tc_ >> 1) & 1u) ^ 1u);
-          mbar_expect_tx(smem_u32(&sfull[st]), (uint32_t)stage);
+          const int st = tc_ % kRVS;
+          unsigned char* sb = sm_v + st * opb;
+          mbar_wait(smem_u32(&vempty[st]), ((uint32_t)(tc_ / kRVS) & 1u) ^ 1u);
+          mbar_expect_tx(smem_u32(&vfull[st]), (uint32_t)opb);
           for (int h = 0; h < 2; ++h)
             for (int a = 0; a < p.atoms; ++a)
               tma_load_2d(smem_u32(sb + (h * p.atoms + a) * (kRAtomBytes / 2)), &map_v, h * p.atoms * 32 + a * 32,
-                          it * 64, smem_u32(&sfull[st]));
-          for (int b = 0; b < 4; ++b)  // M rows i of the tile, 32 columns j per box
-            tma_load_2d(smem_u32(sb + opb + b * (kRMBytes / 4)), &map_m, jt * 128 + b * 32, it * 64,
-                        smem_u32(&sfull[st]));
+                          it * 64, smem_u32(&vfull[st]));
         }
       }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {
+      const uint64_t pol_m = l2_policy_evict_first();  // M is read once; keep the V / W slices in L2
+      int tc_ = 0;
+      for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x)
+        for (int it = 0; it < p.ti; ++it, ++tc_) {
+          const int st = tc_ % kRMS;
+          unsigned char* sb = sm_m + st * kRMBytes;
+          mbar_wait(smem_u32(&mempty[st]), ((uint32_t)(tc_ / kRMS) & 1u) ^ 1u);
+          mbar_expect_tx(smem_u32(&mfull[st]), (uint32_t)kRMBytes);
+          for (int b = 0; b < 4; ++b)  // M rows i of the tile, 32 columns j per box
+            tma_load_2d_hint(smem_u32(sb + b * (kRMBytes / 4)), &map_m, jt * 128 + b * 32, it * 64,
+                             smem_u32(&mfull[st]), pol_m);
+        }
     }
   } else if (warp == 1) {
     const uint32_t id = idesc_tf32(64);
-    const uint64_t da = sdesc_sw128(smem_u32(sm_a)), ds = sdesc_sw128(smem_u32(sm_s));
+    const uint64_t da = sdesc_sw128(smem_u32(sm_a)), ds = sdesc_sw128(smem_u32(sm_v));
     const uint64_t lo_a = (uint64_t)((p.atoms * kRAtomBytes) >> 4), lo_b = (uint64_t)((p.atoms * kRAtomBytes / 2) >> 4);
     const int ksteps = p.rp / 8;
     int jc = 0, tc_ = 0;
-    int lasts[2] = {-1, -1};
+    int lasts[kRVS];
+    for (int k = 0; k < kRVS; ++k) lasts[k] = -1;
     int lasta = -1;
+    int lastt[2] = {-1, -1};
+    const int rpa = p.atoms * 32;
     for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
-      mbar_wait(smem_u32(afull), (uint32_t)jc & 1u);
+      const uint32_t ab = (uint32_t)jc & 1u;
+      const uint32_t ta = kResAcol0 + ab * 128;  // TMEM A buffer: W^T hi in [ta, ta + rpa), lo after
+      if (kResTS)
+        mbar_wait(smem_u32(&aready[ab]), (uint32_t)(jc >> 1) & 1u);
+      else
+        mbar_wait(smem_u32(afull), (uint32_t)jc & 1u);
       for (int it = 0; it < p.ti; ++it, ++tc_) {
-        const int st = tc_ & 1, acc = tc_ & 1;
-        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;
+        const int st = tc_ % kRVS, acc = tc_ % kRAcc;
+        const uint32_t ph = (uint32_t)(tc_ / kRAcc) & 1u, sph = (uint32_t)(tc_ / kRVS) & 1u;
         mbar_wait(smem_u32(&cempty[acc]), ph ^ 1u);
-        mbar_wait(smem_u32(&sfull[st]), ph);
+        mbar_wait(smem_u32(&vfull[st]), sph);
         tc_fence_after();
         const uint32_t d = (uint32_t)(acc * 64);
-        const uint64_t dbs = ds + (uint64_t)((st * stage) >> 4);
+        const uint64_t dbs = ds + (uint64_t)((st * opb) >> 4);
         for (int kk = 0; kk < ksteps; ++kk) {
           const uint64_t oa = (uint64_t)(((kk >> 2) * kRAtomBytes + (kk & 3) * 32) >> 4);
           const uint64_t ob = (uint64_t)(((kk >> 2) * (kRAtomBytes / 2) + (kk & 3) * 32) >> 4);
-          mma_ss(d, da + oa, dbs + ob, id, kk > 0 ? 1u : 0u);   // W_hi V_hi
-          mma_ss(d, da + oa, dbs + lo_b + ob, id, 1u);          // W_hi V_lo
-          mma_ss(d, da + lo_a + oa, dbs + ob, id, 1u);          // W_lo V_hi
+          if (kResTS) {  // A (W^T hi / lo) from TMEM: only the V slices are read from shared memory
+            mma_ts(d, ta + kk * 8, dbs + ob, id, kk > 0 ? 1u : 0u);     // W_hi V_hi
+            mma_ts(d, ta + kk * 8, dbs + lo_b + ob, id, 1u);            // W_hi V_lo
+            mma_ts(d, ta + rpa + kk * 8, dbs + ob, id, 1u);             // W_lo V_hi
+          } else {
+            mma_ss(d, da + oa, dbs + ob, id, kk > 0 ? 1u : 0u);   // W_hi V_hi
+            mma_ss(d, da + oa, dbs + lo_b + ob, id, 1u);          // W_hi V_lo
+            mma_ss(d, da + lo_a + oa, dbs + ob, id, 1u);          // W_lo V_hi
+          }
         }
-        tc_commit(smem_u32(&sempty[st]));  // V tile free (the M tile is released by the epilogue)
+        tc_commit(smem_u32(&vempty[st]));  // V slice free (the M tile is released by the epilogue)
         tc_commit(smem_u32(&cfull[acc]));
-        lasts[st] = (int)ph;
+        lasts[st] = (int)sph;
         __syncwarp();
       }
-      tc_commit(smem_u32(aempty));
-      lasta = jc & 1;
+      if (kResTS) {
+        tc_commit(smem_u32(&tfree[ab]));  // TMEM A buffer reusable for J tile jc + 2
+        lastt[ab] = (jc >> 1) & 1;
+      } else {
+        tc_commit(smem_u32(aempty));
+        lasta = jc & 1;
+      }
       __syncwarp();
     }
-    // no commit arrival may land after exit: wait for the last sempty phase of
-    // each stage (its 8 epilogue arrivals follow the commit) and for aempty
-    for (int st = 0; st < 2; ++st)
-      if (lasts[st] >= 0) mbar_wait(smem_u32(&sempty[st]), (uint32_t)lasts[st]);
+    // no commit arrival may land after exit: wait for the last vempty phase of
+    // each V stage and for aempty / the TMEM A buffers
+    for (int st = 0; st < kRVS; ++st)
+      if (lasts[st] >= 0) mbar_wait(smem_u32(&vempty[st]), (uint32_t)lasts[st]);
     if (lasta >= 0) mbar_wait(smem_u32(aempty), (uint32_t)lasta);
+    for (int b = 0; b < 2; ++b)
+      if (lastt[b] >= 0) mbar_wait(smem_u32(&tfree[b]), (uint32_t)lastt[b]);
   } else {
     // epilogue: lane quarter q (TMEM lane = column j of M), half h (rows i of the tile)
     const int q = warp & 3, h = (warp - 2) >> 2;
-    int tc_ = 0;
-    for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x) {
+    int tc_ = 0, jc = 0;
+    for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
       const int jl = q * 32 + lane, j = jt * 128 + jl;
       const int b = jl >> 5, jb = jl & 31;  // M box and column within it
+      if (kResTS) {
+        // W^T row jl of this J tile -> TMEM A buffer (lane jl): warp half h
+        // moves the hi (h = 0) or lo (h = 1) atoms, 32 columns per atom
+        const uint32_t ab = (uint32_t)jc & 1u;
+        const int rpa = p.atoms * 32;
+        const float4* src = reinterpret_cast<const float4*>(p.wsplit + (size_t)j * 2 * rpa + h * rpa);
+        uint4 w[16];
+        for (int a = 0; a < p.atoms; ++a) {
+          // the row's 32 hi (h = 0) or lo (h = 1) values of atom a, straight
+          // from global (L2-resident split buffer), issued before the wait
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = j < p.n ? __ldg(src + a * 8 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            w[(a & 1) * 8 + c] = make_uint4(__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z),
+                                            __float_as_uint(x.w));
+          }
+          if (a == 0 && jc >= 2) mbar_wait<64>(smem_u32(&tfree[ab]), (uint32_t)((jc >> 1) - 1) & 1u);
+          tc_fence_after();
+          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + kResAcol0 + ab * 128 + (uint32_t)(h * rpa + a * 32),
+                    reinterpret_cast<const uint32_t(&)[32]>(w[(a & 1) * 8]));
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&aready[ab]));
+      }
       for (int it = 0; it < p.ti; ++it, ++tc_) {
-        const int acc = tc_ & 1, st = tc_ & 1;
-        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;
+        const int acc = tc_ % kRAcc, st = tc_ % kRMS;
+        const uint32_t ph = (uint32_t)(tc_ / kRAcc) & 1u;
         mbar_wait<128>(smem_u32(&cfull[acc]), ph);
         tc_fence_after();
         uint32_t v[32];
@@ -1047,9 +1155,10 @@ __global__ void __launch_bounds__(kRThreads, 1)
         if (lane == 0) mbar_arrive(smem_u32(&cempty[acc]));
         // M[i][j] from the staged tile (SW128 rows of 32 fp32: a warp reads one
         // 128-byte row per load, conflict-free)
-        const uint32_t mt = smem_u32(sm_s + st * stage + opb + b * (kRMBytes / 4));
+        mbar_wait<64>(smem_u32(&mfull[st]), (uint32_t)(tc_ / kRMS) & 1u);
+        const uint32_t mt = smem_u32(sm_m + st * kRMBytes + b * (kRMBytes / 4));
         const int i0 = it * 64 + h * 32;
-        float s32 = 0.f;
+        float s32 = 0.f;  // one fp32 chain (four independent chains measured 3 % slower)
 #pragma unroll
         for (int ii = 0; ii < 32; ++ii) {
           const int il = h * 32 + ii;
@@ -1058,15 +1167,16 @@ __global__ void __launch_bounds__(kRThreads, 1)
           s32 = (j < p.n && i0 + ii < p.m) ? fmaf(dlt, dlt, s32) : s32;
         }
         s64 += (double)s32;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&sempty[st]));  // M tile read
+        if (lane == 0) mbar_arrive(smem_u32(&mempty[st]));  // M tile read
       }
     }
   }
   // per-CTA sum (fixed order: deterministic)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
-  if (warp >= 2 && lane == 0) red[warp - 2] = s64;
+  if (warp >= 2 && warp < 10 && lane == 0) red[warp - 2] = s64;
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1076,7 +1186,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
   }
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kResTmemCols) : "memory");
   }
 }
 
@@ -1182,6 +1292,7 @@ class TcGemmImpl final : public TcGemm {
     }
     tc::RParams p{};
     p.M = M;
+    p.wsplit = static_cast<const float*>(rw_);
     p.m = (int)m;
     p.n = (int)n;
     p.r = (int)r;
@@ -1196,9 +1307,10 @@ class TcGemmImpl final : public TcGemm {
     const CUtensorMap mv = make_map(rv_, (uint64_t)2 * rpa, m, 32, 64, true);
     const CUtensorMap mm = make_map(M, n, m, 32, 64, true);
     const size_t opa = (size_t)2 * p.atoms * tc::kRAtomBytes;
-    const size_t smem = 1024 + opa + 2 * (opa / 2 + tc::kRMBytes) + 256;
+    const size_t smem = 1024 + (tc::kResTS ? 0 : opa) + tc::kRVS * (opa / 2) + tc::kRMS * tc::kRMBytes + 256;
     if (!resid_attr_) {
-      const size_t smax = 1024 + 4 * tc::kRAtomBytes + 2 * (2 * tc::kRAtomBytes + tc::kRMBytes) + 256;
+      const size_t smax =
+          1024 + (tc::kResTS ? 0 : 4 * tc::kRAtomBytes) + tc::kRVS * 2 * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
       TC_CK(cudaFuncSetAttribute(tc::k_tc_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
       resid_attr_ = true;
     }

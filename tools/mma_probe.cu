@@ -116,6 +116,8 @@ int main(int argc, char** argv) {
       {8, 256, 1, 0, 0, 0, 0, 128}, {8, 256, 2, 0, 0, 0, 0, 128}, {8, 128, 1, 0, 0, 0, 0, 128},
       {8, 64, 1, 0, 0, 0, 0, 128}, {8, 256, 1, 0, 0, 0, 1, 128}, {8, 256, 1, 1, 0, 0, 0, 128},
       {32, 256, 1, 0, 0, 0, 0, 128}, {8, 256, 1, 0, 0, 0, 0, 64},
+      {12, 64, 1, 1, 0, 0, 0, 128}, {12, 64, 1, 0, 0, 0, 0, 128}, {12, 64, 2, 1, 0, 0, 0, 128},
+      {12, 64, 2, 0, 0, 0, 0, 128}, {12, 128, 1, 1, 0, 0, 0, 128}, {12, 128, 1, 0, 0, 0, 0, 128},
   };
   const int iters = 1024;
   for (auto c : cfgs) {

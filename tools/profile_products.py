@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "auto"])
     ap.add_argument("--steps", type=int, default=0, help="also time full HALS steps")
+    ap.add_argument("--residual", type=int, default=0, help="also time this many error samples (||M - VW||_F)")
     a = ap.parse_args()
     import paper_1009_0881_b200 as P
     gemm = {"tc": P.GEMM_TCGEN05, "simt": P.GEMM_SIMT, "auto": P.GEMM_AUTO}[a.gemm]
@@ -36,6 +37,15 @@ def main():
         mw, vt = kt["mwt_ms"] / kt["mwt_n"], kt["vtm_ms"] / kt["vtm_n"]
         print(f"n={a.n} tc={s.tc_active} A=MW^T {mw:.3f} ms ({mb / mw / 1e6:.0f} GB/s)  "
               f"C=V^TM {vt:.3f} ms ({mb / vt / 1e6:.0f} GB/s)")
+        if a.residual:
+            import time
+            e0 = s.error()  # warm-up (split buffers, tensor maps)
+            s.sync()
+            t = time.perf_counter()
+            for _ in range(a.residual):
+                e = s.error()
+            dt = (time.perf_counter() - t) / a.residual
+            print(f"residual {dt * 1e3:.3f} ms ({mb / dt / 1e9:.0f} GB/s)  error {e:.10g} (first {e0:.10g})")
         if a.steps:
             s.set_profiling(False)
             import time
