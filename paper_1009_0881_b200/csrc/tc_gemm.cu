@@ -1381,7 +1381,8 @@ class TcGemmImpl final : public TcGemm {
     p.chunks_per_split = (int)cdiv(p.nchunks, splits);
     if (p.wide) {
       p.chunks_per_split += p.chunks_per_split & 1;
-      p.interleave = 0, p.rotate = 0;  // pairs must stay (c even, c + 1)
+      if (p.interleave == 1) p.interleave = 0;  // pairs must stay (c even, c + 1)
+      p.rotate = 0;
     }
     p.splits = p.interleave == 1 ? splits : (int)cdiv(p.nchunks, p.chunks_per_split);
     const size_t out_count = rows * r;
