@@ -872,48 +872,53 @@ __global__ void k_split_reduce(const double* __restrict__ part, size_t count, in
 // Per tile (128 columns J of M) x (64 rows I of M):
 //   P^T[j][i] = sum_k W[k][j] V[i][k]   (3xTF32: W^T_hi V_hi + W^T_hi V_lo + W^T_lo V_hi)
 // in TMEM (M_mma = 128 columns j, N = 64 rows i, K = r_pad), then the epilogue
-// sums (M[i][j] - P[i][j])^2 in fp32 per 32 and fp64
-// across.  Operands come pre-split, K-major, row width 2 * rpa (hi | lo),
-// rpa = r_pad rounded up to whole 128-byte swizzle atoms.  The A operand
-// (W^T tile) is loaded once per J tile into a TMEM buffer (TS form, default)
-// or kept in shared memory (SS form, MLB_TC_RES_TS=0); each I tile's V slice
-// and M tile (TMA, 4 boxes of 64 rows x 128 B) stream through separate rings,
-// released by the MMA commit and by the epilogue respectively.  Config-4
-// slice (n = 65536): SS 4.9 ms -> TS + separate rings 3.8 ms (4.5 TB/s).
+// sums (M[i][j] - P[i][j])^2 in fp32 per 32 and fp64 across.  Operands come
+// pre-split (k_split_rows), K-major, row width 2 * rpa (hi | lo), rpa = r_pad
+// rounded up to whole 128-byte swizzle atoms.
+//   A operand (W^T tile, 128 j x 2 rpa): loaded once per J tile by the
+//     epilogue warps, global -> registers -> a TMEM buffer (double-buffered
+//     across J tiles): TS form, so the MMAs read only V from shared memory
+//     (SS at N = 64 is shared-memory bound, 48 vs 32 cycles per MMA:
+//     tools/mma_probe2.cu).
+//   V slices (64 i x 2 rpa, L2) and M tiles (TMA, 4 boxes of 64 rows x 128 B,
+//     HBM, evict-first) stream through separate rings, released by the MMA
+//     commit and by the epilogue respectively.
+//   Two MMA warps take alternate I tiles (own V stage and accumulator), so one
+//     warp's barrier waits and commits overlap the other's MMAs (with a single
+//     MMA warp and no memory traffic at all the kernel ran at ~50 % of the
+//     tensor rate).
+// Config-4 slice (n = 65536): SS form 4.9 ms -> TS + separate rings 3.8 ms.
 // (Per-lane global loads of M ran at 0.9 TB/s; the TMA-staged tile reads it
 // at the HBM rate.)
 // ----------------------------------------------------------------------------
-constexpr int kRThreads = (2 + 8 + 1) * 32;  // warp 0 TMA (V, A), warp 1 TMEM alloc + MMA, warps 2-9 epilogue, warp 10 TMA (M)
-#ifndef MLB_TC_RES_TS
-#define MLB_TC_RES_TS 1
+// warps: 0 TMA (V), 1 MMA (1 allocates TMEM), 2 .. 2 + kREpi - 1 epilogue,
+// then TMA (M), then (optional) a second MMA warp taking the odd I tiles
+#ifndef MLB_TC_RES_EPI
+#define MLB_TC_RES_EPI 8
 #endif
-// TS form: the epilogue warps copy each J tile's W^T hi|lo into a TMEM A
-// buffer (double-buffered across J tiles), so the 3 x r/8 MMAs per tile read
-// only the V slices from shared memory (the SS form read both operands:
-// ~4.5 KB of shared memory traffic per KB of M, above the 128 B/clk port;
-// tools/mma_probe2.cu: SS at N = 64 runs at 2/3 of the TS rate).
-constexpr bool kResTS = MLB_TC_RES_TS != 0;
-constexpr int kResAcol0 = 256;                    // TMEM A buffers at columns 256 / 384
-// V slices and M tiles stream through separate rings: a V stage is released
-// by the MMA commit, an M stage by the epilogue.  TS: the W^T tile goes
-// global -> registers -> TMEM (no shared-memory landing zone), which leaves
-// room for a deeper M ring (the DRAM stream; V comes from L2).
+#ifndef MLB_TC_RES_MMA2
+#define MLB_TC_RES_MMA2 0
+#endif
+constexpr int kREpi = MLB_TC_RES_EPI;        // epilogue warps: 4 lane quarters x kREpi / 4 row groups
+constexpr int kRRows = 64 / (kREpi / 4);     // rows i per epilogue warp and tile
+constexpr int kRMmaWarps = MLB_TC_RES_MMA2 ? 2 : 1;
+constexpr int kRWarpM = 2 + kREpi, kRWarpMma1 = 3 + kREpi;
+constexpr int kRThreads = (3 + kREpi + (kRMmaWarps - 1)) * 32;
+static_assert(kREpi == 8 || kREpi == 16, "epilogue: 2 or 4 row groups per lane quarter");
+constexpr int kResAcol0 = 256;  // TMEM: accumulators at columns 0 / 64, A buffers at 256 / 384
 #ifndef MLB_TC_RES_VS
 #define MLB_TC_RES_VS 2
 #endif
-constexpr int kRVS = kResTS ? MLB_TC_RES_VS : 2;
+constexpr int kRVS = MLB_TC_RES_VS;  // V stages (tile t uses stage t % kRVS)
+static_assert(kRVS % 2 == 0, "V ring: whole pairs (accumulator / MMA-warp parity)");
 #ifndef MLB_TC_RES_MS
 #define MLB_TC_RES_MS 4
 #endif
-constexpr int kRMS = kResTS ? MLB_TC_RES_MS : 2;
-#ifndef MLB_TC_RES_ACC
-#define MLB_TC_RES_ACC 2
-#endif
-constexpr int kRAcc = kResTS ? MLB_TC_RES_ACC : 2;  // accumulator buffers (64 columns each, below the A buffers)
-static_assert(kRAcc * 64 <= 256, "residual TMEM map: accumulators in columns 0..255");
-constexpr int kResTmemCols = kResTS ? 512 : 128;  // accumulators at columns 0 / 64
-constexpr int kRAtomBytes = 128 * 128;    // one 128-row x 32-fp32 SW128 box
-constexpr int kRMBytes = 64 * 128 * 4;     // M tile: 64 rows i x 128 columns j
+constexpr int kRMS = MLB_TC_RES_MS;  // M stages
+constexpr int kRAcc = 2;             // accumulators (one per MMA warp)
+constexpr int kResTmemCols = 512;
+constexpr int kRAtomBytes = 128 * 128;  // one 128-row x 32-fp32 SW128 box
+constexpr int kRMBytes = 64 * 128 * 4;   // M tile: 64 rows i x 128 columns j
 
 // X -> S (rows x 2 rpa): [rna(x) | rna(x - rna(x))], zero padded.  trans: X is
 // r x rows (W, row-major) and row j of S comes from column j of X.
@@ -935,66 +940,66 @@ __global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S,
   }
 }
 
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 struct RParams {
   const float* M;
-  const float* wsplit;     // (TS) W^T split rows: n x 2 rpa, [hi | lo]
+  const float* wsplit;     // W^T split rows: n x 2 rpa, [hi | lo]
   int m, n, r, rp, atoms;  // atoms = rpa / 32
   int tj, ti;              // tile counts along n (J) and m (I)
   double* part;            // [gridDim.x] per-CTA sums
 };
 
+// The MMAs of one tile: K = KS x 8 (KS = 0: runtime p.rp / 8), A = TMEM
+// columns [ta, ta + rpa) (hi) and [ta + rpa, ...) (lo), B = the V stage.
+template <int KS>
+__device__ __forceinline__ void res_tile_mmas(uint32_t d, uint32_t ta, int rpa, uint64_t dbs, uint64_t lo_b,
+                                              uint32_t id, int ks_rt) {
+  const int ksteps = KS > 0 ? KS : ks_rt;
+#pragma unroll
+  for (int kk = 0; kk < (KS > 0 ? KS : 16); ++kk) {
+    if (KS == 0 && kk >= ksteps) break;
+    const uint64_t ob = (uint64_t)(((kk >> 2) * (kRAtomBytes / 2) + (kk & 3) * 32) >> 4);
+    mma_ts(d, ta + kk * 8, dbs + ob, id, kk > 0 ? 1u : 0u);  // W_hi V_hi
+    mma_ts(d, ta + kk * 8, dbs + lo_b + ob, id, 1u);         // W_hi V_lo
+    mma_ts(d, ta + rpa + kk * 8, dbs + ob, id, 1u);          // W_lo V_hi
+  }
+}
+
 __global__ void __launch_bounds__(kRThreads, 1)
-    k_tc_residual(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_v,
-                  const __grid_constant__ CUtensorMap map_m, const RParams p) {
+    k_tc_residual(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_m,
+                  const RParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int opa = 2 * p.atoms * kRAtomBytes;      // W^T tile: 128 j x 2 rpa (hi atoms, then lo atoms)
-  const int opb = 2 * p.atoms * kRAtomBytes / 2;  // V tile: 64 i x 2 rpa
-  unsigned char* sm_a = base;
-  unsigned char* sm_v = kResTS ? base : base + opa;  // kRVS V stages of opb bytes
-  unsigned char* sm_m = sm_v + kRVS * opb;           // kRMS M stages (64 i x 128 j, four 32-column boxes)
+  const int opb = p.atoms * kRAtomBytes;  // V slice: 64 i x 2 rpa
+  unsigned char* sm_v = base;                // kRVS V stages
+  unsigned char* sm_m = sm_v + kRVS * opb;   // kRMS M stages (64 i x 128 j, four 32-column boxes)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_m + kRMS * kRMBytes);
-  uint64_t* afull = bars;            // (SS) A landed
-  uint64_t* aempty = bars + 1;       // (SS) MMAs of the J tile done
-  uint64_t* vfull = bars + 2;        // [kRVS] V slice landed
-  uint64_t* vempty = vfull + kRVS;   // [kRVS] MMAs reading it done (commit)
-  uint64_t* mfull = vempty + kRVS;   // [kRMS] M tile landed
-  uint64_t* mempty = mfull + kRMS;   // [kRMS] epilogue done with it (8 warps)
-  uint64_t* cfull = mempty + kRMS;   // [kRAcc] accumulator ready for the epilogue
-  uint64_t* cempty = cfull + kRAcc;  // [kRAcc] epilogue done with the accumulator
-  uint64_t* aready = cempty + kRAcc;     // [2] (TS) W^T tile stored in TMEM A buffer b: 8 epilogue warps
-  uint64_t* tfree = aready + 2;      // [2] (TS) MMAs of the J tile in TMEM A buffer b done
+  uint64_t* vfull = bars;              // [kRVS] V slice landed
+  uint64_t* vempty = vfull + kRVS;     // [kRVS] MMAs reading it done (commit)
+  uint64_t* mfull = vempty + kRVS;     // [kRMS] M tile landed
+  uint64_t* mempty = mfull + kRMS;     // [kRMS] epilogue done with it (8 warps)
+  uint64_t* cfull = mempty + kRMS;     // [kRAcc] accumulator ready for the epilogue
+  uint64_t* cempty = cfull + kRAcc;    // [kRAcc] epilogue done with the accumulator
+  uint64_t* aready = cempty + kRAcc;   // [2] W^T tile stored in TMEM A buffer b (8 epilogue warps)
+  uint64_t* tfree = aready + 2;        // [2] both MMA warps done with TMEM A buffer b
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfree + 2);
-  __shared__ double red[8];
+  __shared__ double red[kREpi];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(smem_u32(afull), 1);
-    mbar_init(smem_u32(aempty), 1);
     for (int i = 0; i < kRVS; ++i) {
       mbar_init(smem_u32(&vfull[i]), 1);
       mbar_init(smem_u32(&vempty[i]), 1);
     }
     for (int i = 0; i < kRMS; ++i) {
       mbar_init(smem_u32(&mfull[i]), 1);
-      mbar_init(smem_u32(&mempty[i]), 8);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&aready[i]), 8);
-      mbar_init(smem_u32(&tfree[i]), 1);
+      mbar_init(smem_u32(&mempty[i]), kREpi);
     }
     for (int i = 0; i < kRAcc; ++i) {
       mbar_init(smem_u32(&cfull[i]), 1);
-      mbar_init(smem_u32(&cempty[i]), 8);
+      mbar_init(smem_u32(&cempty[i]), kREpi);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&aready[i]), kREpi);
+      mbar_init(smem_u32(&tfree[i]), kRMmaWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1011,30 +1016,29 @@ __global__ void __launch_bounds__(kRThreads, 1)
   double s64 = 0.0;
 
   if (warp == 0) {
+    // ---- TMA producer: V slices ----
     if (lane == 0) {
-      int jc = 0, tc_ = 0;
-      for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
-        if (!kResTS) {
-          mbar_wait(smem_u32(aempty), ((uint32_t)jc & 1u) ^ 1u);
-          mbar_expect_tx(smem_u32(afull), (uint32_t)opa);
-          for (int h = 0; h < 2; ++h)
-            for (int a = 0; a < p.atoms; ++a)
-              tma_load_2d(smem_u32(sm_a + (h * p.atoms + a) * kRAtomBytes), &map_w, h * p.atoms * 32 + a * 32,
-                          jt * 128, smem_u32(afull));
-        }
+      int tc_ = 0;
+      for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x)
         for (int it = 0; it < p.ti; ++it, ++tc_) {
           const int st = tc_ % kRVS;
           unsigned char* sb = sm_v + st * opb;
           mbar_wait(smem_u32(&vempty[st]), ((uint32_t)(tc_ / kRVS) & 1u) ^ 1u);
+#ifdef MLB_TC_RES_EXP_NOV
+          if (tc_ >= kRVS) {  // timing experiment only: reuse the first V slices (wrong results)
+            mbar_arrive(smem_u32(&vfull[st]));
+            continue;
+          }
+#endif
           mbar_expect_tx(smem_u32(&vfull[st]), (uint32_t)opb);
           for (int h = 0; h < 2; ++h)
             for (int a = 0; a < p.atoms; ++a)
               tma_load_2d(smem_u32(sb + (h * p.atoms + a) * (kRAtomBytes / 2)), &map_v, h * p.atoms * 32 + a * 32,
                           it * 64, smem_u32(&vfull[st]));
         }
-      }
     }
-  } else if (warp == 10) {
+  } else if (warp == kRWarpM) {
+    // ---- TMA producer: M tiles ----
     if (lane == 0) {
       const uint64_t pol_m = l2_policy_evict_first();  // M is read once; keep the V / W slices in L2
       int tc_ = 0;
@@ -1043,99 +1047,87 @@ __global__ void __launch_bounds__(kRThreads, 1)
           const int st = tc_ % kRMS;
           unsigned char* sb = sm_m + st * kRMBytes;
           mbar_wait(smem_u32(&mempty[st]), ((uint32_t)(tc_ / kRMS) & 1u) ^ 1u);
+#ifdef MLB_TC_RES_EXP_NOM
+          if (tc_ >= kRMS) {  // timing experiment only: reuse the first M tiles (wrong results)
+            mbar_arrive(smem_u32(&mfull[st]));
+            continue;
+          }
+#endif
           mbar_expect_tx(smem_u32(&mfull[st]), (uint32_t)kRMBytes);
           for (int b = 0; b < 4; ++b)  // M rows i of the tile, 32 columns j per box
             tma_load_2d_hint(smem_u32(sb + b * (kRMBytes / 4)), &map_m, jt * 128 + b * 32, it * 64,
                              smem_u32(&mfull[st]), pol_m);
         }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (kRMmaWarps == 2 && warp == kRWarpMma1)) {
+    // ---- MMA issuer(s): with two, warp w takes the I tiles with tc_ % 2 == w ----
+    const int w = warp == 1 ? 0 : 1;
     const uint32_t id = idesc_tf32(64);
-    const uint64_t da = sdesc_sw128(smem_u32(sm_a)), ds = sdesc_sw128(smem_u32(sm_v));
-    const uint64_t lo_a = (uint64_t)((p.atoms * kRAtomBytes) >> 4), lo_b = (uint64_t)((p.atoms * kRAtomBytes / 2) >> 4);
-    const int ksteps = p.rp / 8;
-    int jc = 0, tc_ = 0;
-    int lasts[kRVS];
-    for (int k = 0; k < kRVS; ++k) lasts[k] = -1;
-    int lasta = -1;
+    const uint64_t ds = sdesc_sw128(smem_u32(sm_v));
+    const uint64_t lo_b = (uint64_t)((p.atoms * kRAtomBytes / 2) >> 4);
+    const int rpa = p.atoms * 32, ks_rt = p.rp / 8;
+    int jc = 0, tc_ = 0, lastv[kRVS];
+    for (int k = 0; k < kRVS; ++k) lastv[k] = -1;
     int lastt[2] = {-1, -1};
-    const int rpa = p.atoms * 32;
     for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
       const uint32_t ab = (uint32_t)jc & 1u;
       const uint32_t ta = kResAcol0 + ab * 128;  // TMEM A buffer: W^T hi in [ta, ta + rpa), lo after
-      if (kResTS)
-        mbar_wait(smem_u32(&aready[ab]), (uint32_t)(jc >> 1) & 1u);
-      else
-        mbar_wait(smem_u32(afull), (uint32_t)jc & 1u);
+      mbar_wait(smem_u32(&aready[ab]), (uint32_t)(jc >> 1) & 1u);
       for (int it = 0; it < p.ti; ++it, ++tc_) {
-        const int st = tc_ % kRVS, acc = tc_ % kRAcc;
-        const uint32_t ph = (uint32_t)(tc_ / kRAcc) & 1u, sph = (uint32_t)(tc_ / kRVS) & 1u;
-        mbar_wait(smem_u32(&cempty[acc]), ph ^ 1u);
-        mbar_wait(smem_u32(&vfull[st]), sph);
+        if (kRMmaWarps == 2 && (tc_ & 1) != w) continue;
+        const int sa = tc_ & 1, sv = tc_ % kRVS;        // accumulator = tile parity; V stage
+        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;  // tile tc_ is use tc_ / 2 of accumulator sa
+        const uint32_t vph = (uint32_t)(tc_ / kRVS) & 1u;
+        mbar_wait(smem_u32(&cempty[sa]), ph ^ 1u);
+        mbar_wait(smem_u32(&vfull[sv]), vph);
         tc_fence_after();
-        const uint32_t d = (uint32_t)(acc * 64);
-        const uint64_t dbs = ds + (uint64_t)((st * opb) >> 4);
-        for (int kk = 0; kk < ksteps; ++kk) {
-          const uint64_t oa = (uint64_t)(((kk >> 2) * kRAtomBytes + (kk & 3) * 32) >> 4);
-          const uint64_t ob = (uint64_t)(((kk >> 2) * (kRAtomBytes / 2) + (kk & 3) * 32) >> 4);
-          if (kResTS) {  // A (W^T hi / lo) from TMEM: only the V slices are read from shared memory
-            mma_ts(d, ta + kk * 8, dbs + ob, id, kk > 0 ? 1u : 0u);     // W_hi V_hi
-            mma_ts(d, ta + kk * 8, dbs + lo_b + ob, id, 1u);            // W_hi V_lo
-            mma_ts(d, ta + rpa + kk * 8, dbs + ob, id, 1u);             // W_lo V_hi
-          } else {
-            mma_ss(d, da + oa, dbs + ob, id, kk > 0 ? 1u : 0u);   // W_hi V_hi
-            mma_ss(d, da + oa, dbs + lo_b + ob, id, 1u);          // W_hi V_lo
-            mma_ss(d, da + lo_a + oa, dbs + ob, id, 1u);          // W_lo V_hi
-          }
-        }
-        tc_commit(smem_u32(&vempty[st]));  // V slice free (the M tile is released by the epilogue)
-        tc_commit(smem_u32(&cfull[acc]));
-        lasts[st] = (int)sph;
+        const uint32_t d = (uint32_t)(sa * 64);
+        const uint64_t dbs = ds + (uint64_t)((sv * opb) >> 4);
+        if (ks_rt == 8)
+          res_tile_mmas<8>(d, ta, rpa, dbs, lo_b, id, ks_rt);
+        else
+          res_tile_mmas<0>(d, ta, rpa, dbs, lo_b, id, ks_rt);
+        tc_commit(smem_u32(&vempty[sv]));  // V slice free (the M tile is released by the epilogue)
+        tc_commit(smem_u32(&cfull[sa]));
+        lastv[sv] = (int)vph;
         __syncwarp();
       }
-      if (kResTS) {
-        tc_commit(smem_u32(&tfree[ab]));  // TMEM A buffer reusable for J tile jc + 2
-        lastt[ab] = (jc >> 1) & 1;
-      } else {
-        tc_commit(smem_u32(aempty));
-        lasta = jc & 1;
-      }
+      tc_commit(smem_u32(&tfree[ab]));  // this warp is done with TMEM A buffer ab (count 2)
+      lastt[ab] = (jc >> 1) & 1;
       __syncwarp();
     }
-    // no commit arrival may land after exit: wait for the last vempty phase of
-    // each V stage and for aempty / the TMEM A buffers
-    for (int st = 0; st < kRVS; ++st)
-      if (lasts[st] >= 0) mbar_wait(smem_u32(&vempty[st]), (uint32_t)lasts[st]);
-    if (lasta >= 0) mbar_wait(smem_u32(aempty), (uint32_t)lasta);
+    // no commit arrival may land after exit
+    for (int k = 0; k < kRVS; ++k)
+      if (lastv[k] >= 0) mbar_wait(smem_u32(&vempty[k]), (uint32_t)lastv[k]);
     for (int b = 0; b < 2; ++b)
       if (lastt[b] >= 0) mbar_wait(smem_u32(&tfree[b]), (uint32_t)lastt[b]);
   } else {
-    // epilogue: lane quarter q (TMEM lane = column j of M), half h (rows i of the tile)
+    // ---- epilogue: lane quarter q (TMEM lane = column j of M), row group h (kRRows rows i of the tile) ----
     const int q = warp & 3, h = (warp - 2) >> 2;
+    const int rpa = p.atoms * 32;
     int tc_ = 0, jc = 0;
     for (int jt = blockIdx.x; jt < p.tj; jt += gridDim.x, ++jc) {
       const int jl = q * 32 + lane, j = jt * 128 + jl;
       const int b = jl >> 5, jb = jl & 31;  // M box and column within it
-      if (kResTS) {
-        // W^T row jl of this J tile -> TMEM A buffer (lane jl): warp half h
-        // moves the hi (h = 0) or lo (h = 1) atoms, 32 columns per atom
+      {
+        // W^T row jl of this J tile -> TMEM A buffer (lane jl), straight from
+        // the (L2-resident) split buffer: the row's 2 x atoms 32-column pieces
+        // (hi atoms, then lo atoms) are shared out over the kREpi / 4 warps of
+        // the lane quarter
         const uint32_t ab = (uint32_t)jc & 1u;
-        const int rpa = p.atoms * 32;
-        const float4* src = reinterpret_cast<const float4*>(p.wsplit + (size_t)j * 2 * rpa + h * rpa);
-        uint4 w[16];
-        for (int a = 0; a < p.atoms; ++a) {
-          // the row's 32 hi (h = 0) or lo (h = 1) values of atom a, straight
-          // from global (L2-resident split buffer), issued before the wait
+        const float4* src = reinterpret_cast<const float4*>(p.wsplit + (size_t)j * 2 * rpa);
+        bool waited = jc < 2;
+        for (int pc = h; pc < 2 * p.atoms; pc += kREpi / 4) {
+          uint4 wv[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 x = j < p.n ? __ldg(src + a * 8 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-            w[(a & 1) * 8 + c] = make_uint4(__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z),
-                                            __float_as_uint(x.w));
+            const float4 x = j < p.n ? __ldg(src + pc * 8 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            wv[c] = make_uint4(__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
           }
-          if (a == 0 && jc >= 2) mbar_wait<64>(smem_u32(&tfree[ab]), (uint32_t)((jc >> 1) - 1) & 1u);
+          if (!waited) mbar_wait<64>(smem_u32(&tfree[ab]), (uint32_t)((jc >> 1) - 1) & 1u), waited = true;
           tc_fence_after();
-          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + kResAcol0 + ab * 128 + (uint32_t)(h * rpa + a * 32),
-                    reinterpret_cast<const uint32_t(&)[32]>(w[(a & 1) * 8]));
+          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + kResAcol0 + ab * 128 + (uint32_t)(pc * 32),
+                    reinterpret_cast<const uint32_t(&)[32]>(wv));
         }
         tmem_wait_st();
         tc_fence_before();
@@ -1143,12 +1135,16 @@ __global__ void __launch_bounds__(kRThreads, 1)
         if (lane == 0) mbar_arrive(smem_u32(&aready[ab]));
       }
       for (int it = 0; it < p.ti; ++it, ++tc_) {
-        const int acc = tc_ % kRAcc, st = tc_ % kRMS;
-        const uint32_t ph = (uint32_t)(tc_ / kRAcc) & 1u;
+        const int acc = tc_ & 1, st = tc_ % kRMS;
+        const uint32_t ph = (uint32_t)(tc_ >> 1) & 1u;
         mbar_wait<128>(smem_u32(&cfull[acc]), ph);
         tc_fence_after();
         uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + h * 32, v);
+        if (kRRows == 32)
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + h * 32, v);
+        else
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + h * kRRows,
+                    reinterpret_cast<uint32_t(&)[16]>(v));
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -1157,11 +1153,11 @@ __global__ void __launch_bounds__(kRThreads, 1)
         // 128-byte row per load, conflict-free)
         mbar_wait<64>(smem_u32(&mfull[st]), (uint32_t)(tc_ / kRMS) & 1u);
         const uint32_t mt = smem_u32(sm_m + st * kRMBytes + b * (kRMBytes / 4));
-        const int i0 = it * 64 + h * 32;
+        const int i0 = it * 64 + h * kRRows;
         float s32 = 0.f;  // one fp32 chain (four independent chains measured 3 % slower)
 #pragma unroll
-        for (int ii = 0; ii < 32; ++ii) {
-          const int il = h * 32 + ii;
+        for (int ii = 0; ii < kRRows; ++ii) {
+          const int il = h * kRRows + ii;
           const float mval = lds32(mt + il * 128 + ((((jb >> 2) ^ (il & 7)) << 4) | ((jb & 3) << 2)));
           const float dlt = mval - __uint_as_float(v[ii]);
           s32 = (j < p.n && i0 + ii < p.m) ? fmaf(dlt, dlt, s32) : s32;
@@ -1176,12 +1172,12 @@ __global__ void __launch_bounds__(kRThreads, 1)
   // per-CTA sum (fixed order: deterministic)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
-  if (warp >= 2 && warp < 10 && lane == 0) red[warp - 2] = s64;
+  if (warp >= 2 && warp < 2 + kREpi && lane == 0) red[warp - 2] = s64;
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
+    for (int w = 0; w < kREpi; ++w) t += red[w];
     p.part[blockIdx.x] = t;
   }
   if (warp == 1) {
@@ -1303,18 +1299,17 @@ class TcGemmImpl final : public TcGemm {
     const int grid = std::min(p.tj, sms_);
     ensure(&part_, &part_bytes_, (size_t)grid * 8);
     p.part = static_cast<double*>(part_);
-    const CUtensorMap mw = make_map(rw_, (uint64_t)2 * rpa, n, 32, 128, true);
     const CUtensorMap mv = make_map(rv_, (uint64_t)2 * rpa, m, 32, 64, true);
     const CUtensorMap mm = make_map(M, n, m, 32, 64, true);
-    const size_t opa = (size_t)2 * p.atoms * tc::kRAtomBytes;
-    const size_t smem = 1024 + (tc::kResTS ? 0 : opa) + tc::kRVS * (opa / 2) + tc::kRMS * tc::kRMBytes + 256;
+    // V stages (64 rows x 2 rpa) + M stages + barriers; the launch is one CTA
+    // per SM at every rank (512 TMEM columns)
+    const size_t smem = 1024 + (size_t)tc::kRVS * p.atoms * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
     if (!resid_attr_) {
-      const size_t smax =
-          1024 + (tc::kResTS ? 0 : 4 * tc::kRAtomBytes) + tc::kRVS * 2 * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
+      const size_t smax = 1024 + (size_t)tc::kRVS * 2 * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
       TC_CK(cudaFuncSetAttribute(tc::k_tc_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
       resid_attr_ = true;
     }
-    tc::k_tc_residual<<<grid, tc::kRThreads, smem, s>>>(mw, mv, mm, p);
+    tc::k_tc_residual<<<grid, tc::kRThreads, smem, s>>>(mv, mm, p);
     TC_CK(cudaGetLastError());
     tc::k_sum_parts<<<1, 256, 0, s>>>(static_cast<const double*>(part_), grid, out);
     TC_CK(cudaGetLastError());

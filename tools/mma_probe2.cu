@@ -93,5 +93,10 @@ int main() {
   run<128, 1, true>(d, 148);
   run<64, 4, true>(d, 148);
   run<256, 1, false>(d, 1);
+  // one accumulation chain vs independent accumulators at N = 64 (TS)
+  run<64, 1, true>(d, 148);
+  run<64, 2, true>(d, 148);
+  run<64, 3, true>(d, 148);
+  run<128, 1, true>(d, 148);
   return 0;
 }
