@@ -205,6 +205,44 @@ __device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// CTA pairs (cta_group::2): the peer-visible address of a shared-memory
+// location in CTA `cta` of the cluster, and a release arrive on it
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(cta));
+  return r;
+}
+// (default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive: a
+// .cluster-scope release compiles to a MEMBAR that stalled the converters and
+// the epilogue ~100k samples in ncu and made the pair kernel 1.6x slower)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory, completion counted on an mbarrier that
+// may live in the peer CTA of the pair (the leader's)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar_c,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar_c), "l"(pol)
+      : "memory");
+}
+// pair commit: arrives on the barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(mbar),
+      "h"((uint16_t)3)
+      : "memory");
+}
 // warp-wide call; one elected lane commits
 __device__ __forceinline__ void tc_commit(uint32_t mbar) {
   asm volatile(
@@ -285,9 +323,10 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)2u << 61;                 // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128.
-__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// Instruction descriptor: D f32, A/B tf32, K-major both, N, M (128; 256 for
+// a CTA pair).
+__host__ __device__ constexpr uint32_t idesc_tf32(int N, int M = 128) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // One pipeline chunk (K = 32, four K-steps of 8) on staging slot S into
@@ -328,30 +367,37 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc, uint32_t id_full, ui
 // (rows 0..r_pad of the stage, then rows r_pad..2 r_pad).  Half the TMEM
 // columns of the stacked form, so 6 staging slots fit and the epilogue drains
 // half as much.
-template <int S, int ACC>
+#define MLB_ISSUE3(CG)                                                                                        \
+  asm volatile(                                                                                              \
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"                                                              \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                      \
+      "setp.eq.u32 p, %12, 0;\n\t"                                                                           \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%1], %3, %11, p;\n\t"                              \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%13], %4, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%14], %5, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%15], %6, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%2], %3, %11, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%16], %4, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%17], %5, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%18], %6, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%1], %7, %11, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%13], %8, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%14], %9, %11, 1;\n\t"                             \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%15], %10, %11, 1;\n\t}" ::"r"(d),                \
+      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2),      \
+      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24),   \
+      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24)                                                         \
+      : "memory")
+// PAIR: the same 12 MMAs as one CTA-pair instruction stream (cta_group::2,
+// M = 256: A from each CTA's own TMEM slot, B rows split r_pad / 2 per CTA)
+template <int S, int ACC, bool PAIR = false>
 __device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first) {
   constexpr uint32_t d = ACC * kAccStride;
   constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.eq.u32 p, %12, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %11, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %4, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %5, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %6, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%16], %4, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%17], %5, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%18], %6, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %7, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %8, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %9, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %10, %11, 1;\n\t}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2),
-      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24),
-      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24)
-      : "memory");
+  if constexpr (PAIR)
+    MLB_ISSUE3("2");
+  else
+    MLB_ISSUE3("1");
 }
 
 // Optional event trace of CTA 0 (build with -DMLB_TC_TRACE=1; tools/tc_trace.py).
@@ -443,11 +489,12 @@ __device__ __forceinline__ int unit_chunk(const Params& p, const Unit& x, int i)
 // single issuing warp stalls inside the MMAs and its per-chunk waits and
 // commits leave the pipe idle; with two, one warp's bookkeeping overlaps the
 // other's MMAs.
-template <int W>
-__device__ __forceinline__ void mma_role(const Params& p, int total_units, uint64_t bdesc0, uint64_t* ready,
+template <int W, bool PAIR>
+__device__ __forceinline__ void mma_role(const Params& p, int total_units, int u0, int ustep, bool issue,
+                                         uint64_t bdesc0, uint64_t* ready,
                                          uint64_t* sdone, uint64_t* bfull, uint64_t* bempty, uint64_t* afull,
                                          uint64_t* aempty) {
-  const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp);
+  const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp, PAIR ? 256 : 128);
   int g = 0;
   int wc = 0;  // windows this warp has opened (all units): buffer wc % kAccBufs
   int lastph[kSlots / 2];    // parity of the last commit on this warp's slots W, W + 2, ...
@@ -456,7 +503,8 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
   int lastb[kBStages];       // ... and on the factor-slice stages this warp used
 #pragma unroll
   for (int k = 0; k < kBStages; ++k) lastb[k] = -1;
-  for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+  static_assert(!PAIR || kK3, "CTA pairs: K3 form only");
+  for (int u = u0; u < total_units; u += ustep) {
     const int n_u = unit_of(p, u).n;
     for (int i = own_first(g, W), j = 0; i < n_u; i += 2, ++j) {
       const int gg = g + i, slot = gg % kSlots;
@@ -466,8 +514,16 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       // warps for the drain -- at alternating times, not together
       const int wpos = (j + W * (kWindow / 2)) % kWindow;
       const int abuf = wc % kAccBufs, abar = W * kAccBufs + abuf;
-      if (wpos == 0 || j == 0) mbar_wait(smem_u32(&aempty[abar]), ((uint32_t)(wc / kAccBufs) & 1u) ^ 1u);
       const int bs = gg % kBStages;
+      if (!issue) {
+        // peer CTA of a pair: no MMAs here, only the bookkeeping of the
+        // leader's multicast commits for the drain below
+        lastph[slot >> 1] = (int)sph;
+        lastb[bs] = (int)((gg / kBStages) & 1);
+        if (wpos == kWindow - 1 || i + 2 >= n_u) ++wc;
+        continue;
+      }
+      if (wpos == 0 || j == 0) mbar_wait(smem_u32(&aempty[abar]), ((uint32_t)(wc / kAccBufs) & 1u) ^ 1u);
       mbar_wait(smem_u32(&ready[slot]), sph);
       mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(gg / kBStages) & 1u);
       TCT(4, gg);
@@ -476,17 +532,18 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
       const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4);
       TCT(7, gg);  // issue start (after the waits and the fence)
       if constexpr (kK3) {
-        const uint64_t bd_lo = bd + ((uint64_t)(p.rp * 128) >> 4);  // F_lo rows of the stage
+        // F_lo rows of the stage (PAIR: each CTA holds r_pad / 2 rows of each)
+        const uint64_t bd_lo = bd + ((uint64_t)((PAIR ? p.rp / 2 : p.rp) * 128) >> 4);
         constexpr int A0 = W * kAccBufs, A1 = W * kAccBufs + (kAccBufs > 1 ? 1 : 0);
         const int sidx = slot >> 1;  // this warp's slots are W, W + 2, ...
         if (abuf == 0) {
-          if (sidx == 0) issue_chunk3<W, A0>(bd, bd_lo, id_hi, first);
-          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0>(bd, bd_lo, id_hi, first);
-          else issue_chunk3<(W + 4) % kSlots, A0>(bd, bd_lo, id_hi, first);
+          if (sidx == 0) issue_chunk3<W, A0, PAIR>(bd, bd_lo, id_hi, first);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0, PAIR>(bd, bd_lo, id_hi, first);
+          else issue_chunk3<(W + 4) % kSlots, A0, PAIR>(bd, bd_lo, id_hi, first);
         } else {
-          if (sidx == 0) issue_chunk3<W, A1>(bd, bd_lo, id_hi, first);
-          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1>(bd, bd_lo, id_hi, first);
-          else issue_chunk3<(W + 4) % kSlots, A1>(bd, bd_lo, id_hi, first);
+          if (sidx == 0) issue_chunk3<W, A1, PAIR>(bd, bd_lo, id_hi, first);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
+          else issue_chunk3<(W + 4) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
         }
       } else {
         if (slot == W)
@@ -494,13 +551,21 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
         else
           issue_chunk<(W + 2) % kSlots, W>(bd, id_full, id_hi, first);
       }
-      tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
-      tc_commit(smem_u32(&bempty[bs]));    // ... and the factor-slice stage
+      if (PAIR) {  // both CTAs' slots and factor halves
+        tc_commit_pair(smem_u32(&sdone[slot]));
+        tc_commit_pair(smem_u32(&bempty[bs]));
+      } else {
+        tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
+        tc_commit(smem_u32(&bempty[bs]));    // ... and the factor-slice stage
+      }
       lastph[slot >> 1] = (int)sph;
       lastb[bs] = (int)((gg / kBStages) & 1);
       TCT(5, gg);
       if (wpos == kWindow - 1 || i + 2 >= n_u) {
-        tc_commit(smem_u32(&afull[abar]));
+        if (PAIR)
+          tc_commit_pair(smem_u32(&afull[abar]));
+        else
+          tc_commit(smem_u32(&afull[abar]));
         ++wc;
       }
       __syncwarp();
@@ -514,7 +579,14 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, uint6
     if (lastb[k] >= 0) mbar_wait(smem_u32(&bempty[k]), (uint32_t)lastb[k]);
 }
 
-template <bool TRANS>
+// PAIR: CTA pairs (clusters of 2 on one TPC) share a 256-row tile: each CTA
+// streams and converts its own 128 rows into its own TMEM, loads half of
+// each factor slice (r_pad / 2 rows of F_hi and of F_lo), and the leader
+// (rank 0) issues cta_group::2 MMAs (M = 256) for both; its commits are
+// multicast to both CTAs' barriers, and the peer's converters / epilogue
+// arrive on the leader's barriers.  Per SM this halves the factor-slice
+// traffic (TMA and MMA reads of shared memory) and the MMA issue work.
+template <bool TRANS, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
                  const Params p) {
@@ -539,6 +611,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 2 * kAccBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kTileRows = PAIR ? 256 : 128;
+  static_assert(!PAIR || MLB_TC_BSINGLE, "CTA pairs: single factor-slice producer");
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const int row0 = (int)crank * 128;  // this CTA's rows within a tile
+  const int u0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMGroups; ++i) {
@@ -546,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&mempty[i]), 4 * kMGroup);  // 4 converter warps per slice
     }
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(smem_u32(&ready[i]), 4);  // the 4 converter warps
+      mbar_init(smem_u32(&ready[i]), PAIR ? 8 : 4);  // the 4 converter warps (of both CTAs)
       mbar_init(smem_u32(&sdone[i]), 1);
     }
     for (int i = 0; i < kBStages; ++i) {
@@ -555,20 +633,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2 * kAccBufs; ++i) {
       mbar_init(smem_u32(&afull[i]), 1);
-      mbar_init(smem_u32(&aempty[i]), 8);
+      mbar_init(smem_u32(&aempty[i]), PAIR ? 16 : 8);  // the 8 epilogue warps (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_m)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
   if (warp == kWarpMma0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   if (tmem != 0) __trap();  // one CTA per SM owning all 512 columns: base is lane 0, column 0
@@ -597,19 +685,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           // in one request stream (a 2-D box per chunk fetches 128 B per row
           // and DRAM serves that pattern at ~4.6 TB/s; 256 B rows ~7 TB/s --
           // tools/stream_probe.cu)
-          tma_load_3d_hint(smem_u32(dst), &map_m, 0, pc[0], pt[0] * 128, fm, pol_m);
+          tma_load_3d_hint(smem_u32(dst), &map_m, 0, pc[0], pt[0] * kTileRows + row0, fm, pol_m);
         } else {
           for (int k = 0; k < npend; ++k) {
             if (!TRANS)
-              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * 128, fm, pol_m);
+              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pc[k] * kChunk, pt[k] * kTileRows + row0, fm,
+                               pol_m);
             else
-              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * 128, pc[k] * kChunk, fm, pol_m);
+              tma_load_2d_hint(smem_u32(dst + k * kMTileBytes), &map_m, pt[k] * kTileRows + row0, pc[k] * kChunk, fm,
+                               pol_m);
           }
         }
         g += kMGroup;
         npend = 0;
       };
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (int u = u0; u < total_units; u += ustep) {
         const Unit x = unit_of(p, u);
         for (int i = 0; i < x.n; ++i) {
           pt[npend] = x.tile, pc[npend] = unit_chunk(p, x, i);
@@ -627,15 +717,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       // one thread, all chunks in stream order, spin without sleeping
       const uint64_t pol_b = l2_policy_evict_last();
       int g = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (int u = u0; u < total_units; u += ustep) {
         const Unit x = unit_of(p, u);
         const int n_u = x.n;
         for (int i = 0; i < n_u; ++i) {
           const int gg = g + i, bs = gg % kBStages;
           mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
-          mbar_expect_tx(fb, b_bytes);
-          tma_load_2d_hint(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, x, i) * kChunk, 0, fb, pol_b);
+          if (PAIR) {
+            // this CTA's halves: rows [crank * rp/2, +rp/2) of F_hi and of F_lo,
+            // counted on the leader's barrier (which expects both CTAs' bytes)
+            const uint32_t fbc = cluster_addr(fb, 0);
+            const int hr = p.rp / 2;
+            if (crank == 0) mbar_expect_tx(fb, b_bytes);
+            const uint32_t dst = smem_u32(sm_b + bs * kBStageBytes);
+            tma_load_2d_pair(dst, &map_b, unit_chunk(p, x, i) * kChunk, (int)crank * hr, fbc, pol_b);
+            tma_load_2d_pair(dst + hr * 128, &map_b, unit_chunk(p, x, i) * kChunk, p.rp + (int)crank * hr, fbc, pol_b);
+          } else {
+            mbar_expect_tx(fb, b_bytes);
+            tma_load_2d_hint(smem_u32(sm_b + bs * kBStageBytes), &map_b, unit_chunk(p, x, i) * kChunk, 0, fb, pol_b);
+          }
           if (kBPrefetch > 0 && i + kBPrefetch < n_u) tma_prefetch_2d(&map_b, unit_chunk(p, x, i + kBPrefetch) * kChunk, 0);
           TCT(6, gg);
         }
@@ -646,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int w = lane;
     if (lane < 2) {
       int g = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (int u = u0; u < total_units; u += ustep) {
         const Unit x = unit_of(p, u);
         const int n_u = x.n;
         for (int i = own_first(g, w); i < n_u; i += 2) {
@@ -667,10 +768,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The whole warp runs the (warp-uniform) loop so every MMA operand stays in
     // the uniform datapath; one elected lane issues each tcgen05 instruction.
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
+    const bool issue = !PAIR || crank == 0;  // in a pair only the leader issues
     if (warp == kWarpMma0)
-      mma_role<0>(p, total_units, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
+      mma_role<0, PAIR>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
     else
-      mma_role<1>(p, total_units, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
+      mma_role<1, PAIR>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
   } else if (warp < kWarpEpi0) {
     // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
     // kConvGroups groups of 4 warps take alternate chunks (more chunks in
@@ -679,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;   // MMA row (= TMEM lane) owned by this thread
     int g = 0;                       // global chunk sequence number
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (int u = u0; u < total_units; u += ustep) {
       const int n_u = unit_of(p, u).n;
       for (int c = 0; c < n_u; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
@@ -744,7 +846,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&ready[slot]));
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(cluster_addr(smem_u32(&ready[slot]), 0));  // the leader issues the MMAs
+          else
+            mbar_arrive(smem_u32(&ready[slot]));
+        }
         if (q == 0) TCT(3, g);
       }
     }
@@ -761,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int wcnt[2] = {0, 0};  // windows drained per accumulator warp (all units)
     int g = 0;
     double sum[32];
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (int u = u0; u < total_units; u += ustep) {
       const Unit x = unit_of(p, u);
       const int tile = x.tile, split = x.split, n_u = x.n;
       const int c1 = own_count(g, n_u, 1);
@@ -790,12 +897,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&aempty[abar]));
+          if (lane == 0) {
+            if (PAIR)
+              mbar_arrive_cluster(cluster_addr(smem_u32(&aempty[abar]), 0));
+            else
+              mbar_arrive(smem_u32(&aempty[abar]));
+          }
           ++wcnt[w];
         }
       }
       g += n_u;
-      const int gi = tile * 128 + row;
+      const int gi = tile * kTileRows + row0 + row;
       if (live && gi < p.rows) {
         if (!TRANS) {
           double* out = p.part + (size_t)split * p.rows * p.r + (size_t)gi * p.r + cb;
@@ -813,10 +925,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // the peer's TMEM is read by the leader's MMAs until the end
+  else
+    __syncthreads();
   if (warp == kWarpMma0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 
@@ -1333,12 +1451,16 @@ class TcGemmImpl final : public TcGemm {
       TC_CK(cudaGetLastError());
       ++*launches;
     }
+    // CTA pairs (cta_group::2, 256-row tiles): r_pad in {32, 64} (N split in
+    // halves of >= 16 rows), an even SM count, enough tiles to fill the pairs
+    const bool pair = pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
+    const int slots = pair ? sms_ / 2 : sms_;  // persistent schedulers: pairs or CTAs
     tc::Params p{};
     p.rows = (int)rows;
     p.kdim = (int)K;
     p.r = (int)r;
     p.rp = rp;
-    p.tiles = (int)cdiv(rows, 128);
+    p.tiles = (int)cdiv(rows, pair ? 256 : 128);
     p.nchunks = (int)cdiv(K, tc::kChunk);
     p.wide = (!TRANS && tc::kMGroup == 2 && n % 64 == 0) ? 1 : 0;
     if (const char* e = getenv("MLB_TC_WIDE")) p.wide = p.wide && atoi(e);  // debug override
@@ -1364,8 +1486,8 @@ class TcGemmImpl final : public TcGemm {
         if (p.wide) cps += cps & 1;  // whole chunk pairs per unit
         const int spr = (int)cdiv(p.nchunks, cps);
         const double units = (double)p.tiles * spr;
-        const double rounds = std::ceil(units / sms_);
-        const double balance = units / (rounds * sms_);
+        const double rounds = std::ceil(units / slots);
+        const double balance = units / (rounds * slots);
         const double extra = spr > 1 ? (double)spr * rows * r * 16.0 / ((double)rows * K * 4.0) : 0.0;
         const double score = balance / (1.0 + extra);
         if (score > best + 1e-9) best = score, splits = sp;
@@ -1390,17 +1512,34 @@ class TcGemmImpl final : public TcGemm {
     const CUtensorMap mm = TRANS    ? make_map(M, n, m, 128, tc::kChunk, false)
                            : p.wide ? make_map3_rows(M, n, m)
                                     : make_map(M, n, m, tc::kChunk, 128, true);
-    const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, 2 * rp, true);
+    // factor slices: the whole [F_hi; F_lo] (2 rp rows) per chunk, or per CTA
+    // of a pair its rp / 2 rows of each half (two boxes)
+    const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, pair ? rp / 2 : 2 * rp, true);
     const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
-    auto kern = tc::k_tc_product<TRANS>;
-    if (!attr_set_[TRANS ? 1 : 0]) {
+    auto kern = pair ? tc::k_tc_product<TRANS, true> : tc::k_tc_product<TRANS, false>;
+    const int ak = (TRANS ? 1 : 0) + (pair ? 2 : 0);
+    if (!attr_set_[ak]) {
       TC_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set_[TRANS ? 1 : 0] = true;
+      attr_set_[ak] = true;
     }
     const int units = p.tiles * p.splits;
-    int grid = std::min(units, sms_);
+    int grid = std::min(units, slots);
     if (const char* e = getenv("MLB_TC_GRID")) grid = std::max(1, std::min(grid, atoi(e)));  // debug override
-    kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
+    if (pair) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * grid);
+      cfg.blockDim = dim3(tc::kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      TC_CK(cudaLaunchKernelEx(&cfg, kern, mm, mb, p));
+    } else {
+      kern<<<grid, tc::kThreads, smem, s>>>(mm, mb, p);
+    }
     TC_CK(cudaGetLastError());
 #if MLB_TC_TRACE
     if (const char* path = getenv("MLB_TC_TRACE_OUT")) {
@@ -1439,7 +1578,12 @@ class TcGemmImpl final : public TcGemm {
   size_t split_bytes_ = 0;
   void* part_ = nullptr;
   size_t part_bytes_ = 0;
-  bool attr_set_[2] = {false, false};
+  bool attr_set_[4] = {false, false, false, false};
+  // CTA-pair products (MLB_TC_PAIR=1 to enable; see k_tc_product)
+  bool pair_ = [] {
+    const char* e = getenv("MLB_TC_PAIR");
+    return e != nullptr && atoi(e) != 0;
+  }();
   void* rv_ = nullptr;  // residual operands: V and W^T split into [hi | lo] rows
   void* rw_ = nullptr;
   size_t rv_bytes_ = 0, rw_bytes_ = 0;
