@@ -372,9 +372,15 @@ struct Engine::Impl {
     if (r > 128) throw std::invalid_argument("anls on the device supports rank <= 128");
     const size_t gbytes = (size_t)r * r * 8, wb = nnls_warp_bytes(r);
     if (gbytes + wb > kSmemMax) throw std::invalid_argument("anls: rank too large for shared memory");
-    const int nw = (int)std::min<size_t>(8, (kSmemMax - gbytes) / wb);
+    // warps per block: as many as the SM's shared memory holds (the Gram is
+    // staged once per block, so one wide block per SM beats several narrow
+    // ones; 8 warps per block left large-rank problems at 8 warps per SM and
+    // latency-bound), but no more than spreads the problems over every SM
+    const size_t nw_max = std::max<size_t>(1, std::min<size_t>(32, (kSmemMax - gbytes) / wb));
+    const int nw = (int)std::min(nw_max, std::max<size_t>(1, ceil_div(nprob, (size_t)sm_count)));
     const size_t smem = gbytes + nw * wb;
-    const size_t blocks = std::min<size_t>(ceil_div(nprob, nw), (size_t)sm_count * 8);
+    const size_t per_sm = std::max<size_t>(1, std::min<size_t>(kSmemMax / smem, 64 / nw));
+    const size_t blocks = std::min<size_t>(ceil_div(nprob, nw), (size_t)sm_count * per_sm);
     int* cnt = reserve_counts(nprob);
     if (exact())
       launch(k_nnls_batch<T, true>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi, xe,

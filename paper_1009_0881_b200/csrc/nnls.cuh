@@ -37,7 +37,12 @@ __host__ __device__ inline size_t nnls_warp_bytes(int r) {
 }
 
 // Cholesky of the packed lower p x p matrix in place; false on a non-positive
-// or non-finite pivot (solvers.cpp:26-37).
+// or non-finite pivot (solvers.cpp:26-37).  !EXACT: the column is scaled by
+// one reciprocal of the pivot (an fp64 division is a ~100-cycle dependent
+// MUFU + Newton sequence; ncu put the divisions among the hottest spots of
+// the batched NNLS), and the diagonal holds 1 / L[k][k] for the
+// substitutions, which then multiply instead of divide.
+template <bool EXACT>
 __device__ inline bool warp_cholesky(double* L, int p, int lane) {
   for (int k = 0; k < p; ++k) {
     const size_t rk = (size_t)k * (k + 1) / 2;
@@ -48,14 +53,15 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
       return false;
     }
     const double lkk = sqrt(d);
+    const double ilkk = EXACT ? 0.0 : 1.0 / lkk;
     for (int i = k + 1 + lane; i < p; i += 32) {
       const size_t ri = (size_t)i * (i + 1) / 2;
       double s = L[ri + k];
       for (int q = 0; q < k; ++q) s = msub(s, L[ri + q], L[rk + q]);
-      L[ri + k] = s / lkk;
+      L[ri + k] = EXACT ? s / lkk : s * ilkk;
     }
     __syncwarp();
-    if (lane == 0) L[rk + k] = lkk;
+    if (lane == 0) L[rk + k] = EXACT ? lkk : ilkk;
     __syncwarp();
   }
   return true;
@@ -66,7 +72,7 @@ __device__ inline void warp_substitute(const double* L, double* b, int p, int la
   // forward: L y = b (solvers.cpp:39-43), right-looking, same per-element order
   for (int q = 0; q < p; ++q) {
     const size_t rq = (size_t)q * (q + 1) / 2;
-    const double bq = b[q] / L[rq + q];
+    const double bq = EXACT ? b[q] / L[rq + q] : b[q] * L[rq + q];  // !EXACT: diagonal holds 1 / L[q][q]
     __syncwarp();
     if (lane == 0) b[q] = bq;
     for (int i = q + 1 + lane; i < p; i += 32) b[i] = msub(b[i], L[(size_t)i * (i + 1) / 2 + q], bq);
@@ -84,7 +90,7 @@ __device__ inline void warp_substitute(const double* L, double* b, int p, int la
     __syncwarp();
   } else {
     for (int q = p - 1; q >= 0; --q) {
-      const double bq = b[q] / L[(size_t)q * (q + 1) / 2 + q];
+      const double bq = b[q] * L[(size_t)q * (q + 1) / 2 + q];
       __syncwarp();
       if (lane == 0) b[q] = bq;
       const size_t rq = (size_t)q * (q + 1) / 2;
@@ -115,7 +121,7 @@ __device__ inline bool warp_solve_passive(const double* Gs, int r, const NnlsWar
     }
     for (int a = lane; a < p; a += 32) wm.b[a] = wm.b0[a];
     __syncwarp();
-    if (warp_cholesky(wm.L, p, lane)) {
+    if (warp_cholesky<EXACT>(wm.L, p, lane)) {
       warp_substitute<EXACT>(wm.L, wm.b, p, lane);
       return true;
     }
