@@ -353,12 +353,17 @@ def run_e2e(P, host, local, gemm, iters, norm, world=1, rank=0, nccl_id=None, co
             "iters_per_call": steps, "wall_s": wall, "final_rel_error": float(tr.error[-1]) / norm}
 
 
+# solver kinds BASELINE.json names per config (configs[0..3])
+SMALL_KINDS = {0: ("hals",), 1: ("mu", "hals"), 2: ("anls", "hals"), 3: ("hals", "mu", "anls")}
+
+
 def small_configs(P, local, with_cpu):
     """BASELINE configs 0-3 (L2-resident, launch/latency bound):
-    HALS single-level sweeps/s on the device (fp32 storage, SIMT fp64-accumulate
-    products, data generated on the device, trace_every=0, 100 sweeps), next to
-    the reference's own hals_step (oracle/_ref, fp64, OpenMP on all host cores)
-    timed on the same host for 3 steps."""
+    single-level sweeps/s on the device for every solver kind BASELINE.json
+    names for the config (fp32 storage, SIMT fp64-accumulate products, data
+    generated on the device, trace_every=0; HALS/MU 100 sweeps, ANLS 20),
+    next to the reference's own step (oracle/_ref, fp64, OpenMP on all host
+    cores) from the same random init, median of 2 steps."""
     out = {}
     ref = None
     if with_cpu:
@@ -367,29 +372,34 @@ def small_configs(P, local, with_cpu):
             ref, restated = oracle.Reference(), oracle.Restated()
     for cfg in (0, 1, 2, 3):
         c = P.GEN_CONFIGS[cfg]
-        with P.Session(device=local, dtype=P.F32) as s:
-            s.generate(cfg, seed=0)
-            s.run_configuration(1, "hals", "none", c["r"], 0, 5.0, 0)  # warm-up (graphs, buffers)
-            s.sync()
-            t0 = time.perf_counter()
-            tr = s.run_configuration(1, "hals", "none", c["r"], 0, 100.0, 0)
-            s.sync()
-            wall = time.perf_counter() - t0
-        steps = int(tr.phase_steps.sum())
-        e = {"shape": f"{c['h']}x{c['w']} (m={c['h'] * c['w']}) x n={c['n']}, r={c['r']}",
-             "gpu_it_s": steps / wall, "gpu_ms_per_step": wall / steps * 1e3}
-        if ref is not None:
-            M = oracle.generate_config(cfg, restated=restated)
-            V, W = ref.random_init(M.shape[0], M.shape[1], c["r"], 0)
-            ts = []
-            for _ in range(3):
+        M = oracle.generate_config(cfg, restated=restated) if ref is not None else None
+        for kind in SMALL_KINDS[cfg]:
+            work = 20.0 if kind == "anls" else 100.0
+            with P.Session(device=local, dtype=P.F32) as s:
+                s.generate(cfg, seed=0)
+                s.run_configuration(1, kind, "none", c["r"], 0, 5.0, 0)  # warm-up (graphs, buffers)
+                s.sync()
                 t0 = time.perf_counter()
-                V, W, _ = ref.hals_step(M, V, W)
-                ts.append(time.perf_counter() - t0)
-            e["cpu_ref_ms_per_step"] = float(np.median(ts)) * 1e3
-            e["cpu_cores"] = os.cpu_count() or 1
-            e["speedup"] = e["cpu_ref_ms_per_step"] / e["gpu_ms_per_step"]
-        out[f"config{cfg}"] = e
+                tr = s.run_configuration(1, kind, "none", c["r"], 0, work, 0)
+                s.sync()
+                wall = time.perf_counter() - t0
+            steps = int(tr.phase_steps.sum())
+            e = {"shape": f"{c['h']}x{c['w']} (m={c['h'] * c['w']}) x n={c['n']}, r={c['r']}", "kind": kind,
+                 "sweeps": steps, "gpu_it_s": steps / wall, "gpu_ms_per_step": wall / steps * 1e3}
+            if ref is not None:
+                V, W = ref.random_init(M.shape[0], M.shape[1], c["r"], 0)
+                step = {"mu": ref.mu_step, "hals": ref.hals_step, "anls": ref.anls_step}[kind]
+                ts = []
+                for _ in range(2):
+                    t1 = time.perf_counter()
+                    res = step(M, V, W)
+                    ts.append(time.perf_counter() - t1)
+                    V, W = res[0], res[1]
+                e["cpu_ref_ms_per_step"] = float(np.median(ts)) * 1e3
+                e["cpu_ref_note"] = "first two steps from random init (ANLS: cold active sets, slowest sweeps)"
+                e["cpu_cores"] = os.cpu_count() or 1
+                e["speedup"] = e["cpu_ref_ms_per_step"] / e["gpu_ms_per_step"]
+            out[f"config{cfg}_{kind}"] = e
     return out
 
 
