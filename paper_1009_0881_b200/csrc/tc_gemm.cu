@@ -53,6 +53,14 @@
 namespace mlb {
 namespace tc {
 
+// nanosleep (ns) between failed barrier polls of the TMA producers and of
+// the converters (0: spin); spinning warps take issue slots and power
+#ifndef MLB_TC_PSLEEP
+#define MLB_TC_PSLEEP 0
+#endif
+#ifndef MLB_TC_CSLEEP
+#define MLB_TC_CSLEEP 0
+#endif
 #ifndef MLB_TC_MSTAGES
 #define MLB_TC_MSTAGES 8
 #endif
@@ -675,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_m = l2_policy_evict_first();
       auto issue_group = [&]() {
         const int pg = g / kMGroup, ps = pg % kMGroups;
-        mbar_wait(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMGroups) & 1u) ^ 1u);
+        mbar_wait<MLB_TC_PSLEEP>(smem_u32(&mempty[ps]), ((uint32_t)(pg / kMGroups) & 1u) ^ 1u);
         const uint32_t fm = smem_u32(&mfull[ps]);
         mbar_expect_tx(fm, npend * kMTileBytes);
         for (int k = 0; k < npend; ++k) TCT(0, g + k);
@@ -722,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_u = x.n;
         for (int i = 0; i < n_u; ++i) {
           const int gg = g + i, bs = gg % kBStages;
-          mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
+          mbar_wait<MLB_TC_PSLEEP>(smem_u32(&bempty[bs]), ((uint32_t)(gg / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           if (PAIR) {
             // this CTA's halves: rows [crank * rp/2, +rp/2) of F_hi and of F_lo,
@@ -787,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (g % kConvGroups != grp) continue;
         const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots;
         const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
-        mbar_wait(smem_u32(&mfull[ps]), mph);
+        mbar_wait<MLB_TC_CSLEEP>(smem_u32(&mfull[ps]), mph);
         if (q == 0) TCT(1, g);
         // the thread's 32 values of this chunk (its MMA row / TMEM lane)
         float x[32];
@@ -837,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&mempty[ps]));  // slice consumed: TMA may refill the group
-        mbar_wait(smem_u32(&sdone[slot]), sphase ^ 1);
+        mbar_wait<MLB_TC_CSLEEP>(smem_u32(&sdone[slot]), sphase ^ 1);
         if (q == 0) TCT(2, g);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStgCol0 + slot * 64;
