@@ -321,8 +321,8 @@ struct Engine::Impl {
     const size_t smem = (r * r + r * bd) * 8;
     const dim3 gv((unsigned)ceil_div(L.m, bd));
     if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
-      launch(k_hals_v_warp<T>, dim3((unsigned)ceil_div(L.m, 8)), dim3(256), r * r * 8, (const double*)A(),
-             (const double*)B(), V, L.m, (int)r, deg);
+      launch(k_hals_v_warp<T>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
+             (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
     } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
       hals_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, deg, s);
       ++e->launches_;
@@ -342,8 +342,9 @@ struct Engine::Impl {
     T* Wp = W.as<T>();
     const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
     if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
-      launch(k_hals_w_warp<T>, dim3((unsigned)ceil_div(e->n_loc_, 8)), dim3(256), r * r * 8,
-             (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_, (int)r, deg);
+      launch(k_hals_w_warp<T>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
+             dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+             e->n_loc_, (int)r, deg);
     } else if (kind == kHals && hals_reg_supported(r)) {
       hals_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
       ++e->launches_;

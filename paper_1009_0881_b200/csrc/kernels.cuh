@@ -276,37 +276,44 @@ __device__ __forceinline__ double warp_allsum(double v) {
 }
 
 // rows of V (m x r): x_k <- max(0, (A_ik + x_k G_kk - sum_l x_l G_lk) / G_kk)
+// One warp per row (lanes hold x_l and A_il for l = lane, lane + 32), the
+// blocks persistent over rows so the Gram and its diagonal reciprocals are
+// staged once per block; the row of A is loaded before the sequential k loop
+// (a dependent global load per k was the sweep's critical path).
+// Non-exact mode only (tree-reduced dots, reciprocal of G_kk).
 template <typename T>
 __global__ void __launch_bounds__(256) k_hals_v_warp(const double* __restrict__ A, const double* __restrict__ G,
                                                      T* __restrict__ V, size_t m, int r, int* __restrict__ degenerate) {
-  extern __shared__ double Gs[];
+  extern __shared__ double Gs[];  // r x r, then r reciprocals of the diagonal
+  double* Ginv = Gs + (size_t)r * r;
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = G[e];
+  for (int k = threadIdx.x; k < r; k += blockDim.x) Ginv[k] = G[(size_t)k * r + k] > 0.0 ? 1.0 / G[(size_t)k * r + k] : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const bool act = i < m;
-  double x0 = (act && lane < r) ? (double)V[i * r + lane] : 0.0;
-  double x1 = (act && lane + 32 < r) ? (double)V[i * r + lane + 32] : 0.0;
-  for (int k = 0; k < r; ++k) {
-    const double gkk = Gs[k * r + k];
-    if (gkk <= 0.0) {
-      if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(degenerate, 1);
-      continue;
+  if (degenerate && blockIdx.x == 0 && threadIdx.x == 0)  // hals_step's count: once per skipped k
+    for (int k = 0; k < r; ++k)
+      if (Gs[(size_t)k * r + k] <= 0.0) atomicAdd(degenerate, 1);
+  for (size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += (size_t)gridDim.x * 8) {
+    double x0 = lane < r ? (double)V[i * r + lane] : 0.0;
+    double x1 = lane + 32 < r ? (double)V[i * r + lane + 32] : 0.0;
+    const double a0 = lane < r ? A[i * r + lane] : 0.0;
+    const double a1 = lane + 32 < r ? A[i * r + lane + 32] : 0.0;
+    for (int k = 0; k < r; ++k) {
+      const double gkk = Gs[k * r + k];
+      if (gkk <= 0.0) continue;
+      double part = 0.0;
+      if (lane < r) part = x0 * Gs[lane * r + k];
+      if (lane + 32 < r) part = fma(x1, Gs[(lane + 32) * r + k], part);
+      const double dot = warp_allsum(part);
+      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+      const double a = __shfl_sync(0xffffffffu, k < 32 ? a0 : a1, k & 31);
+      const double q = (a + xk * gkk - dot) * Ginv[k];
+      const double nk = q > 0.0 ? q : 0.0;
+      if (lane == (k & 31)) {
+        if (k < 32) x0 = nk;
+        else x1 = nk;
+      }
     }
-    double part = 0.0;
-    if (lane < r) part = x0 * Gs[lane * r + k];
-    if (lane + 32 < r) part = fma(x1, Gs[(lane + 32) * r + k], part);
-    const double dot = warp_allsum(part);
-    const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-    const double a = act ? A[i * r + k] : 0.0;
-    const double q = (a + xk * gkk - dot) / gkk;
-    const double nk = q > 0.0 ? q : 0.0;
-    if (lane == (k & 31)) {
-      if (k < 32) x0 = nk;
-      else x1 = nk;
-    }
-  }
-  if (act) {
     if (lane < r) V[i * r + lane] = to_t<T>(x0);
     if (lane + 32 < r) V[i * r + lane + 32] = to_t<T>(x1);
   }
@@ -316,34 +323,36 @@ __global__ void __launch_bounds__(256) k_hals_v_warp(const double* __restrict__ 
 template <typename T>
 __global__ void __launch_bounds__(256) k_hals_w_warp(const double* __restrict__ Cm, const double* __restrict__ D,
                                                      T* __restrict__ W, size_t n, int r, int* __restrict__ degenerate) {
-  extern __shared__ double Ds[];
+  extern __shared__ double Ds[];  // r x r, then r reciprocals of the diagonal
+  double* Dinv = Ds + (size_t)r * r;
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) Ds[e] = D[e];
+  for (int k = threadIdx.x; k < r; k += blockDim.x) Dinv[k] = D[(size_t)k * r + k] > 0.0 ? 1.0 / D[(size_t)k * r + k] : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const size_t j = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const bool act = j < n;
-  double x0 = (act && lane < r) ? (double)W[(size_t)lane * n + j] : 0.0;
-  double x1 = (act && lane + 32 < r) ? (double)W[(size_t)(lane + 32) * n + j] : 0.0;
-  for (int k = 0; k < r; ++k) {
-    const double dkk = Ds[k * r + k];
-    if (dkk <= 0.0) {
-      if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(degenerate, 1);
-      continue;
+  if (degenerate && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int k = 0; k < r; ++k)
+      if (Ds[(size_t)k * r + k] <= 0.0) atomicAdd(degenerate, 1);
+  for (size_t j = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < n; j += (size_t)gridDim.x * 8) {
+    double x0 = lane < r ? (double)W[(size_t)lane * n + j] : 0.0;
+    double x1 = lane + 32 < r ? (double)W[(size_t)(lane + 32) * n + j] : 0.0;
+    const double c0 = lane < r ? Cm[(size_t)lane * n + j] : 0.0;
+    const double c1 = lane + 32 < r ? Cm[(size_t)(lane + 32) * n + j] : 0.0;
+    for (int k = 0; k < r; ++k) {
+      const double dkk = Ds[k * r + k];
+      if (dkk <= 0.0) continue;
+      double part = 0.0;
+      if (lane < r) part = Ds[k * r + lane] * x0;
+      if (lane + 32 < r) part = fma(Ds[k * r + lane + 32], x1, part);
+      const double dot = warp_allsum(part);
+      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+      const double c = __shfl_sync(0xffffffffu, k < 32 ? c0 : c1, k & 31);
+      const double q = (c + dkk * xk - dot) * Dinv[k];
+      const double nk = q > 0.0 ? q : 0.0;
+      if (lane == (k & 31)) {
+        if (k < 32) x0 = nk;
+        else x1 = nk;
+      }
     }
-    double part = 0.0;
-    if (lane < r) part = Ds[k * r + lane] * x0;
-    if (lane + 32 < r) part = fma(Ds[k * r + lane + 32], x1, part);
-    const double dot = warp_allsum(part);
-    const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-    const double c = act ? Cm[(size_t)k * n + j] : 0.0;
-    const double q = (c + dkk * xk - dot) / dkk;
-    const double nk = q > 0.0 ? q : 0.0;
-    if (lane == (k & 31)) {
-      if (k < 32) x0 = nk;
-      else x1 = nk;
-    }
-  }
-  if (act) {
     if (lane < r) W[(size_t)lane * n + j] = to_t<T>(x0);
     if (lane + 32 < r) W[(size_t)(lane + 32) * n + j] = to_t<T>(x1);
   }
