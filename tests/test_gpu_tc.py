@@ -111,3 +111,22 @@ def test_tc_residual_error(P, gpu, m, n, r):
         assert s.tc_active and not s.gram_error
         e_tc = s.error()
     assert abs(e_tc - ref) / ref < 1e-7, (e_tc, ref)
+
+
+@pytest.mark.parametrize("m,n,r", [(2048, 4096, 64), (4096, 2304, 32), (3000, 2600, 64)])
+def test_tc_products_cta_pairs(P, gpu, monkeypatch, m, n, r):
+    """The opt-in CTA-pair products (cta_group::2, 256-row tiles, MLB_TC_PAIR=1,
+    read when a session's tensor path is created) agree with fp64 like the
+    single-CTA kernel, including ragged 256-row tiles."""
+    monkeypatch.setenv("MLB_TC_PAIR", "1")
+    rng = np.random.default_rng(m + n + r)
+    M = rng.random((m, n)).astype(np.float32)
+    V = rng.random((m, r)).astype(np.float32)
+    W = (rng.random((r, n)) * 2).astype(np.float32)
+    M64, V64, W64 = M.astype(np.float64), V.astype(np.float64), W.astype(np.float64)
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V64, W64)
+        A, C = s.products()
+    ea, ec = relnorm(A, M64 @ W64.T), relnorm(C, V64.T @ M64)
+    assert ea < TOL and ec < TOL, (ea, ec)
