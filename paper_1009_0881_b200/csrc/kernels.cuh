@@ -276,11 +276,73 @@ __device__ __forceinline__ double warp_allsum(double v) {
 }
 
 // rows of V (m x r): x_k <- max(0, (A_ik + x_k G_kk - sum_l x_l G_lk) / G_kk)
-// One warp per row (lanes hold x_l and A_il for l = lane, lane + 32), the
-// blocks persistent over rows so the Gram and its diagonal reciprocals are
-// staged once per block; the row of A is loaded before the sequential k loop
-// (a dependent global load per k was the sweep's critical path).
-// Non-exact mode only (tree-reduced dots, reciprocal of G_kk).
+// One warp per row, or per pair of rows interleaved when there are more rows
+// than resident warps: each sequential k step is a shuffle-reduction chain
+// (~200 cycles of latency), so a second independent row fills the gaps.  Lanes hold x_l and A_il for l = lane, lane + 32;
+// the blocks are persistent over row pairs so the Gram and its diagonal
+// reciprocals are staged once per block, and the rows of A are loaded before
+// the k loop.  Non-exact mode only (tree-reduced dots, reciprocal of G_kk).
+// The W half is the same update on columns of W with C and D (CT = true:
+// element (k, j) at k * n + j).
+template <typename T, bool CT, bool TWO>
+__device__ __forceinline__ void hals_warp_rows(const double* __restrict__ A, const double* Gs, const double* Ginv,
+                                               T* __restrict__ V, size_t m, int r, size_t i, size_t i2) {
+  const int lane = threadIdx.x & 31;
+  auto at = [&](size_t row, int k) -> size_t { return CT ? (size_t)k * m + row : row * (size_t)r + k; };
+  double x0 = lane < r ? (double)V[at(i, lane)] : 0.0;
+  double x1 = lane + 32 < r ? (double)V[at(i, lane + 32)] : 0.0;
+  double y0 = TWO && lane < r ? (double)V[at(i2, lane)] : 0.0;
+  double y1 = TWO && lane + 32 < r ? (double)V[at(i2, lane + 32)] : 0.0;
+  const double a0 = lane < r ? A[at(i, lane)] : 0.0;
+  const double a1 = lane + 32 < r ? A[at(i, lane + 32)] : 0.0;
+  const double b0 = TWO && lane < r ? A[at(i2, lane)] : 0.0;
+  const double b1 = TWO && lane + 32 < r ? A[at(i2, lane + 32)] : 0.0;
+  for (int k = 0; k < r; ++k) {
+    const double gkk = Gs[k * r + k];
+    if (gkk <= 0.0) continue;
+    // column k of G for rows of V, row k of D for columns of W
+    const double g0 = lane < r ? (CT ? Gs[k * r + lane] : Gs[lane * r + k]) : 0.0;
+    const double g1 = lane + 32 < r ? (CT ? Gs[k * r + lane + 32] : Gs[(lane + 32) * r + k]) : 0.0;
+    double pa = fma(x1, g1, x0 * g0), pb = TWO ? fma(y1, g1, y0 * g0) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pa += __shfl_xor_sync(0xffffffffu, pa, o);
+      if (TWO) pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    }
+    const int src = k & 31;
+    const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, src);
+    const double ak = __shfl_sync(0xffffffffu, k < 32 ? a0 : a1, src);
+    const double qa = (ak + xk * gkk - pa) * Ginv[k];
+    double qb = 0.0;
+    if (TWO) {
+      const double yk = __shfl_sync(0xffffffffu, k < 32 ? y0 : y1, src);
+      const double bk = __shfl_sync(0xffffffffu, k < 32 ? b0 : b1, src);
+      qb = (bk + yk * gkk - pb) * Ginv[k];
+    }
+    if (lane == src) {
+      if (k < 32) x0 = qa > 0.0 ? qa : 0.0, y0 = qb > 0.0 ? qb : 0.0;
+      else x1 = qa > 0.0 ? qa : 0.0, y1 = qb > 0.0 ? qb : 0.0;
+    }
+  }
+  if (lane < r) V[at(i, lane)] = to_t<T>(x0);
+  if (lane + 32 < r) V[at(i, lane + 32)] = to_t<T>(x1);
+  if (TWO && lane < r) V[at(i2, lane)] = to_t<T>(y0);
+  if (TWO && lane + 32 < r) V[at(i2, lane + 32)] = to_t<T>(y1);
+}
+
+// rows i (and i + nw when there are more rows than warps) per warp
+template <typename T, bool CT>
+__device__ __forceinline__ void hals_warp_pairs(const double* __restrict__ A, const double* Gs, const double* Ginv,
+                                                T* __restrict__ V, size_t m, int r) {
+  const size_t nw = (size_t)gridDim.x * 8;
+  for (size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += 2 * nw) {
+    if (i + nw < m)
+      hals_warp_rows<T, CT, true>(A, Gs, Ginv, V, m, r, i, i + nw);
+    else
+      hals_warp_rows<T, CT, false>(A, Gs, Ginv, V, m, r, i, i);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_hals_v_warp(const double* __restrict__ A, const double* __restrict__ G,
                                                      T* __restrict__ V, size_t m, int r, int* __restrict__ degenerate) {
@@ -289,34 +351,10 @@ __global__ void __launch_bounds__(256) k_hals_v_warp(const double* __restrict__ 
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = G[e];
   for (int k = threadIdx.x; k < r; k += blockDim.x) Ginv[k] = G[(size_t)k * r + k] > 0.0 ? 1.0 / G[(size_t)k * r + k] : 0.0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   if (degenerate && blockIdx.x == 0 && threadIdx.x == 0)  // hals_step's count: once per skipped k
     for (int k = 0; k < r; ++k)
       if (Gs[(size_t)k * r + k] <= 0.0) atomicAdd(degenerate, 1);
-  for (size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += (size_t)gridDim.x * 8) {
-    double x0 = lane < r ? (double)V[i * r + lane] : 0.0;
-    double x1 = lane + 32 < r ? (double)V[i * r + lane + 32] : 0.0;
-    const double a0 = lane < r ? A[i * r + lane] : 0.0;
-    const double a1 = lane + 32 < r ? A[i * r + lane + 32] : 0.0;
-    for (int k = 0; k < r; ++k) {
-      const double gkk = Gs[k * r + k];
-      if (gkk <= 0.0) continue;
-      double part = 0.0;
-      if (lane < r) part = x0 * Gs[lane * r + k];
-      if (lane + 32 < r) part = fma(x1, Gs[(lane + 32) * r + k], part);
-      const double dot = warp_allsum(part);
-      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-      const double a = __shfl_sync(0xffffffffu, k < 32 ? a0 : a1, k & 31);
-      const double q = (a + xk * gkk - dot) * Ginv[k];
-      const double nk = q > 0.0 ? q : 0.0;
-      if (lane == (k & 31)) {
-        if (k < 32) x0 = nk;
-        else x1 = nk;
-      }
-    }
-    if (lane < r) V[i * r + lane] = to_t<T>(x0);
-    if (lane + 32 < r) V[i * r + lane + 32] = to_t<T>(x1);
-  }
+  hals_warp_pairs<T, false>(A, Gs, Ginv, V, m, r);
 }
 
 // columns of W (r x n): the same update with C (r x n) and D (r x r)
@@ -328,34 +366,10 @@ __global__ void __launch_bounds__(256) k_hals_w_warp(const double* __restrict__ 
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) Ds[e] = D[e];
   for (int k = threadIdx.x; k < r; k += blockDim.x) Dinv[k] = D[(size_t)k * r + k] > 0.0 ? 1.0 / D[(size_t)k * r + k] : 0.0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   if (degenerate && blockIdx.x == 0 && threadIdx.x == 0)
     for (int k = 0; k < r; ++k)
       if (Ds[(size_t)k * r + k] <= 0.0) atomicAdd(degenerate, 1);
-  for (size_t j = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < n; j += (size_t)gridDim.x * 8) {
-    double x0 = lane < r ? (double)W[(size_t)lane * n + j] : 0.0;
-    double x1 = lane + 32 < r ? (double)W[(size_t)(lane + 32) * n + j] : 0.0;
-    const double c0 = lane < r ? Cm[(size_t)lane * n + j] : 0.0;
-    const double c1 = lane + 32 < r ? Cm[(size_t)(lane + 32) * n + j] : 0.0;
-    for (int k = 0; k < r; ++k) {
-      const double dkk = Ds[k * r + k];
-      if (dkk <= 0.0) continue;
-      double part = 0.0;
-      if (lane < r) part = Ds[k * r + lane] * x0;
-      if (lane + 32 < r) part = fma(Ds[k * r + lane + 32], x1, part);
-      const double dot = warp_allsum(part);
-      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-      const double c = __shfl_sync(0xffffffffu, k < 32 ? c0 : c1, k & 31);
-      const double q = (c + dkk * xk - dot) * Dinv[k];
-      const double nk = q > 0.0 ? q : 0.0;
-      if (lane == (k & 31)) {
-        if (k < 32) x0 = nk;
-        else x1 = nk;
-      }
-    }
-    if (lane < r) W[(size_t)lane * n + j] = to_t<T>(x0);
-    if (lane + 32 < r) W[(size_t)(lane + 32) * n + j] = to_t<T>(x1);
-  }
+  hals_warp_pairs<T, true>(Cm, Ds, Dinv, W, n, r);
 }
 
 // ---------------------------------------------------------------------------
