@@ -290,8 +290,12 @@ struct Engine::Impl {
   // (config 3's W half: n = 165).  With many rows the thread-per-row kernels
   // win (measured: config 3's V half 0.58 -> 0.82 ms/step and config 4's step
   // +2 ms with warps).  Exact mode keeps the reference's sequential order.
+  // (re-measured with the persistent two-row warp kernels: config 3 0.585 ->
+  // 0.713 ms/step, config 4 +1.3 ms/step; MLNMF_WARP_SWEEPS=1 forces them)
+  static constexpr size_t kWarpSweepMax = 16384;
   bool warp_sweeps(size_t r, size_t count) const {
-    return !exact() && r <= 64 && count < 16384 && std::getenv("MLNMF_THREAD_SWEEPS") == nullptr;
+    if (exact() || r > 64 || std::getenv("MLNMF_THREAD_SWEEPS") != nullptr) return false;
+    return count < kWarpSweepMax || std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
   }
   int sweep_block(int r) const {
     for (int bd : {128, 64, 32})
