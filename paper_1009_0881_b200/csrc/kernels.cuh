@@ -51,12 +51,14 @@ __host__ __device__ __forceinline__ double sm64_uniform(uint64_t seed, uint64_t 
 }
 
 // ---------------------------------------------------------------------------
-// Tall-skinny GEMMs.  Tiles 64 x 64 outputs, K step 32, 256 threads, 4x4
-// outputs per thread; fp64 accumulators; operand tiles staged in shared
-// memory as fp64.
+// Tall-skinny GEMMs.  Tiles 64 x 64 outputs, K step 16 in two stages, 256
+// threads, 4x4 outputs per thread; fp64 accumulators; operand tiles staged
+// in shared memory as fp64.  Each output accumulates over p in ascending
+// order within its K chunk (the EXACT variants follow the reference order).
 // ---------------------------------------------------------------------------
 constexpr int GT = 64;   // output tile edge
-constexpr int GK = 32;   // K step
+constexpr int GK = 32;   // K granule of the split-K chunking (host side)
+constexpr int GKS = 16;  // K step of the two-stage kernels (2 x 2 x 16 x 65 doubles of static smem)
 
 // part[z][i][k] = sum_{p in split z} X[i][p] * Y[k][p]
 //   X: rows x K (row-major, ld = K), Y: ny x K (row-major, ld = K).
@@ -65,8 +67,12 @@ template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const T* __restrict__ Y,
                                                   size_t rows, size_t ny, size_t K, size_t kchunk,
                                                   double* __restrict__ part) {
-  __shared__ double Xs[GK][GT + 1];
-  __shared__ double Ys[GK][GT + 1];
+  // two stages: the next K step's operands are loaded into registers while
+  // the current one is multiplied (one barrier per step; the single-stage
+  // version exposed an L2 round trip per 32-wide K step)
+  __shared__ double Xs[2][GKS][GT + 1];
+  __shared__ double Ys[2][GKS][GT + 1];
+  constexpr int PQ = (GT * GKS) / 256;  // operand elements per thread and stage
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const size_t i0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
   const size_t kb = (size_t)blockIdx.z * kchunk;
@@ -76,29 +82,39 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (size_t p0 = kb; p0 < ke; p0 += GK) {
+  double rx[PQ], ry[PQ];
+  auto fetch = [&](size_t p0) {
 #pragma unroll
-    for (int q = 0; q < (GT * GK) / 256; ++q) {
-      const int e = tid + 256 * q, rr = e / GK, pp = e % GK;
-      const size_t p = p0 + pp;
-      const size_t gi = i0 + rr, gk = k0 + rr;
-      Xs[pp][rr] = (gi < rows && p < ke) ? (double)X[gi * K + p] : 0.0;
-      Ys[pp][rr] = (gk < ny && p < ke) ? (double)Y[gk * K + p] : 0.0;
+    for (int q = 0; q < PQ; ++q) {
+      const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
+      const size_t p = p0 + pp, gi = i0 + rr, gk = k0 + rr;
+      rx[q] = (gi < rows && p < ke) ? (double)X[gi * K + p] : 0.0;
+      ry[q] = (gk < ny && p < ke) ? (double)Y[gk * K + p] : 0.0;
+    }
+  };
+  fetch(kb);
+  int buf = 0;
+  for (size_t p0 = kb; p0 < ke; p0 += GKS, buf ^= 1) {
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) {
+      const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
+      Xs[buf][pp][rr] = rx[q];
+      Ys[buf][pp][rr] = ry[q];
     }
     __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < GK; ++kk) {
+    if (p0 + GKS < ke) fetch(p0 + GKS);
+#pragma unroll
+    for (int kk = 0; kk < GKS; ++kk) {
       double xa[4], yb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) xa[a] = Xs[kk][ty + 16 * a];
+      for (int a = 0; a < 4; ++a) xa[a] = Xs[buf][kk][ty + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) yb[b] = Ys[kk][tx + 16 * b];
+      for (int b = 0; b < 4; ++b) yb[b] = Ys[buf][kk][tx + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], xa[a], yb[b]);
     }
-    __syncthreads();
   }
   double* out = part + (size_t)blockIdx.z * rows * ny;
 #pragma unroll
@@ -120,8 +136,9 @@ template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const T* __restrict__ X,
                                                   size_t K, size_t r, size_t ncols, size_t kchunk,
                                                   double* __restrict__ part) {
-  __shared__ double Xs[GK][GT + 1];
-  __shared__ double Vs[GK][GT + 1];
+  __shared__ double Xs[2][GKS][GT + 1];  // two stages, as k_gemm_abt
+  __shared__ double Vs[2][GKS][GT + 1];
+  constexpr int PQ = (GT * GKS) / 256;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const size_t j0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
   const size_t ib = (size_t)blockIdx.z * kchunk;
@@ -131,29 +148,39 @@ __global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (size_t p0 = ib; p0 < ie; p0 += GK) {
+  double rx[PQ], rv[PQ];
+  auto fetch = [&](size_t p0) {
 #pragma unroll
-    for (int q = 0; q < (GT * GK) / 256; ++q) {
+    for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
-      const size_t i = p0 + ii;
-      const size_t gj = j0 + cc, gk = k0 + cc;
-      Xs[ii][cc] = (i < ie && gj < ncols) ? (double)X[i * ncols + gj] : 0.0;
-      Vs[ii][cc] = (i < ie && gk < r) ? (double)V[i * r + gk] : 0.0;
+      const size_t i = p0 + ii, gj = j0 + cc, gk = k0 + cc;
+      rx[q] = (i < ie && gj < ncols) ? (double)X[i * ncols + gj] : 0.0;
+      rv[q] = (i < ie && gk < r) ? (double)V[i * r + gk] : 0.0;
+    }
+  };
+  fetch(ib);
+  int buf = 0;
+  for (size_t p0 = ib; p0 < ie; p0 += GKS, buf ^= 1) {
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) {
+      const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
+      Xs[buf][ii][cc] = rx[q];
+      Vs[buf][ii][cc] = rv[q];
     }
     __syncthreads();
-#pragma unroll 8
-    for (int ii = 0; ii < GK; ++ii) {
+    if (p0 + GKS < ie) fetch(p0 + GKS);
+#pragma unroll
+    for (int ii = 0; ii < GKS; ++ii) {
       double va[4], xb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) va[a] = Vs[ii][ty + 16 * a];
+      for (int a = 0; a < 4; ++a) va[a] = Vs[buf][ii][ty + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) xb[b] = Xs[ii][tx + 16 * b];
+      for (int b = 0; b < 4; ++b) xb[b] = Xs[buf][ii][tx + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], va[a], xb[b]);
     }
-    __syncthreads();
   }
   double* out = part + (size_t)blockIdx.z * r * ncols;
 #pragma unroll
