@@ -175,22 +175,27 @@ struct Engine::Impl {
   }
 
   // out (rows x ny, fp64) = X (rows x K) * Y (ny x K)^T
+  // output tile extent along the narrow (rank) dimension
+  static int narrow_tile(size_t extent) { return extent <= 32 ? 32 : extent <= 48 ? 48 : 64; }
+
   template <typename T>
   void gemm_abt(const T* X, const T* Y, size_t rows, size_t ny, size_t K, double* out) {
-    const size_t tiles = ceil_div(rows, GT) * ceil_div(ny, GT);
+    const int tc = narrow_tile(ny);
+    const size_t tiles = ceil_div(rows, GT) * ceil_div(ny, (size_t)tc);
     const int sp = splits_for(tiles, K);
     const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
     const int spr = (int)ceil_div(K, kchunk);
-    dim3 g((unsigned)ceil_div(rows, GT), (unsigned)ceil_div(ny, GT), (unsigned)spr);
+    dim3 g((unsigned)ceil_div(rows, GT), (unsigned)ceil_div(ny, (size_t)tc), (unsigned)spr);
     double* dst = out;
     if (spr > 1) {
       part.ensure((size_t)spr * rows * ny * 8);
       dst = part.as<double>();
     }
+    auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst); };
     if (exact())
-      launch(k_gemm_abt<T, true>, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst);
+      tc == 32 ? go(k_gemm_abt<T, true, 32>) : tc == 48 ? go(k_gemm_abt<T, true, 48>) : go(k_gemm_abt<T, true, 64>);
     else
-      launch(k_gemm_abt<T, false>, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst);
+      tc == 32 ? go(k_gemm_abt<T, false, 32>) : tc == 48 ? go(k_gemm_abt<T, false, 48>) : go(k_gemm_abt<T, false, 64>);
     if (spr > 1) {
       const size_t cnt = rows * ny;
       reduce_splits(part.as<double>(), cnt, spr, out);
@@ -200,20 +205,22 @@ struct Engine::Impl {
   // out (r x ncols, fp64) = V (K x r)^T * X (K x ncols)
   template <typename T>
   void gemm_atb(const T* V, const T* X, size_t K, size_t r, size_t ncols, double* out) {
-    const size_t tiles = ceil_div(ncols, GT) * ceil_div(r, GT);
+    const int tr = narrow_tile(r);
+    const size_t tiles = ceil_div(ncols, GT) * ceil_div(r, (size_t)tr);
     const int sp = splits_for(tiles, K);
     const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
     const int spr = (int)ceil_div(K, kchunk);
-    dim3 g((unsigned)ceil_div(ncols, GT), (unsigned)ceil_div(r, GT), (unsigned)spr);
+    dim3 g((unsigned)ceil_div(ncols, GT), (unsigned)ceil_div(r, (size_t)tr), (unsigned)spr);
     double* dst = out;
     if (spr > 1) {
       part.ensure((size_t)spr * r * ncols * 8);
       dst = part.as<double>();
     }
+    auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst); };
     if (exact())
-      launch(k_gemm_atb<T, true>, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst);
+      tr == 32 ? go(k_gemm_atb<T, true, 32>) : tr == 48 ? go(k_gemm_atb<T, true, 48>) : go(k_gemm_atb<T, true, 64>);
     else
-      launch(k_gemm_atb<T, false>, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst);
+      tr == 32 ? go(k_gemm_atb<T, false, 32>) : tr == 48 ? go(k_gemm_atb<T, false, 48>) : go(k_gemm_atb<T, false, 64>);
     if (spr > 1) {
       const size_t cnt = r * ncols;
       reduce_splits(part.as<double>(), cnt, spr, out);

@@ -63,32 +63,40 @@ constexpr int GKS = 16;  // K step of the two-stage kernels (2 x 2 x 16 x 65 dou
 // part[z][i][k] = sum_{p in split z} X[i][p] * Y[k][p]
 //   X: rows x K (row-major, ld = K), Y: ny x K (row-major, ld = K).
 //   (A = M W^T with X = M, Y = W; B = W W^T with X = Y = W.)
-template <typename T, bool EXACT>
+// TC: the output tile's width along Y (32 / 48 / 64; ny = r is narrow)
+template <typename T, bool EXACT, int TC = GT>
 __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const T* __restrict__ Y,
                                                   size_t rows, size_t ny, size_t K, size_t kchunk,
                                                   double* __restrict__ part) {
   // two stages: the next K step's operands are loaded into registers while
   // the current one is multiplied (one barrier per step; the single-stage
   // version exposed an L2 round trip per 32-wide K step)
+  constexpr int NB = TC / 16;             // outputs per thread along Y
   __shared__ double Xs[2][GKS][GT + 1];
-  __shared__ double Ys[2][GKS][GT + 1];
-  constexpr int PQ = (GT * GKS) / 256;  // operand elements per thread and stage
+  __shared__ double Ys[2][GKS][TC + 1];
+  constexpr int PQ = (GT * GKS) / 256;    // X elements per thread and stage
+  constexpr int PQY = (TC * GKS) / 256;   // Y elements per thread and stage
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const size_t i0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
+  const size_t i0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * TC;
   const size_t kb = (size_t)blockIdx.z * kchunk;
   const size_t ke = kb + kchunk < K ? kb + kchunk : K;
-  double acc[4][4];
+  double acc[4][NB];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  double rx[PQ], ry[PQ];
+    for (int b = 0; b < NB; ++b) acc[a][b] = 0.0;
+  double rx[PQ], ry[PQY];
   auto fetch = [&](size_t p0) {
 #pragma unroll
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
-      const size_t p = p0 + pp, gi = i0 + rr, gk = k0 + rr;
+      const size_t p = p0 + pp, gi = i0 + rr;
       rx[q] = (gi < rows && p < ke) ? (double)X[gi * K + p] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PQY; ++q) {
+      const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
+      const size_t p = p0 + pp, gk = k0 + rr;
       ry[q] = (gk < ny && p < ke) ? (double)Y[gk * K + p] : 0.0;
     }
   };
@@ -99,21 +107,25 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
       Xs[buf][pp][rr] = rx[q];
+    }
+#pragma unroll
+    for (int q = 0; q < PQY; ++q) {
+      const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
       Ys[buf][pp][rr] = ry[q];
     }
     __syncthreads();
     if (p0 + GKS < ke) fetch(p0 + GKS);
 #pragma unroll
     for (int kk = 0; kk < GKS; ++kk) {
-      double xa[4], yb[4];
+      double xa[4], yb[NB];
 #pragma unroll
       for (int a = 0; a < 4; ++a) xa[a] = Xs[buf][kk][ty + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) yb[b] = Ys[buf][kk][tx + 16 * b];
+      for (int b = 0; b < NB; ++b) yb[b] = Ys[buf][kk][tx + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], xa[a], yb[b]);
+        for (int b = 0; b < NB; ++b) acc[a][b] = madd<EXACT>(acc[a][b], xa[a], yb[b]);
     }
   }
   double* out = part + (size_t)blockIdx.z * rows * ny;
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const
     const size_t gi = i0 + ty + 16 * a;
     if (gi >= rows) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const size_t gk = k0 + tx + 16 * b;
       if (gk < ny) out[gi * ny + gk] = acc[a][b];
     }
@@ -132,29 +144,37 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const
 // part[z][k][j] = sum_{i in split z} V[i][k] * X[i][j]
 //   V: K x r (row-major), X: K x ncols (row-major).
 //   (C = V^T M with X = M; D = V^T V with X = V, ncols = r.)
-template <typename T, bool EXACT>
+// TR: the output tile's height along r (32 / 48 / 64)
+template <typename T, bool EXACT, int TR = GT>
 __global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const T* __restrict__ X,
                                                   size_t K, size_t r, size_t ncols, size_t kchunk,
                                                   double* __restrict__ part) {
+  constexpr int NA = TR / 16;            // outputs per thread along r
   __shared__ double Xs[2][GKS][GT + 1];  // two stages, as k_gemm_abt
-  __shared__ double Vs[2][GKS][GT + 1];
+  __shared__ double Vs[2][GKS][TR + 1];
   constexpr int PQ = (GT * GKS) / 256;
+  constexpr int PQV = (TR * GKS) / 256;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const size_t j0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * GT;
+  const size_t j0 = (size_t)blockIdx.x * GT, k0 = (size_t)blockIdx.y * TR;
   const size_t ib = (size_t)blockIdx.z * kchunk;
   const size_t ie = ib + kchunk < K ? ib + kchunk : K;
-  double acc[4][4];
+  double acc[NA][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < NA; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  double rx[PQ], rv[PQ];
+  double rx[PQ], rv[PQV];
   auto fetch = [&](size_t p0) {
 #pragma unroll
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
-      const size_t i = p0 + ii, gj = j0 + cc, gk = k0 + cc;
+      const size_t i = p0 + ii, gj = j0 + cc;
       rx[q] = (i < ie && gj < ncols) ? (double)X[i * ncols + gj] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PQV; ++q) {
+      const int e = tid + 256 * q, ii = e / TR, cc = e % TR;
+      const size_t i = p0 + ii, gk = k0 + cc;
       rv[q] = (i < ie && gk < r) ? (double)V[i * r + gk] : 0.0;
     }
   };
@@ -165,26 +185,30 @@ __global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
       Xs[buf][ii][cc] = rx[q];
+    }
+#pragma unroll
+    for (int q = 0; q < PQV; ++q) {
+      const int e = tid + 256 * q, ii = e / TR, cc = e % TR;
       Vs[buf][ii][cc] = rv[q];
     }
     __syncthreads();
     if (p0 + GKS < ie) fetch(p0 + GKS);
 #pragma unroll
     for (int ii = 0; ii < GKS; ++ii) {
-      double va[4], xb[4];
+      double va[NA], xb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) va[a] = Vs[buf][ii][ty + 16 * a];
+      for (int a = 0; a < NA; ++a) va[a] = Vs[buf][ii][ty + 16 * a];
 #pragma unroll
       for (int b = 0; b < 4; ++b) xb[b] = Xs[buf][ii][tx + 16 * b];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < NA; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = madd<EXACT>(acc[a][b], va[a], xb[b]);
     }
   }
   double* out = part + (size_t)blockIdx.z * r * ncols;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
+  for (int a = 0; a < NA; ++a) {
     const size_t gk = k0 + ty + 16 * a;
     if (gk >= r) continue;
 #pragma unroll
