@@ -292,7 +292,7 @@ struct Engine::Impl {
   }
 
   // ---------------- row/column sweeps ----------------
-  // Non-exact HALS sweeps over few rows / columns use a warp per row (warp-
+  // Non-exact HALS (and MU) sweeps over few rows / columns use a warp per row (warp-
   // shuffle dot products): one thread per column leaves the GPU idle there
   // (config 3's W half: n = 165).  With many rows the thread-per-row kernels
   // win (measured: config 3's V half 0.58 -> 0.82 ms/step and config 4's step
@@ -339,6 +339,9 @@ struct Engine::Impl {
       ++e->launches_;
     } else if (kind == kHals) {
       launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
+    } else if (kind == kMu && warp_sweeps(r, L.m)) {
+      launch(k_mu_warp<T, false>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)),
+             dim3(256), r * r * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r);
     } else if (kind == kMu && mu_reg_supported(r)) {
       mu_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, s);
       ++e->launches_;
@@ -362,6 +365,10 @@ struct Engine::Impl {
     } else if (kind == kHals) {
       launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
              e->n_loc_, (int)r, deg);
+    } else if (kind == kMu && warp_sweeps(r, e->n_loc_)) {
+      launch(k_mu_warp<T, true>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
+             dim3(256), r * r * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_,
+             (int)r);
     } else if (kind == kMu && mu_reg_supported(r)) {
       mu_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, s);
       ++e->launches_;

@@ -472,6 +472,35 @@ __global__ void k_mu_w(const double* __restrict__ Cm, const double* __restrict__
   }
 }
 
+// Warp-per-row MU (non-exact: fused multiply-adds in register order) for few
+// rows / columns, where one thread per row leaves most SMs idle (config 1's
+// W half: 2429 columns -> 19 blocks of the thread kernels).  Lanes own the
+// outputs k = lane, lane + 32; the factor row is broadcast by shuffles; the
+// Gram sits in shared memory once per persistent block.  CT: columns of W
+// (element (k, j) at k * n + j) against D; otherwise rows of V against B.
+template <typename T, bool CT>
+__global__ void __launch_bounds__(256) k_mu_warp(const double* __restrict__ A, const double* __restrict__ G,
+                                                 T* __restrict__ V, size_t m, int r) {
+  extern __shared__ double Gs[];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = G[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  auto at = [&](size_t row, int k) -> size_t { return CT ? (size_t)k * m + row : row * (size_t)r + k; };
+  for (size_t i = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += (size_t)gridDim.x * 8) {
+    const double v0 = lane < r ? (double)V[at(i, lane)] : 0.0;
+    const double v1 = lane + 32 < r ? (double)V[at(i, lane + 32)] : 0.0;
+    double s0 = 0.0, s1 = 0.0;
+    for (int p = 0; p < r; ++p) {
+      const double vp = __shfl_sync(0xffffffffu, p < 32 ? v0 : v1, p & 31);
+      // V: (V B)_k = sum_p v_p B[p][k];  W: (D W)_k = sum_p D[k][p] w_p
+      if (lane < r) s0 = fma(vp, CT ? Gs[lane * r + p] : Gs[p * r + lane], s0);
+      if (lane + 32 < r) s1 = fma(vp, CT ? Gs[(lane + 32) * r + p] : Gs[p * r + lane + 32], s1);
+    }
+    if (lane < r) V[at(i, lane)] = to_t<T>(v0 * (A[at(i, lane)] / mu_floor(s0)));
+    if (lane + 32 < r) V[at(i, lane + 32)] = to_t<T>(v1 * (A[at(i, lane + 32)] / mu_floor(s1)));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Direct residual ||M - VW||^2 per column (kernels.cpp:48-60):
 //   part[z][j] = sum_{i in split z} (M_ij - sum_k V_ik W_kj)^2
