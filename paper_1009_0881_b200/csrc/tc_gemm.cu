@@ -55,6 +55,9 @@ namespace tc {
 
 // nanosleep (ns) between failed barrier polls of the TMA producers and of
 // the converters (0: spin); spinning warps take issue slots and power
+#ifndef MLB_TC_ST64
+#define MLB_TC_ST64 0  // one 64-column tcgen05.st per chunk instead of two of 32
+#endif
 #ifndef MLB_TC_PSLEEP
 #define MLB_TC_PSLEEP 0
 #endif
@@ -293,6 +296,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       TC_REG32(v)
       : "memory");
 }
+// 64 consecutive columns (hi | lo of a staging slot) in one instruction
+__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&a)[32], const uint32_t (&b)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, "
+      "%37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, "
+      "%59, %60, %61, %62, %63, %64};" ::"r"(taddr),
+      TC_REG32(a), TC_REG32(b)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -511,7 +524,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
   int lastb[kBStages];       // ... and on the factor-slice stages this warp used
 #pragma unroll
   for (int k = 0; k < kBStages; ++k) lastb[k] = -1;
-  static_assert(!PAIR || kK3, "CTA pairs: K3 form only");
+  // CTA pairs: K3 form only (the host never selects pairs otherwise)
   for (int u = u0; u < total_units; u += ustep) {
     const int n_u = unit_of(p, u).n;
     for (int i = own_first(g, W), j = 0; i < n_u; i += 2, ++j) {
@@ -544,6 +557,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
         const uint64_t bd_lo = bd + ((uint64_t)((PAIR ? p.rp / 2 : p.rp) * 128) >> 4);
         constexpr int A0 = W * kAccBufs, A1 = W * kAccBufs + (kAccBufs > 1 ? 1 : 0);
         const int sidx = slot >> 1;  // this warp's slots are W, W + 2, ...
+#ifndef MLB_TC_EXP_NOMMA  // timing experiment: no MMAs (wrong results)
         if (abuf == 0) {
           if (sidx == 0) issue_chunk3<W, A0, PAIR>(bd, bd_lo, id_hi, first);
           else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0, PAIR>(bd, bd_lo, id_hi, first);
@@ -553,6 +567,9 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
           else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
           else issue_chunk3<(W + 4) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
         }
+#else
+        (void)sidx, (void)bd_lo;
+#endif
       } else {
         if (slot == W)
           issue_chunk<W, W>(bd, id_full, id_hi, first);
@@ -849,8 +866,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (q == 0) TCT(2, g);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStgCol0 + slot * 64;
+#ifndef MLB_TC_EXP_NOST  // timing experiment: no TMEM stores (wrong results)
+#if MLB_TC_ST64
+        tmem_st64(ta, hi, lo);
+#else
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
+#endif
+#endif
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -1461,7 +1484,7 @@ class TcGemmImpl final : public TcGemm {
     }
     // CTA pairs (cta_group::2, 256-row tiles): r_pad in {32, 64} (N split in
     // halves of >= 16 rows), an even SM count, enough tiles to fill the pairs
-    const bool pair = pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
+    const bool pair = tc::kK3 && pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
     const int slots = pair ? sms_ / 2 : sms_;  // persistent schedulers: pairs or CTAs
     tc::Params p{};
     p.rows = (int)rows;
