@@ -44,10 +44,22 @@ __host__ __device__ inline size_t nnls_warp_bytes(int r) {
 // substitutions, which then multiply instead of divide.
 template <bool EXACT>
 __device__ inline bool warp_cholesky(double* L, int p, int lane) {
+  // 32-bit packed-row offsets and 4-way unrolled dot products: the kernel is
+  // issue-bound (ncu: 62 % issue-active, ~42k warp instructions per
+  // subproblem), and 64-bit index math plus loop overhead were most of the
+  // inner loops' instructions.  The subtraction order is unchanged.
   for (int k = 0; k < p; ++k) {
-    const size_t rk = (size_t)k * (k + 1) / 2;
-    double d = L[rk + k];
-    for (int q = 0; q < k; ++q) d = msub(d, L[rk + q], L[rk + q]);
+    const double* Lk = L + (unsigned)(k * (k + 1) / 2);
+    double d = Lk[k];
+    int q = 0;
+    for (; q + 4 <= k; q += 4) {
+      const double a0 = Lk[q], a1 = Lk[q + 1], a2 = Lk[q + 2], a3 = Lk[q + 3];
+      d = msub(d, a0, a0);
+      d = msub(d, a1, a1);
+      d = msub(d, a2, a2);
+      d = msub(d, a3, a3);
+    }
+    for (; q < k; ++q) d = msub(d, Lk[q], Lk[q]);
     if (d <= 0.0 || !isfinite(d)) {
       __syncwarp();
       return false;
@@ -55,13 +67,20 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
     const double lkk = sqrt(d);
     const double ilkk = EXACT ? 0.0 : 1.0 / lkk;
     for (int i = k + 1 + lane; i < p; i += 32) {
-      const size_t ri = (size_t)i * (i + 1) / 2;
-      double s = L[ri + k];
-      for (int q = 0; q < k; ++q) s = msub(s, L[ri + q], L[rk + q]);
-      L[ri + k] = EXACT ? s / lkk : s * ilkk;
+      double* Li = L + (unsigned)(i * (i + 1) / 2);
+      double s = Li[k];
+      int qq = 0;
+      for (; qq + 4 <= k; qq += 4) {
+        s = msub(s, Li[qq], Lk[qq]);
+        s = msub(s, Li[qq + 1], Lk[qq + 1]);
+        s = msub(s, Li[qq + 2], Lk[qq + 2]);
+        s = msub(s, Li[qq + 3], Lk[qq + 3]);
+      }
+      for (; qq < k; ++qq) s = msub(s, Li[qq], Lk[qq]);
+      Li[k] = EXACT ? s / lkk : s * ilkk;
     }
     __syncwarp();
-    if (lane == 0) L[rk + k] = EXACT ? lkk : ilkk;
+    if (lane == 0) L[(unsigned)(k * (k + 1) / 2) + k] = EXACT ? lkk : ilkk;
     __syncwarp();
   }
   return true;
