@@ -309,7 +309,8 @@ def run_b200(args):
                      "frac": achieved / peak, "traffic": traffic_for(dom, world), "kernel": dom,
                      "peak_source": peak_src, "traffic_source": TRAFFIC_SRC,
                      "algorithmic_bytes_per_launch": bytes_per_pass,
-                     "avg_ms": {"A = M W^T": mwt_ms, "C = V^T M": vtm_ms},
+                     "avg_ms": {"A = M W^T": mwt_ms, "C = V^T M": vtm_ms,
+                                "allreduce [A|B]": kt["comm_ms"] / max(kt["comm_n"], 1) if kt["comm_n"] else 0.0},
                      "step_frac_in_products": (mwt_ms + vtm_ms) / (ms_max / args.steps)},
         "rel_error": {"start": float(tr0.error[0]) / norm, "after_bench": err_end / norm},
         "gen_s": t_gen,

@@ -203,6 +203,9 @@ int mlnmf_session_products(mlnmf_session* s, double* A, double* C);
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
 int mlnmf_session_set_profiling(mlnmf_session* s, int on);
 int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, double* vtm_ms, long* vtm_n);
+/* profiled time of the per-step NCCL allreduce of [M W^T | W W^T] (world > 1;
+ * 0 calls on one rank), CUDA events on the engine stream */
+int mlnmf_session_comm_time(mlnmf_session* s, double* ms, long* count);
 long mlnmf_session_launches(mlnmf_session* s);
 void* mlnmf_session_stream(mlnmf_session* s);
 /* 1 if the tcgen05 path serves the M-streaming products */

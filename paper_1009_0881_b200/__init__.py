@@ -829,7 +829,9 @@ class Session:
         a, c = C.c_double(), C.c_double()
         an, cn = C.c_long(), C.c_long()
         _check(_lib.mlnmf_session_kernel_times(self._h, C.byref(a), C.byref(an), C.byref(c), C.byref(cn)))
-        return dict(mwt_ms=a.value, mwt_n=an.value, vtm_ms=c.value, vtm_n=cn.value)
+        x, xn = C.c_double(), C.c_long()
+        _check(_lib.mlnmf_session_comm_time(self._h, C.byref(x), C.byref(xn)))
+        return dict(mwt_ms=a.value, mwt_n=an.value, vtm_ms=c.value, vtm_n=cn.value, comm_ms=x.value, comm_n=xn.value)
 
     @property
     def launches(self) -> int:

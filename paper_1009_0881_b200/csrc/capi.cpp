@@ -459,6 +459,13 @@ int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, do
   });
 }
 
+int mlnmf_session_comm_time(mlnmf_session* s, double* ms, long* count) {
+  return guard([&] {
+    KernelTimes k = s->e->kernel_times();
+    *ms = k.comm_ms, *count = k.comm_n;
+  });
+}
+
 long mlnmf_session_launches(mlnmf_session* s) { return s->e->launches(); }
 void* mlnmf_session_stream(mlnmf_session* s) { return s->e->stream(); }
 int mlnmf_session_tc_active(mlnmf_session* s) { return s->e->tc_active() ? 1 : 0; }

@@ -109,7 +109,7 @@ struct Engine::Impl {
   // NCCL
   ncclComm_t comm = nullptr;
   // profiling
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mwt, ev_vtm;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mwt, ev_vtm, ev_comm;
   std::vector<cudaEvent_t> ev_pool;
   std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
   TcGemm* tc = nullptr;
@@ -320,11 +320,20 @@ struct Engine::Impl {
     if (needB) gram_W<T>();
     product_mwt<T>(l);
     if (comm) {
+      std::pair<cudaEvent_t, cudaEvent_t> evp{};
+      if (e->profiling_) {
+        evp = {ev(), ev()};
+        CK(cudaEventRecord(evp.first, s));
+      }
       if (needB && L.m == e->lv_[0].m) {
         allreduce_sum(A(), L.m * r + r * r);  // A|B contiguous: one collective
       } else {
         allreduce_sum(A(), L.m * r);
         if (needB) allreduce_sum(B(), r * r);
+      }
+      if (e->profiling_) {
+        CK(cudaEventRecord(evp.second, s));
+        ev_comm.push_back(evp);
       }
     }
     T* V = static_cast<T*>(L.V);
@@ -1145,6 +1154,12 @@ KernelTimes Engine::kernel_times() {
     kt.vtm_ms += ms;
     ++kt.vtm_n;
   }
+  for (auto& p : impl_->ev_comm) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p.first, p.second));
+    kt.comm_ms += ms;
+    ++kt.comm_n;
+  }
   return kt;
 }
 
@@ -1152,8 +1167,10 @@ void Engine::reset_kernel_times() {
   sync();
   for (auto& p : impl_->ev_mwt) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
   for (auto& p : impl_->ev_vtm) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
+  for (auto& p : impl_->ev_comm) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
   impl_->ev_mwt.clear();
   impl_->ev_vtm.clear();
+  impl_->ev_comm.clear();
 }
 
 }  // namespace mlb

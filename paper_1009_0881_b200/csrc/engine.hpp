@@ -57,6 +57,8 @@ struct Sample {
 struct KernelTimes {  // filled when profiling is on (CUDA events on the engine stream)
   double mwt_ms = 0, vtm_ms = 0;  // total over recorded launches
   long mwt_n = 0, vtm_n = 0;
+  double comm_ms = 0;  // the per-step allreduce of [A | B] (world > 1)
+  long comm_n = 0;
 };
 
 class Engine {

@@ -402,3 +402,24 @@ def test_nccl_single_rank_path(P, cfg0):
             V1, W1 = s.get_factors()
         assert np.array_equal(t0.error, t1.error)
         assert np.array_equal(V0, V1) and np.array_equal(W0, W1)
+
+
+def test_nccl_allreduce_is_profiled(P, cfg0):
+    """With profiling on, every step's allreduce of [A | B] is timed on the
+    engine stream (bench.py reports it per step at N > 1); none without a
+    communicator."""
+    nid = P.nccl_unique_id()
+    with P.Session(dtype=P.F32, world=1, rank=0, nccl_id=nid) as s:
+        s.set_data(cfg0, P.ImageGrid(32, 32))
+        s.run_configuration(1, "hals", "none", 20, 0, 0.0, 0)
+        s.set_profiling(True)
+        s.steps("hals", 4)
+        kt = s.kernel_times()
+    assert kt["comm_n"] == 4 and kt["comm_ms"] > 0.0, kt
+    assert kt["mwt_n"] == 4 and kt["vtm_n"] == 4
+    with P.Session(dtype=P.F32) as s:
+        s.set_data(cfg0, P.ImageGrid(32, 32))
+        s.run_configuration(1, "hals", "none", 20, 0, 0.0, 0)
+        s.set_profiling(True)
+        s.steps("hals", 2)
+        assert s.kernel_times()["comm_n"] == 0
