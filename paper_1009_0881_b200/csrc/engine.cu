@@ -300,6 +300,9 @@ struct Engine::Impl {
   // (re-measured with the persistent two-row warp kernels: config 3 0.585 ->
   // 0.713 ms/step, config 4 +1.3 ms/step; MLNMF_WARP_SWEEPS=1 forces them)
   static constexpr size_t kWarpSweepMax = 16384;
+  // register sweeps at the config-4 rank: interleaved fused dot chains in
+  // non-exact runs (MLNMF_EXACT_SWEEPS=1 keeps the reference order)
+  bool fast_sweeps() const { return !exact() && std::getenv("MLNMF_EXACT_SWEEPS") == nullptr; }
   bool warp_sweeps(size_t r, size_t count) const {
     if (exact() || r > 64 || std::getenv("MLNMF_THREAD_SWEEPS") != nullptr) return false;
     return count < kWarpSweepMax || std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
@@ -344,7 +347,7 @@ struct Engine::Impl {
       launch(k_hals_v_warp<T>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
              (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
     } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
-      hals_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, deg, s);
+      hals_v_reg(r, sizeof(T) == 4, fast_sweeps(), A(), B(), V, L.m, deg, s);
       ++e->launches_;
     } else if (kind == kHals) {
       launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
@@ -369,7 +372,7 @@ struct Engine::Impl {
              dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
              e->n_loc_, (int)r, deg);
     } else if (kind == kHals && hals_reg_supported(r)) {
-      hals_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
+      hals_w_reg(r, sizeof(T) == 4, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
       ++e->launches_;
     } else if (kind == kHals) {
       launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,

@@ -27,7 +27,11 @@ __device__ __forceinline__ double msub(double acc, double a, double b) { return 
 // and l loops are unrolled.  Same arithmetic and operation order as k_hals_v /
 // k_hals_w (the reference's, unfused), so results are bitwise identical;
 // ~10x fewer shared-memory accesses.
-template <typename T, int R>
+// FAST (non-exact runs): the l-sum as four interleaved fused chains and the
+// division by a per-block reciprocal -- the reference-order chain is 2R
+// dependent fp64 operations per update (~1000 cycles of latency at R = 64),
+// the interleaved one R / 4 fused ones.
+template <typename T, int R, bool FAST = false>
 __global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A, const double* __restrict__ B,
                                                     T* __restrict__ V, size_t m, int* __restrict__ degenerate) {
   __shared__ double Bt[R * R];  // Bt[k][l] = B[l][k]: row k is the column the update reads
@@ -47,10 +51,18 @@ __global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A
       continue;
     }
     const double a = act ? A[i * R + k] : 0.0;
-    double num = __dadd_rn(a, __dmul_rn(v[k], bkk));
+    double q;
+    if (FAST) {
+      double p4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int l = 0; l < R; ++l) num = msub(num, v[l], Bt[k * R + l]);
-    const double q = num / bkk;
+      for (int l = 0; l < R; ++l) p4[l & 3] = fma(v[l], Bt[k * R + l], p4[l & 3]);
+      q = (fma(v[k], bkk, a) - ((p4[0] + p4[1]) + (p4[2] + p4[3]))) * (1.0 / bkk);
+    } else {
+      double num = __dadd_rn(a, __dmul_rn(v[k], bkk));
+#pragma unroll
+      for (int l = 0; l < R; ++l) num = msub(num, v[l], Bt[k * R + l]);
+      q = num / bkk;
+    }
     v[k] = q > 0.0 ? q : 0.0;
   }
   if (act)
@@ -58,7 +70,7 @@ __global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A
     for (int l = 0; l < R; ++l) V[i * R + l] = to_t<T>(v[l]);
 }
 
-template <typename T, int R>
+template <typename T, int R, bool FAST = false>
 __global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ Cm, const double* __restrict__ D,
                                                     T* __restrict__ W, size_t n, int* __restrict__ degenerate) {
   __shared__ double Ds[R * R];
@@ -78,10 +90,18 @@ __global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ C
       continue;
     }
     const double c = act ? Cm[(size_t)k * n + j] : 0.0;
-    double num = __dadd_rn(c, __dmul_rn(dkk, w[k]));
+    double q;
+    if (FAST) {
+      double p4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int l = 0; l < R; ++l) num = msub(num, Ds[k * R + l], w[l]);
-    const double q = num / dkk;
+      for (int l = 0; l < R; ++l) p4[l & 3] = fma(Ds[k * R + l], w[l], p4[l & 3]);
+      q = (fma(dkk, w[k], c) - ((p4[0] + p4[1]) + (p4[2] + p4[3]))) * (1.0 / dkk);
+    } else {
+      double num = __dadd_rn(c, __dmul_rn(dkk, w[k]));
+#pragma unroll
+      for (int l = 0; l < R; ++l) num = msub(num, Ds[k * R + l], w[l]);
+      q = num / dkk;
+    }
     w[k] = q > 0.0 ? q : 0.0;
   }
   if (act)
@@ -138,17 +158,21 @@ __global__ void __launch_bounds__(128) k_mu_w_reg(const double* __restrict__ Cm,
 }
 
 template <int R>
-void launch_v(bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
+void launch_v(bool f32, bool fast, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
   const dim3 g((unsigned)((m + 127) / 128));
-  if (f32)
+  if (f32 && fast)
+    k_hals_v_reg<float, R, true><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m, deg);
+  else if (f32)
     k_hals_v_reg<float, R><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m, deg);
   else
     k_hals_v_reg<double, R><<<g, 128, 0, s>>>(A, B, static_cast<double*>(V), m, deg);
 }
 template <int R>
-void launch_w(bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
+void launch_w(bool f32, bool fast, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
   const dim3 g((unsigned)((n + 127) / 128));
-  if (f32)
+  if (f32 && fast)
+    k_hals_w_reg<float, R, true><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n, deg);
+  else if (f32)
     k_hals_w_reg<float, R><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n, deg);
   else
     k_hals_w_reg<double, R><<<g, 128, 0, s>>>(C, D, static_cast<double*>(W), n, deg);
@@ -181,14 +205,16 @@ void mu_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, siz
   check(cudaGetLastError());
 }
 
-void hals_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
-  if (r == 64) launch_v<64>(f32, A, B, V, m, deg, s);
+void hals_v_reg(size_t r, bool f32, bool fast, const double* A, const double* B, void* V, size_t m, int* deg,
+                cudaStream_t s) {
+  if (r == 64) launch_v<64>(f32, fast, A, B, V, m, deg, s);
   else throw std::invalid_argument("hals_v_reg: unsupported rank");
   check(cudaGetLastError());
 }
 
-void hals_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
-  if (r == 64) launch_w<64>(f32, C, D, W, n, deg, s);
+void hals_w_reg(size_t r, bool f32, bool fast, const double* C, const double* D, void* W, size_t n, int* deg,
+                cudaStream_t s) {
+  if (r == 64) launch_w<64>(f32, fast, C, D, W, n, deg, s);
   else throw std::invalid_argument("hals_w_reg: unsupported rank");
   check(cudaGetLastError());
 }

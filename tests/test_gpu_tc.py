@@ -130,3 +130,21 @@ def test_tc_products_cta_pairs(P, gpu, monkeypatch, m, n, r):
         A, C = s.products()
     ea, ec = relnorm(A, M64 @ W64.T), relnorm(C, V64.T @ M64)
     assert ea < TOL and ec < TOL, (ea, ec)
+
+
+def test_fast_register_sweeps_match_reference_order(P, gpu, monkeypatch):
+    """Config-4 rank (r = 64) at >= 16k rows and columns: the non-exact
+    register sweeps (interleaved fused dot chains, reciprocal pivots) agree
+    with the reference-order register sweeps to fp64 rounding over 3 HALS
+    steps (same tensor-core products on both sides)."""
+    out = []
+    for exact_sweeps in (False, True):
+        if exact_sweeps:
+            monkeypatch.setenv("MLNMF_EXACT_SWEEPS", "1")
+        with P.Session(dtype=P.F32) as s:
+            s.generate(4, seed=0, n_total=16384)
+            s.run_configuration(1, "hals", "none", 64, 0, 0.0, 0)
+            s.steps("hals", 3)
+            out.append(s.get_factors())
+    (V0, W0), (V1, W1) = out
+    assert relnorm(V0, V1) < 1e-6 and relnorm(W0, W1) < 1e-6, (relnorm(V0, V1), relnorm(W0, W1))
