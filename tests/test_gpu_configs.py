@@ -1,4 +1,5 @@
-"""GPU parity at BASELINE configs 2 and 3: the paper's face-sized
+"""GPU parity at BASELINE configs 1-3: the CBCL-sized 19 x 19
+(2 levels, 19x19 -> 10x10 by the odd-size rule), the paper's face-sized
 (112 x 92, 4 levels: 112x92 -> 56x46 -> 28x23 -> 14x12) and large-image
 (243 x 320, 5 levels: -> 122x160 -> 61x80 -> 31x40 -> 16x20) shapes, whose
 pyramids exercise the odd-size coarsening and boundary-renormalised transfer
@@ -25,6 +26,11 @@ def _defaults(P):
     P.set_default_options()
     yield
     P.set_default_options()
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return oracle.generate_config(1)  # 361 x 2429, scaled to [0, 1]
 
 
 @pytest.fixture(scope="module")
@@ -55,6 +61,8 @@ def same_schedule(tg, to):
 
 CASES_EXACT = [
     # (config, grid h, w, levels, kind, cycle, rank, budget)
+    (1, 19, 19, 2, "hals", "fmg", 49, 20.0),
+    (1, 19, 19, 2, "mu", "vc", 49, 20.0),
     (2, 112, 92, 4, "anls", "fmg", 40, 2.0),
     (2, 112, 92, 4, "hals", "vc", 40, 4.0),
     (3, 243, 320, 5, "hals", "fmg", 49, 2.0),
@@ -64,9 +72,9 @@ CASES_EXACT = [
 
 
 @pytest.mark.parametrize("case", CASES_EXACT, ids=lambda c: f"cfg{c[0]}-{c[4]}-{c[5]}")
-def test_configs_exact_bitwise(P, restated, cfg2, cfg3, case):
+def test_configs_exact_bitwise(P, restated, cfg1, cfg2, cfg3, case):
     cfg, h, w, L, kind, cycle, r, budget = case
-    M = cfg2 if cfg == 2 else cfg3
+    M = {1: cfg1, 2: cfg2, 3: cfg3}[cfg]
     P.set_default_options(exact=True)
     Vo, Wo, to = restated.run_configuration(M, h, w, L, kind, cycle, r, 0, budget, 1)
     res = P.run_configuration(M, P.ImageGrid(h, w), L, kind, cycle, r, 0, budget, 1)
@@ -78,6 +86,7 @@ def test_configs_exact_bitwise(P, restated, cfg2, cfg3, case):
 
 
 CASES_FP32 = [
+    (1, 19, 19, 2, "hals", "ni", 49, 20.0),
     (2, 112, 92, 4, "hals", "ni", 40, 4.0),
     (2, 112, 92, 4, "mu", "fmg", 40, 3.0),
     (3, 243, 320, 5, "hals", "vc", 49, 2.0),
@@ -86,9 +95,9 @@ CASES_FP32 = [
 
 
 @pytest.mark.parametrize("case", CASES_FP32, ids=lambda c: f"cfg{c[0]}-{c[4]}-{c[5]}")
-def test_configs_fp32_within_1e5(P, restated, cfg2, cfg3, case):
+def test_configs_fp32_within_1e5(P, restated, cfg1, cfg2, cfg3, case):
     cfg, h, w, L, kind, cycle, r, budget = case
-    M = cfg2 if cfg == 2 else cfg3
+    M = {1: cfg1, 2: cfg2, 3: cfg3}[cfg]
     m, n = M.shape
     M32 = M.astype(np.float32)
     V0, W0 = restated.random_init(m, n, r, 0)
