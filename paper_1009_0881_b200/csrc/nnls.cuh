@@ -48,18 +48,20 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
   // issue-bound (ncu: 62 % issue-active, ~42k warp instructions per
   // subproblem), and 64-bit index math plus loop overhead were most of the
   // inner loops' instructions.  The subtraction order is unchanged.
+  // EXACT: the reference's unfused d - a * b; otherwise one fused multiply-add
+  auto sub = [](double acc, double a, double b) { return EXACT ? msub(acc, a, b) : fma(-a, b, acc); };
   for (int k = 0; k < p; ++k) {
     const double* Lk = L + (unsigned)(k * (k + 1) / 2);
     double d = Lk[k];
     int q = 0;
     for (; q + 4 <= k; q += 4) {
       const double a0 = Lk[q], a1 = Lk[q + 1], a2 = Lk[q + 2], a3 = Lk[q + 3];
-      d = msub(d, a0, a0);
-      d = msub(d, a1, a1);
-      d = msub(d, a2, a2);
-      d = msub(d, a3, a3);
+      d = sub(d, a0, a0);
+      d = sub(d, a1, a1);
+      d = sub(d, a2, a2);
+      d = sub(d, a3, a3);
     }
-    for (; q < k; ++q) d = msub(d, Lk[q], Lk[q]);
+    for (; q < k; ++q) d = sub(d, Lk[q], Lk[q]);
     if (d <= 0.0 || !isfinite(d)) {
       __syncwarp();
       return false;
@@ -71,12 +73,12 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
       double s = Li[k];
       int qq = 0;
       for (; qq + 4 <= k; qq += 4) {
-        s = msub(s, Li[qq], Lk[qq]);
-        s = msub(s, Li[qq + 1], Lk[qq + 1]);
-        s = msub(s, Li[qq + 2], Lk[qq + 2]);
-        s = msub(s, Li[qq + 3], Lk[qq + 3]);
+        s = sub(s, Li[qq], Lk[qq]);
+        s = sub(s, Li[qq + 1], Lk[qq + 1]);
+        s = sub(s, Li[qq + 2], Lk[qq + 2]);
+        s = sub(s, Li[qq + 3], Lk[qq + 3]);
       }
-      for (; qq < k; ++qq) s = msub(s, Li[qq], Lk[qq]);
+      for (; qq < k; ++qq) s = sub(s, Li[qq], Lk[qq]);
       Li[k] = EXACT ? s / lkk : s * ilkk;
     }
     __syncwarp();
@@ -94,7 +96,8 @@ __device__ inline void warp_substitute(const double* L, double* b, int p, int la
     const double bq = EXACT ? b[q] / L[rq + q] : b[q] * L[rq + q];  // !EXACT: diagonal holds 1 / L[q][q]
     __syncwarp();
     if (lane == 0) b[q] = bq;
-    for (int i = q + 1 + lane; i < p; i += 32) b[i] = msub(b[i], L[(size_t)i * (i + 1) / 2 + q], bq);
+    for (int i = q + 1 + lane; i < p; i += 32)
+      b[i] = EXACT ? msub(b[i], L[(size_t)i * (i + 1) / 2 + q], bq) : fma(-L[(size_t)i * (i + 1) / 2 + q], bq, b[i]);
     __syncwarp();
   }
   // backward: L^T x = y (solvers.cpp:44-48)
@@ -113,7 +116,7 @@ __device__ inline void warp_substitute(const double* L, double* b, int p, int la
       __syncwarp();
       if (lane == 0) b[q] = bq;
       const size_t rq = (size_t)q * (q + 1) / 2;
-      for (int ii = lane; ii < q; ii += 32) b[ii] = msub(b[ii], L[rq + ii], bq);
+      for (int ii = lane; ii < q; ii += 32) b[ii] = fma(-L[rq + ii], bq, b[ii]);
       __syncwarp();
     }
   }
