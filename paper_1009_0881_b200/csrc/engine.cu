@@ -445,7 +445,9 @@ struct Engine::Impl {
     const size_t blocks = std::min<size_t>(ceil_div(count, 256), 4 * (size_t)sm_count);
     red.ensure(std::max<size_t>(blocks, 1) * 8);
     double* rp = red.as<double>();
-    if (a_is_t) {
+    if (a_is_t && b_kind == 0 && sizeof(T) == 4 && count % 4 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) {
+      launch(k_sq_partial_v4, dim3((unsigned)blocks), dim3(256), 0, (const float4*)a, count / 4, rp);
+    } else if (a_is_t) {
       if (b_kind == 0) launch(k_dot_partial<T, T>, dim3((unsigned)blocks), dim3(256), 0, (const T*)a, (const T*)nullptr, count, rp);
       else launch(k_dot_partial<T, T>, dim3((unsigned)blocks), dim3(256), 0, (const T*)a, (const T*)b, count, rp);
     } else {
