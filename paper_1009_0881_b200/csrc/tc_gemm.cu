@@ -1089,6 +1089,35 @@ __global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S,
   }
 }
 
+// The transposed case (W, r x rows -> S rows x 2 rpa) through a shared-memory
+// tile: 64 columns of W read row by row (coalesced), written as 64 contiguous
+// S rows (coalesced); the element-wise version scattered 4-byte writes at a
+// 2 rpa stride (0.35 ms per error sample at config 4).
+__global__ void __launch_bounds__(256) k_split_rows_t(const float* __restrict__ X, float* __restrict__ S, int r,
+                                                      int rpa, size_t rows) {
+  __shared__ float tile[64][65];  // [k][j], k < rpa <= 64
+  const size_t j0 = (size_t)blockIdx.x * 64;
+  const int t = threadIdx.x, tj = t & 63, tk = t >> 6;  // 4 k-rows per pass
+  for (int k = tk; k < rpa; k += 4) {
+    const size_t j = j0 + tj;
+    tile[k][tj] = (k < r && j < rows) ? X[(size_t)k * rows + j] : 0.f;
+  }
+  __syncthreads();
+  // each warp writes whole S rows: lanes over k (hi then lo)
+  const int warp = t >> 5, lane = t & 31;
+  for (int jj = warp; jj < 64; jj += 8) {
+    const size_t j = j0 + jj;
+    if (j >= rows) break;
+    float* row = S + j * 2 * (size_t)rpa;
+    for (int k = lane; k < rpa; k += 32) {
+      const float x = tile[k][jj];
+      const float hi = __uint_as_float(tf32_rna(x));
+      row[k] = hi;
+      row[rpa + k] = __uint_as_float(tf32_rna(x - hi));
+    }
+  }
+}
+
 struct RParams {
   const float* M;
   const float* wsplit;     // W^T split rows: n x 2 rpa, [hi | lo]
@@ -1429,9 +1458,8 @@ class TcGemmImpl final : public TcGemm {
     ensure(&rw_, &rw_bytes_, (size_t)n * 2 * rpa * 4);
     {
       const unsigned gv = (unsigned)std::min<size_t>(cdiv((size_t)m * rpa, 256), 16384);
-      const unsigned gw = (unsigned)std::min<size_t>(cdiv((size_t)n * rpa, 256), 16384);
       tc::k_split_rows<<<gv, 256, 0, s>>>(V, static_cast<float*>(rv_), (int)r, rpa, m, 0);
-      tc::k_split_rows<<<gw, 256, 0, s>>>(W, static_cast<float*>(rw_), (int)r, rpa, n, 1);
+      tc::k_split_rows_t<<<(unsigned)cdiv(n, 64), 256, 0, s>>>(W, static_cast<float*>(rw_), (int)r, rpa, n);
       TC_CK(cudaGetLastError());
       *launches += 2;
     }
