@@ -213,6 +213,27 @@ int mlnmf_session_tc_active(mlnmf_session* s);
 int mlnmf_session_gram_error(mlnmf_session* s);
 
 /* ---------------------------------------------------------------------------
+ * Dataset and result I/O (proj/include/mlnmf/io.hpp), host only; the same code
+ * and byte formats as the mlnmf_b200 CLI.  Errors: MLNMF_ERR_DATA with the
+ * reference's message texts (file name, byte offset / row / column).
+ * ------------------------------------------------------------------------- */
+/* load_pgm_dir (io.hpp:46-48, io.cpp:118-144): every P5 file of `dir` in
+ * byte-wise filename order as one column; *M_out (m x n, row-major, pixel
+ * (i,j) of an h x w image at row j*h + i) is released with mlnmf_free */
+int mlnmf_load_pgm_dir(const char* dir, double** M_out, size_t* m, size_t* n, size_t* h, size_t* w);
+/* load_csv (io.hpp:50-51, io.cpp:146-187) */
+int mlnmf_load_csv(const char* path, double** M_out, size_t* m, size_t* n);
+/* save_matrix_csv / save_trace_csv (io.hpp:53-58): %.17g, header
+ * "elapsed_s,work_units,level,error" for traces */
+int mlnmf_save_matrix_csv(const double* A, size_t rows, size_t cols, const char* path);
+int mlnmf_save_trace_csv(const mlnmf_trace* t, const char* path);
+/* save_basis_mosaic (io.hpp:60-63): basis_kkk.pgm per column of V + mosaic.pgm */
+int mlnmf_save_basis_mosaic(const double* V, size_t m, size_t r, size_t grid_h, size_t grid_w, const char* dir);
+/* synth_smooth_dataset (io.hpp:69-75): M_out is (h*w) x n, caller-allocated */
+int mlnmf_synth_smooth_dataset(size_t h, size_t w, size_t n, size_t blobs, uint64_t seed, double* M_out);
+void mlnmf_free(void* p);
+
+/* ---------------------------------------------------------------------------
  * Traces: RunTrace (proj/include/mlnmf/solvers.hpp:14-35).
  * ------------------------------------------------------------------------- */
 size_t mlnmf_trace_num_samples(const mlnmf_trace* t);

@@ -237,6 +237,14 @@ _proto("mlnmf_trace_degenerate", C.c_int, _vp)
 _proto("mlnmf_trace_num_phases", _sz, _vp)
 _proto("mlnmf_trace_phases", None, _vp, _ip, _lp)
 _proto("mlnmf_trace_free", None, _vp)
+_proto("mlnmf_session_comm_time", C.c_int, _vp, _dp, _lp)
+_proto("mlnmf_load_pgm_dir", C.c_int, C.c_char_p, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz),
+       C.POINTER(_sz))
+_proto("mlnmf_load_csv", C.c_int, C.c_char_p, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz))
+_proto("mlnmf_save_matrix_csv", C.c_int, _dp, _sz, _sz, C.c_char_p)
+_proto("mlnmf_save_basis_mosaic", C.c_int, _dp, _sz, _sz, _sz, _sz, C.c_char_p)
+_proto("mlnmf_synth_smooth_dataset", C.c_int, _sz, _sz, _sz, _sz, C.c_uint64, _dp)
+_proto("mlnmf_free", None, _vp)
 
 EXPORTED_SYMBOLS = sorted(n for n in dir(_lib) if n.startswith("mlnmf_"))
 
@@ -848,3 +856,68 @@ class Session:
     @property
     def gram_error(self) -> bool:
         return bool(_lib.mlnmf_session_gram_error(self._h))
+
+
+# ---------------------------------------------------------------------------
+# dataset / result I/O (proj/include/mlnmf/io.hpp) -- host code in the library
+# (csrc/host_io.cpp), the same formats as the mlnmf_b200 CLI
+# ---------------------------------------------------------------------------
+@dataclass
+class Dataset:
+    """mlnmf::Dataset (io.hpp:16-21): one column per image; grid None for CSV."""
+    matrix: np.ndarray
+    grid: Optional[ImageGrid]
+    name: str
+
+
+def _take_matrix(ptr, m, n):
+    try:
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(m, n)).copy() if m * n else \
+            np.zeros((m, n))
+    finally:
+        _lib.mlnmf_free(ptr)
+
+
+def load_pgm_dir(path) -> Dataset:
+    """load_pgm_dir (io.hpp:46-48): every P5 image in byte-wise filename order."""
+    ptr, m, n, h, w = C.c_void_p(), C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+    _check(_lib.mlnmf_load_pgm_dir(os.fsencode(str(path)), C.byref(ptr), C.byref(m), C.byref(n), C.byref(h),
+                                   C.byref(w)))
+    M = _take_matrix(ptr, m.value, n.value)
+    return Dataset(M, ImageGrid(h.value, w.value), os.path.basename(os.path.normpath(str(path))))
+
+
+def load_csv(path) -> Dataset:
+    """load_csv (io.hpp:50-51): rectangular nonnegative CSV, no header."""
+    ptr, m, n = C.c_void_p(), C.c_size_t(), C.c_size_t()
+    _check(_lib.mlnmf_load_csv(os.fsencode(str(path)), C.byref(ptr), C.byref(m), C.byref(n)))
+    return Dataset(_take_matrix(ptr, m.value, n.value), None, os.path.splitext(os.path.basename(str(path)))[0])
+
+
+def save_matrix_csv(M, path):
+    """save_matrix_csv (io.hpp:53): one row per line, %.17g."""
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    _check(_lib.mlnmf_save_matrix_csv(_d(M), M.shape[0], M.shape[1], os.fsencode(str(path))))
+
+
+def save_trace_csv(trace: RunTrace, path):
+    """save_trace_csv (io.hpp:55-57): header elapsed_s,work_units,level,error,
+    %.17g values (the same bytes as the C writer)."""
+    with open(path, "w") as f:
+        f.write("elapsed_s,work_units,level,error\n")
+        for a, b, c, d in zip(trace.elapsed_s, trace.work_units, trace.level, trace.error):
+            f.write("%.17g,%.17g,%d,%.17g\n" % (a, b, c, d))
+
+
+def save_basis_mosaic(V, grid: ImageGrid, path):
+    """save_basis_mosaic (io.hpp:60-63): basis_kkk.pgm per column + mosaic.pgm."""
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    _check(_lib.mlnmf_save_basis_mosaic(_d(V), V.shape[0], V.shape[1], grid.height, grid.width,
+                                        os.fsencode(str(path))))
+
+
+def synth_smooth_dataset(height: int, width: int, n: int, blobs: int, seed: int) -> Dataset:
+    """synth_smooth_dataset (io.hpp:69-75): the reference's seeded PGM image set."""
+    M = np.empty((height * width, n))
+    _check(_lib.mlnmf_synth_smooth_dataset(height, width, n, blobs, C.c_uint64(seed), _d(M)))
+    return Dataset(M, ImageGrid(height, width), "synth")

@@ -1,6 +1,7 @@
 // capi.cpp -- the extern "C" boundary (include/mlnmf_b200.h) over the device
 // Engine and the host scheduler.  C++ exceptions become status codes with a
 // per-thread message, mirroring the reference's exception classes.
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -13,6 +14,7 @@
 
 #include "../../include/mlnmf_b200.h"
 #include "engine.hpp"
+#include "host_io.hpp"
 #include "nccl_shim.hpp"
 #include "scheduler.hpp"
 
@@ -40,6 +42,9 @@ int guard(F&& f) {
     g_err = ex.what();
     return MLNMF_ERR_NNLS_CAP;
   } catch (const DataError& ex) {
+    g_err = ex.what();
+    return MLNMF_ERR_DATA;
+  } catch (const io::DataError& ex) {  // dataset / result I/O (host_io.cpp)
     g_err = ex.what();
     return MLNMF_ERR_DATA;
   } catch (const std::invalid_argument& ex) {
@@ -502,5 +507,67 @@ void mlnmf_trace_phases(const mlnmf_trace* t, int* level, long* steps) {
   }
 }
 void mlnmf_trace_free(mlnmf_trace* t) { delete t; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Dataset / result I/O (proj/include/mlnmf/io.hpp) over host_io.cpp: the same
+// PGM / CSV ingestion and byte-compatible writers the CLI uses.  Buffers the
+// library allocates are released with mlnmf_free.
+// ---------------------------------------------------------------------------
+namespace {
+double* export_matrix(const io::Dense& d) {
+  double* p = static_cast<double*>(std::malloc(d.v.size() * sizeof(double)));
+  if (!p) throw std::runtime_error("out of host memory");
+  std::memcpy(p, d.v.data(), d.v.size() * sizeof(double));
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+
+void mlnmf_free(void* p) { std::free(p); }
+
+int mlnmf_load_pgm_dir(const char* dir, double** M_out, size_t* m, size_t* n, size_t* h, size_t* w) {
+  return guard([&] {
+    const mlb::io::Dataset d = mlb::io::load_pgm_dir(dir ? dir : "");
+    *m = d.M.rows, *n = d.M.cols, *h = d.grid.h, *w = d.grid.w;
+    *M_out = export_matrix(d.M);
+  });
+}
+
+int mlnmf_load_csv(const char* path, double** M_out, size_t* m, size_t* n) {
+  return guard([&] {
+    const mlb::io::Dataset d = mlb::io::load_csv(path ? path : "");
+    *m = d.M.rows, *n = d.M.cols;
+    *M_out = export_matrix(d.M);
+  });
+}
+
+int mlnmf_save_matrix_csv(const double* A, size_t rows, size_t cols, const char* path) {
+  return guard([&] { mlb::io::save_matrix_csv(A, rows, cols, path ? path : ""); });
+}
+
+int mlnmf_save_trace_csv(const mlnmf_trace* t, const char* path) {
+  return guard([&] {
+    if (!t) throw std::invalid_argument("save_trace_csv: null trace");
+    std::vector<mlb::io::Sample> s;
+    s.reserve(t->t.samples.size());
+    for (const auto& x : t->t.samples) s.push_back({x.elapsed_s, x.work_units, x.level, x.error});
+    mlb::io::save_trace_csv(s, path ? path : "");
+  });
+}
+
+int mlnmf_save_basis_mosaic(const double* V, size_t m, size_t r, size_t grid_h, size_t grid_w, const char* dir) {
+  return guard([&] { mlb::io::save_basis_mosaic(V, m, r, mlb::io::Grid{grid_h, grid_w}, dir ? dir : ""); });
+}
+
+int mlnmf_synth_smooth_dataset(size_t h, size_t w, size_t n, size_t blobs, uint64_t seed, double* M_out) {
+  return guard([&] {
+    const mlb::io::Dataset d = mlb::io::synth_smooth_dataset(h, w, n, blobs, seed);
+    std::memcpy(M_out, d.M.v.data(), d.M.v.size() * sizeof(double));
+  });
+}
 
 }  // extern "C"
