@@ -411,14 +411,45 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc, uint32_t id_full, ui
       : "memory")
 // PAIR: the same 12 MMAs as one CTA-pair instruction stream (cta_group::2,
 // M = 256: A from each CTA's own TMEM slot, B rows split r_pad / 2 per CTA)
+// timing experiment (wrong results): MLB_TC_EXP_TERMS = 2 drops the A_lo F_hi
+// MMAs, 1 also the A_hi F_lo ones -- the speed a split with fewer MMA passes
+// per chunk could reach
+#define MLB_ISSUE_N(CG, NT)                                                                             \
+  asm volatile(                                                                                       \
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"                                                      \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                               \
+      "setp.eq.u32 p, %8, 0;\n\t"                                                                     \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%1], %2, %7, p;\n\t"                        \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%9], %3, %7, 1;\n\t"                        \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%10], %4, %7, 1;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%11], %5, %7, 1;\n\t" NT "}" ::"r"(d),     \
+      "r"(a_hi), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "r"(id), "r"(first),      \
+      "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24), "l"(bd_lo + 2), "l"(bd_lo + 4), "l"(bd_lo + 6)    \
+      : "memory")
+#define MLB_HI_LO_TERM                                                                                 \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %6, %7, 1;\n\t"                                  \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %12, %7, 1;\n\t"                                 \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], %13, %7, 1;\n\t"                                \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], %14, %7, 1;\n\t"
+#ifndef MLB_TC_EXP_TERMS
+#define MLB_TC_EXP_TERMS 3
+#endif
 template <int S, int ACC, bool PAIR = false>
 __device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first) {
   constexpr uint32_t d = ACC * kAccStride;
   constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
+#if MLB_TC_EXP_TERMS == 3
   if constexpr (PAIR)
     MLB_ISSUE3("2");
   else
     MLB_ISSUE3("1");
+#elif MLB_TC_EXP_TERMS == 2
+  (void)a_lo;
+  MLB_ISSUE_N("1", MLB_HI_LO_TERM);
+#else
+  (void)a_lo;
+  MLB_ISSUE_N("1", "");
+#endif
 }
 
 // Optional event trace of CTA 0 (build with -DMLB_TC_TRACE=1; tools/tc_trace.py).

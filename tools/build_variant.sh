@@ -11,6 +11,7 @@ NCCL_INC=$(python -c 'import nvidia.nccl as n, os; print(os.path.join(list(n.__p
 L=$REPO/paper_1009_0881_b200/_lib
 nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -O3 \
   -I"$NCCL_INC" -I"$REPO/include" --expt-relaxed-constexpr "$@" -x cu -c "$REPO/paper_1009_0881_b200/csrc/tc_gemm.cu" -o "$OUT/tc_gemm.cu.o"
+OBJS=$(ls "$L"/*.o | grep -v '/tc_gemm.cu.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$OUT/libmlnmf_b200.so" \
-  "$L/engine.cu.o" "$OUT/tc_gemm.cu.o" "$L/hals_reg.cu.o" "$L/scheduler.cpp.o" "$L/capi.cpp.o" -ldl -lpthread -lrt
+  $OBJS "$OUT/tc_gemm.cu.o" -ldl -lpthread -lrt
 echo "$OUT/libmlnmf_b200.so"
