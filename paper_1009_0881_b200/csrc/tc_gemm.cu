@@ -37,6 +37,7 @@
 //   warps 11-18: epilogue (lane quarter x column half), drains all windows
 //   warp 19: TMA producer (factor slices, one thread, stream order)
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -431,13 +432,44 @@ __device__ __forceinline__ void issue_chunk(uint64_t bdesc, uint32_t id_full, ui
   "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %12, %7, 1;\n\t"                                 \
   "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], %13, %7, 1;\n\t"                                \
   "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], %14, %7, 1;\n\t"
+// MIXED: the two 3xTF32 cross terms A_lo F_hi + A_hi F_lo (each ~2^-11 of the
+// result, so ~2^-11 relative accuracy suffices) as ONE K = 64 bf16 product
+// [A_lo | A_hi] . [F_hi ; F_lo]: 4 kind::f16 MMAs (K = 16) instead of 8
+// kind::tf32 ones (K = 8), next to the 4 tf32 MMAs of A_hi F_hi.  Same TMEM
+// slot and factor-slice bytes: the converters store bf16 pairs in the lo
+// half of the slot, k_split_factor writes the F_lo rows as bf16 [F_hi | F_lo]
+// per 32-wide chunk (the same 128 bytes per row the TMA box fetches).
+// Selected per launch (K % 32 == 0, no CTA pairs); MLB_TC_MIXED=0 disables it.
+__host__ __device__ constexpr uint32_t idesc_bf16(int N, int M = 128) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 #ifndef MLB_TC_EXP_TERMS
 #define MLB_TC_EXP_TERMS 3
 #endif
-template <int S, int ACC, bool PAIR = false>
-__device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first) {
+template <int S, int ACC, bool PAIR = false, bool MIXED = false>
+__device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first,
+                                             uint32_t idx = 0) {
   constexpr uint32_t d = ACC * kAccStride;
   constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
+  if constexpr (MIXED) {  // idx: the bf16 instruction descriptor (N = r_pad)
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.u32 p, %12, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %4, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %5, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %6, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %7, %19, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%16], %8, %19, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%17], %9, %19, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%18], %10, %19, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2),
+      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24),
+      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24), "r"(idx)
+      : "memory");
+  return;
+  }
 #if MLB_TC_EXP_TERMS == 3
   if constexpr (PAIR)
     MLB_ISSUE3("2");
@@ -541,12 +573,13 @@ __device__ __forceinline__ int unit_chunk(const Params& p, const Unit& x, int i)
 // single issuing warp stalls inside the MMAs and its per-chunk waits and
 // commits leave the pipe idle; with two, one warp's bookkeeping overlaps the
 // other's MMAs.
-template <int W, bool PAIR>
+template <int W, bool PAIR, bool MIXED>
 __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u0, int ustep, bool issue,
                                          uint64_t bdesc0, uint64_t* ready,
                                          uint64_t* sdone, uint64_t* bfull, uint64_t* bempty, uint64_t* afull,
                                          uint64_t* aempty) {
   const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp, PAIR ? 256 : 128);
+  const uint32_t id_x = idesc_bf16(p.rp);  // MIXED cross terms
   int g = 0;
   int wc = 0;  // windows this warp has opened (all units): buffer wc % kAccBufs
   int lastph[kSlots / 2];    // parity of the last commit on this warp's slots W, W + 2, ...
@@ -590,13 +623,13 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
         const int sidx = slot >> 1;  // this warp's slots are W, W + 2, ...
 #ifndef MLB_TC_EXP_NOMMA  // timing experiment: no MMAs (wrong results)
         if (abuf == 0) {
-          if (sidx == 0) issue_chunk3<W, A0, PAIR>(bd, bd_lo, id_hi, first);
-          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0, PAIR>(bd, bd_lo, id_hi, first);
-          else issue_chunk3<(W + 4) % kSlots, A0, PAIR>(bd, bd_lo, id_hi, first);
+          if (sidx == 0) issue_chunk3<W, A0, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A0, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
+          else issue_chunk3<(W + 4) % kSlots, A0, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
         } else {
-          if (sidx == 0) issue_chunk3<W, A1, PAIR>(bd, bd_lo, id_hi, first);
-          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
-          else issue_chunk3<(W + 4) % kSlots, A1, PAIR>(bd, bd_lo, id_hi, first);
+          if (sidx == 0) issue_chunk3<W, A1, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
+          else if (sidx == 1) issue_chunk3<(W + 2) % kSlots, A1, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
+          else issue_chunk3<(W + 4) % kSlots, A1, PAIR, MIXED>(bd, bd_lo, id_hi, first, id_x);
         }
 #else
         (void)sidx, (void)bd_lo;
@@ -642,7 +675,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
 // multicast to both CTAs' barriers, and the peer's converters / epilogue
 // arrive on the leader's barriers.  Per SM this halves the factor-slice
 // traffic (TMA and MMA reads of shared memory) and the MMA issue work.
-template <bool TRANS, bool PAIR>
+template <bool TRANS, bool PAIR, bool MIXED>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_product(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_b,
                  const Params p) {
@@ -826,9 +859,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
     const bool issue = !PAIR || crank == 0;  // in a pair only the leader issues
     if (warp == kWarpMma0)
-      mma_role<0, PAIR>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
+      mma_role<0, PAIR, MIXED>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
     else
-      mma_role<1, PAIR>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
+      mma_role<1, PAIR, MIXED>(p, total_units, u0, ustep, issue, bdesc0, ready, sdone, bfull, bempty, afull, aempty);
   } else if (warp < kWarpEpi0) {
     // ======================= converters: fp32 -> tf32 hi/lo into TMEM =======================
     // kConvGroups groups of 4 warps take alternate chunks (more chunks in
@@ -882,9 +915,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // round-to-nearest-away == cvt.rna.tf32)
         uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          hi[k] = (__float_as_uint(x[k]) + 0x1000u) & 0xFFFFE000u;
-          lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
+        for (int k = 0; k < 32; ++k) hi[k] = (__float_as_uint(x[k]) + 0x1000u) & 0xFFFFE000u;
+        if (MIXED) {
+          // lo half of the slot: bf16 pairs [x - hi (32) | hi (32)], element 2j in the low 16 bits
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * j] - __uint_as_float(hi[2 * j]),
+                                                            x[2 * j + 1] - __uint_as_float(hi[2 * j + 1]));
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(hi[2 * j]), __uint_as_float(hi[2 * j + 1]));
+            lo[j] = *reinterpret_cast<const uint32_t*>(&l2);
+            lo[16 + j] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
         }
         // The slice was read through the generic proxy and the refill is an
         // async-proxy (TMA) write: order the two before releasing the stage
@@ -1003,6 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // F (rows x ld, row-major, rows <= r) -> S (2 rp x K): S[k] = rna(F[k]),
 // S[rp + k] = rna(F[k] - S[k]); padding rows zero.  trans: F is K x r
 // (V, row-major) and row k of S is column k of F.
+template <bool MIXED>
 __global__ void k_split_factor(const float* __restrict__ F, float* __restrict__ S, int r, int rp, size_t K,
                                int trans) {
   const size_t total = (size_t)rp * K;
@@ -1016,7 +1062,16 @@ __global__ void k_split_factor(const float* __restrict__ F, float* __restrict__ 
       lo = __uint_as_float(tf32_rna(x - hi));
     }
     S[k * K + j] = hi;
-    S[((size_t)rp + k) * K + j] = lo;
+    if (MIXED) {
+      // row k of the lo region as bf16 [F_hi (32) | F_lo (32)] per 32-wide chunk:
+      // the same 128 bytes per row that fp32 columns [32c, 32c + 32) occupy
+      __nv_bfloat16* Sx = reinterpret_cast<__nv_bfloat16*>(S + ((size_t)rp + k) * K);
+      const size_t c = j / 32, t = j % 32;
+      Sx[64 * c + t] = __float2bfloat16_rn(hi);
+      Sx[64 * c + 32 + t] = __float2bfloat16_rn(lo);
+    } else {
+      S[((size_t)rp + k) * K + j] = lo;
+    }
   }
 }
 
@@ -1534,16 +1589,20 @@ class TcGemmImpl final : public TcGemm {
     const size_t rows = TRANS ? n : m;     // MMA-M extent
     // split factor F -> [F_hi ; F_lo] (2 rp x K)
     ensure(&split_, &split_bytes_, (size_t)2 * rp * K * 4);
+    const bool mixed = mixed_ && K % tc::kChunk == 0 && !(pair_ && (rp == 32 || rp == 64) && cdiv(rows, 256) >= 8);
     {
       const size_t tot = (size_t)rp * K;
       const unsigned g = (unsigned)std::min<size_t>(cdiv(tot, 256), 16384);
-      tc::k_split_factor<<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
+      if (mixed)
+        tc::k_split_factor<true><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
+      else
+        tc::k_split_factor<false><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
       TC_CK(cudaGetLastError());
       ++*launches;
     }
     // CTA pairs (cta_group::2, 256-row tiles): r_pad in {32, 64} (N split in
     // halves of >= 16 rows), an even SM count, enough tiles to fill the pairs
-    const bool pair = tc::kK3 && pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
+    const bool pair = tc::kK3 && !mixed && pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
     const int slots = pair ? sms_ / 2 : sms_;  // persistent schedulers: pairs or CTAs
     tc::Params p{};
     p.rows = (int)rows;
@@ -1606,8 +1665,9 @@ class TcGemmImpl final : public TcGemm {
     // of a pair its rp / 2 rows of each half (two boxes)
     const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, pair ? rp / 2 : 2 * rp, true);
     const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
-    auto kern = pair ? tc::k_tc_product<TRANS, true> : tc::k_tc_product<TRANS, false>;
-    const int ak = (TRANS ? 1 : 0) + (pair ? 2 : 0);
+    auto kern = pair ? tc::k_tc_product<TRANS, true, false>
+                : mixed ? tc::k_tc_product<TRANS, false, true> : tc::k_tc_product<TRANS, false, false>;
+    const int ak = (TRANS ? 1 : 0) + (pair ? 2 : 0) + (mixed ? 4 : 0);
     if (!attr_set_[ak]) {
       TC_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set_[ak] = true;
@@ -1668,7 +1728,12 @@ class TcGemmImpl final : public TcGemm {
   size_t split_bytes_ = 0;
   void* part_ = nullptr;
   size_t part_bytes_ = 0;
-  bool attr_set_[4] = {false, false, false, false};
+  bool attr_set_[8] = {false, false, false, false, false, false, false, false};
+  // bf16 cross terms (MLB_TC_MIXED=0 keeps all three terms in tf32)
+  bool mixed_ = [] {
+    const char* e = getenv("MLB_TC_MIXED");
+    return e == nullptr || atoi(e) != 0;
+  }();
   // CTA-pair products (MLB_TC_PAIR=1 to enable; see k_tc_product)
   bool pair_ = [] {
     const char* e = getenv("MLB_TC_PAIR");
