@@ -1157,21 +1157,38 @@ constexpr int kRMBytes = 64 * 128 * 4;   // M tile: 64 rows i x 128 columns j
 
 // X -> S (rows x 2 rpa): [rna(x) | rna(x - rna(x))], zero padded.  trans: X is
 // r x rows (W, row-major) and row j of S comes from column j of X.
-__global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S, int r, int rpa, size_t rows,
-                             int trans) {
+// MIXED (the residual's bf16 cross terms): the lo half of each S row holds
+// bf16 [hi | lo] (V, the B operand) or [lo | hi] (W^T, the A operand) packed
+// in the same rpa 32-bit words, so [W_lo | W_hi] . [V_hi ; V_lo] is one K = 2
+// rpa bf16 product.
+// (the bf16 halves are r_pad long -- the K extent the MMAs cover -- so the
+// pair is [x (rp) | y (rp)] within the 2 rpa bf16 slots; k >= rp is padding)
+__device__ __forceinline__ void put_split(float* row, int rpa, int rp, int k, float x, bool mixed, bool lo_first) {
+  const float hi = __uint_as_float(tf32_rna(x));
+  row[k] = hi;
+  if (mixed) {
+    __nv_bfloat16* bx = reinterpret_cast<__nv_bfloat16*>(row + rpa);
+    const __nv_bfloat16 bh = __float2bfloat16_rn(hi), bl = __float2bfloat16_rn(x - hi);
+    if (k < rp) {
+      bx[k] = lo_first ? bl : bh;
+      bx[rp + k] = lo_first ? bh : bl;
+    } else if (rp + k < 2 * rpa) {
+      bx[rp + k] = __float2bfloat16_rn(0.f);  // zero the tail beyond 2 rp
+    }
+  } else {
+    row[rpa + k] = __uint_as_float(tf32_rna(x - hi));
+  }
+}
+
+__global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S, int r, int rpa, int rp,
+                             size_t rows, int trans, int mixed) {
   const size_t total = (size_t)rows * rpa;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     size_t j, k;
     if (trans) k = e / rows, j = e % rows;  // coalesced reads of W rows
     else j = e / rpa, k = e % rpa;
-    float hi = 0.f, lo = 0.f;
-    if ((int)k < r) {
-      const float x = trans ? X[k * rows + j] : X[j * r + k];
-      hi = __uint_as_float(tf32_rna(x));
-      lo = __uint_as_float(tf32_rna(x - hi));
-    }
-    S[j * 2 * rpa + k] = hi;
-    S[j * 2 * rpa + rpa + k] = lo;
+    const float x = (int)k < r ? (trans ? X[k * rows + j] : X[j * r + k]) : 0.f;
+    put_split(S + j * 2 * rpa, rpa, rp, (int)k, x, mixed != 0, trans != 0);
   }
 }
 
@@ -1180,7 +1197,7 @@ __global__ void k_split_rows(const float* __restrict__ X, float* __restrict__ S,
 // S rows (coalesced); the element-wise version scattered 4-byte writes at a
 // 2 rpa stride (0.35 ms per error sample at config 4).
 __global__ void __launch_bounds__(256) k_split_rows_t(const float* __restrict__ X, float* __restrict__ S, int r,
-                                                      int rpa, size_t rows) {
+                                                      int rpa, int rp, size_t rows, int mixed) {
   __shared__ float tile[64][65];  // [k][j], k < rpa <= 64
   const size_t j0 = (size_t)blockIdx.x * 64;
   const int t = threadIdx.x, tj = t & 63, tk = t >> 6;  // 4 k-rows per pass
@@ -1195,12 +1212,7 @@ __global__ void __launch_bounds__(256) k_split_rows_t(const float* __restrict__ 
     const size_t j = j0 + jj;
     if (j >= rows) break;
     float* row = S + j * 2 * (size_t)rpa;
-    for (int k = lane; k < rpa; k += 32) {
-      const float x = tile[k][jj];
-      const float hi = __uint_as_float(tf32_rna(x));
-      row[k] = hi;
-      row[rpa + k] = __uint_as_float(tf32_rna(x - hi));
-    }
+    for (int k = lane; k < rpa; k += 32) put_split(row, rpa, rp, k, tile[k][jj], mixed != 0, true);
   }
 }
 
@@ -1214,20 +1226,35 @@ struct RParams {
 
 // The MMAs of one tile: K = KS x 8 (KS = 0: runtime p.rp / 8), A = TMEM
 // columns [ta, ta + rpa) (hi) and [ta + rpa, ...) (lo), B = the V stage.
-template <int KS>
+__device__ __forceinline__ void mma_ts_bf16(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+template <int KS, bool MIXED>
 __device__ __forceinline__ void res_tile_mmas(uint32_t d, uint32_t ta, int rpa, uint64_t dbs, uint64_t lo_b,
-                                              uint32_t id, int ks_rt) {
+                                              uint32_t id, uint32_t idx, int ks_rt) {
   const int ksteps = KS > 0 ? KS : ks_rt;
 #pragma unroll
   for (int kk = 0; kk < (KS > 0 ? KS : 16); ++kk) {
     if (KS == 0 && kk >= ksteps) break;
     const uint64_t ob = (uint64_t)(((kk >> 2) * (kRAtomBytes / 2) + (kk & 3) * 32) >> 4);
     mma_ts(d, ta + kk * 8, dbs + ob, id, kk > 0 ? 1u : 0u);  // W_hi V_hi
-    mma_ts(d, ta + kk * 8, dbs + lo_b + ob, id, 1u);         // W_hi V_lo
-    mma_ts(d, ta + rpa + kk * 8, dbs + ob, id, 1u);          // W_lo V_hi
+    if (MIXED) {
+      // K = 16 bf16 of [W_lo | W_hi] . [V_hi ; V_lo] (the same 32-byte step)
+      mma_ts_bf16(d, ta + rpa + kk * 8, dbs + lo_b + ob, idx, 1u);
+    } else {
+      mma_ts(d, ta + kk * 8, dbs + lo_b + ob, id, 1u);  // W_hi V_lo
+      mma_ts(d, ta + rpa + kk * 8, dbs + ob, id, 1u);   // W_lo V_hi
+    }
   }
 }
 
+template <bool MIXED>
 __global__ void __launch_bounds__(kRThreads, 1)
     k_tc_residual(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_m,
                   const RParams p) {
@@ -1348,9 +1375,9 @@ __global__ void __launch_bounds__(kRThreads, 1)
         const uint32_t d = (uint32_t)(sa * 64);
         const uint64_t dbs = ds + (uint64_t)((sv * opb) >> 4);
         if (ks_rt == 8)
-          res_tile_mmas<8>(d, ta, rpa, dbs, lo_b, id, ks_rt);
+          res_tile_mmas<8, MIXED>(d, ta, rpa, dbs, lo_b, id, idesc_bf16(64), ks_rt);
         else
-          res_tile_mmas<0>(d, ta, rpa, dbs, lo_b, id, ks_rt);
+          res_tile_mmas<0, MIXED>(d, ta, rpa, dbs, lo_b, id, idesc_bf16(64), ks_rt);
         tc_commit(smem_u32(&vempty[sv]));  // V slice free (the M tile is released by the epilogue)
         tc_commit(smem_u32(&cfull[sa]));
         lastv[sv] = (int)vph;
@@ -1544,8 +1571,9 @@ class TcGemmImpl final : public TcGemm {
     ensure(&rw_, &rw_bytes_, (size_t)n * 2 * rpa * 4);
     {
       const unsigned gv = (unsigned)std::min<size_t>(cdiv((size_t)m * rpa, 256), 16384);
-      tc::k_split_rows<<<gv, 256, 0, s>>>(V, static_cast<float*>(rv_), (int)r, rpa, m, 0);
-      tc::k_split_rows_t<<<(unsigned)cdiv(n, 64), 256, 0, s>>>(W, static_cast<float*>(rw_), (int)r, rpa, n);
+      tc::k_split_rows<<<gv, 256, 0, s>>>(V, static_cast<float*>(rv_), (int)r, rpa, rp, m, 0, mixed_ ? 1 : 0);
+      tc::k_split_rows_t<<<(unsigned)cdiv(n, 64), 256, 0, s>>>(W, static_cast<float*>(rw_), (int)r, rpa, rp, n,
+                                                               mixed_ ? 1 : 0);
       TC_CK(cudaGetLastError());
       *launches += 2;
     }
@@ -1569,10 +1597,14 @@ class TcGemmImpl final : public TcGemm {
     const size_t smem = 1024 + (size_t)tc::kRVS * p.atoms * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
     if (!resid_attr_) {
       const size_t smax = 1024 + (size_t)tc::kRVS * 2 * tc::kRAtomBytes + tc::kRMS * tc::kRMBytes + 256;
-      TC_CK(cudaFuncSetAttribute(tc::k_tc_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      TC_CK(cudaFuncSetAttribute(tc::k_tc_residual<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      TC_CK(cudaFuncSetAttribute(tc::k_tc_residual<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
       resid_attr_ = true;
     }
-    tc::k_tc_residual<<<grid, tc::kRThreads, smem, s>>>(mv, mm, p);
+    if (mixed_)
+      tc::k_tc_residual<true><<<grid, tc::kRThreads, smem, s>>>(mv, mm, p);
+    else
+      tc::k_tc_residual<false><<<grid, tc::kRThreads, smem, s>>>(mv, mm, p);
     TC_CK(cudaGetLastError());
     tc::k_sum_parts<<<1, 256, 0, s>>>(static_cast<const double*>(part_), grid, out);
     TC_CK(cudaGetLastError());
