@@ -1048,29 +1048,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 // F (rows x ld, row-major, rows <= r) -> S (2 rp x K): S[k] = rna(F[k]),
 // S[rp + k] = rna(F[k] - S[k]); padding rows zero.  trans: F is K x r
 // (V, row-major) and row k of S is column k of F.
+// S rows have pitch Kp = K rounded up to whole 32-wide chunks (zero tail), so
+// the last chunk's bf16 [F_hi | F_lo] block stays inside its row.
 template <bool MIXED>
 __global__ void k_split_factor(const float* __restrict__ F, float* __restrict__ S, int r, int rp, size_t K,
-                               int trans) {
-  const size_t total = (size_t)rp * K;
+                               size_t Kp, int trans) {
+  const size_t total = (size_t)rp * Kp;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    const size_t k = e / K, j = e % K;
+    const size_t k = e / Kp, j = e % Kp;
     float hi = 0.f, lo = 0.f;
-    if ((int)k < r) {
+    if ((int)k < r && j < K) {
       const float x = trans ? F[j * r + k] : F[k * K + j];
       const uint32_t h = tf32_rna(x);
       hi = __uint_as_float(h);
       lo = __uint_as_float(tf32_rna(x - hi));
     }
-    S[k * K + j] = hi;
+    S[k * Kp + j] = hi;
     if (MIXED) {
       // row k of the lo region as bf16 [F_hi (32) | F_lo (32)] per 32-wide chunk:
       // the same 128 bytes per row that fp32 columns [32c, 32c + 32) occupy
-      __nv_bfloat16* Sx = reinterpret_cast<__nv_bfloat16*>(S + ((size_t)rp + k) * K);
+      __nv_bfloat16* Sx = reinterpret_cast<__nv_bfloat16*>(S + ((size_t)rp + k) * Kp);
       const size_t c = j / 32, t = j % 32;
       Sx[64 * c + t] = __float2bfloat16_rn(hi);
       Sx[64 * c + 32 + t] = __float2bfloat16_rn(lo);
     } else {
-      S[((size_t)rp + k) * K + j] = lo;
+      S[((size_t)rp + k) * Kp + j] = lo;
     }
   }
 }
@@ -1620,15 +1622,16 @@ class TcGemmImpl final : public TcGemm {
     const size_t K = TRANS ? m : n;        // contraction
     const size_t rows = TRANS ? n : m;     // MMA-M extent
     // split factor F -> [F_hi ; F_lo] (2 rp x K)
-    ensure(&split_, &split_bytes_, (size_t)2 * rp * K * 4);
-    const bool mixed = mixed_ && K % tc::kChunk == 0 && !(pair_ && (rp == 32 || rp == 64) && cdiv(rows, 256) >= 8);
+    const size_t Kp = cdiv(K, tc::kChunk) * tc::kChunk;  // split row pitch: whole chunks
+    ensure(&split_, &split_bytes_, (size_t)2 * rp * Kp * 4);
+    const bool mixed = mixed_ && !(pair_ && (rp == 32 || rp == 64) && cdiv(rows, 256) >= 8);
     {
       const size_t tot = (size_t)rp * K;
       const unsigned g = (unsigned)std::min<size_t>(cdiv(tot, 256), 16384);
       if (mixed)
-        tc::k_split_factor<true><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
+        tc::k_split_factor<true><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, Kp, TRANS ? 1 : 0);
       else
-        tc::k_split_factor<false><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, TRANS ? 1 : 0);
+        tc::k_split_factor<false><<<g, 256, 0, s>>>(F, static_cast<float*>(split_), (int)r, rp, K, Kp, TRANS ? 1 : 0);
       TC_CK(cudaGetLastError());
       ++*launches;
     }
@@ -1695,7 +1698,7 @@ class TcGemmImpl final : public TcGemm {
                                     : make_map(M, n, m, tc::kChunk, 128, true);
     // factor slices: the whole [F_hi; F_lo] (2 rp rows) per chunk, or per CTA
     // of a pair its rp / 2 rows of each half (two boxes)
-    const CUtensorMap mb = make_map(split_, K, 2 * rp, tc::kChunk, pair ? rp / 2 : 2 * rp, true);
+    const CUtensorMap mb = make_map(split_, Kp, 2 * rp, tc::kChunk, pair ? rp / 2 : 2 * rp, true);
     const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
     auto kern = pair ? tc::k_tc_product<TRANS, true, false>
                 : mixed ? tc::k_tc_product<TRANS, false, true> : tc::k_tc_product<TRANS, false, false>;
