@@ -446,28 +446,33 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int N, int M = 128) {
 #ifndef MLB_TC_EXP_TERMS
 #define MLB_TC_EXP_TERMS 3
 #endif
+#define MLB_ISSUE_MIXED(CG) \
+  asm volatile( \
+      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t" \
+      "elect.sync _|e, 0xffffffff;\n\t" \
+      "setp.eq.u32 p, %12, 0;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%1], %3, %11, p;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%13], %4, %11, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%14], %5, %11, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], [%15], %6, %11, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], [%2], %7, %19, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], [%16], %8, %19, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], [%17], %9, %19, 1;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], [%18], %10, %19, 1;\n\t}" ::"r"(d), \
+      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2), \
+      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24), \
+      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24), "r"(idx) \
+      : "memory")
 template <int S, int ACC, bool PAIR = false, bool MIXED = false>
 __device__ __forceinline__ void issue_chunk3(uint64_t bd, uint64_t bd_lo, uint32_t id, uint32_t first,
                                              uint32_t idx = 0) {
   constexpr uint32_t d = ACC * kAccStride;
   constexpr uint32_t a_hi = kStgCol0 + S * 64, a_lo = a_hi + 32;
-  if constexpr (MIXED) {  // idx: the bf16 instruction descriptor (N = r_pad)
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.eq.u32 p, %12, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %11, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%13], %4, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%14], %5, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%15], %6, %11, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %7, %19, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%16], %8, %19, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%17], %9, %19, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%18], %10, %19, 1;\n\t}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "l"(bd), "l"(bd + 2), "l"(bd + 4), "l"(bd + 6), "l"(bd_lo), "l"(bd_lo + 2),
-      "l"(bd_lo + 4), "l"(bd_lo + 6), "r"(id), "r"(first), "r"(a_hi + 8), "r"(a_hi + 16), "r"(a_hi + 24),
-      "r"(a_lo + 8), "r"(a_lo + 16), "r"(a_lo + 24), "r"(idx)
-      : "memory");
+  if constexpr (MIXED) {  // idx: the bf16 instruction descriptor (N = r_pad; M = 256 for a pair)
+    if constexpr (PAIR)
+      MLB_ISSUE_MIXED("2");
+    else
+      MLB_ISSUE_MIXED("1");
   return;
   }
 #if MLB_TC_EXP_TERMS == 3
@@ -579,7 +584,7 @@ __device__ __forceinline__ void mma_role(const Params& p, int total_units, int u
                                          uint64_t* sdone, uint64_t* bfull, uint64_t* bempty, uint64_t* afull,
                                          uint64_t* aempty) {
   const uint32_t id_full = idesc_tf32(2 * p.rp), id_hi = idesc_tf32(p.rp, PAIR ? 256 : 128);
-  const uint32_t id_x = idesc_bf16(p.rp);  // MIXED cross terms
+  const uint32_t id_x = idesc_bf16(p.rp, PAIR ? 256 : 128);  // MIXED cross terms
   int g = 0;
   int wc = 0;  // windows this warp has opened (all units): buffer wc % kAccBufs
   int lastph[kSlots / 2];    // parity of the last commit on this warp's slots W, W + 2, ...
@@ -1624,7 +1629,7 @@ class TcGemmImpl final : public TcGemm {
     // split factor F -> [F_hi ; F_lo] (2 rp x K)
     const size_t Kp = cdiv(K, tc::kChunk) * tc::kChunk;  // split row pitch: whole chunks
     ensure(&split_, &split_bytes_, (size_t)2 * rp * Kp * 4);
-    const bool mixed = mixed_ && !(pair_ && (rp == 32 || rp == 64) && cdiv(rows, 256) >= 8);
+    const bool mixed = mixed_;
     {
       const size_t tot = (size_t)rp * K;
       const unsigned g = (unsigned)std::min<size_t>(cdiv(tot, 256), 16384);
@@ -1637,7 +1642,7 @@ class TcGemmImpl final : public TcGemm {
     }
     // CTA pairs (cta_group::2, 256-row tiles): r_pad in {32, 64} (N split in
     // halves of >= 16 rows), an even SM count, enough tiles to fill the pairs
-    const bool pair = tc::kK3 && !mixed && pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
+    const bool pair = tc::kK3 && pair_ && (rp == 32 || rp == 64) && sms_ >= 2 && cdiv(rows, 256) >= 8;
     const int slots = pair ? sms_ / 2 : sms_;  // persistent schedulers: pairs or CTAs
     tc::Params p{};
     p.rows = (int)rows;
@@ -1700,7 +1705,7 @@ class TcGemmImpl final : public TcGemm {
     // of a pair its rp / 2 rows of each half (two boxes)
     const CUtensorMap mb = make_map(split_, Kp, 2 * rp, tc::kChunk, pair ? rp / 2 : 2 * rp, true);
     const size_t smem = 1024 + tc::kMStages * tc::kMTileBytes + tc::kBStages * tc::kBStageBytes + 512;
-    auto kern = pair ? tc::k_tc_product<TRANS, true, false>
+    auto kern = pair ? (mixed ? tc::k_tc_product<TRANS, true, true> : tc::k_tc_product<TRANS, true, false>)
                 : mixed ? tc::k_tc_product<TRANS, false, true> : tc::k_tc_product<TRANS, false, false>;
     const int ak = (TRANS ? 1 : 0) + (pair ? 2 : 0) + (mixed ? 4 : 0);
     if (!attr_set_[ak]) {
