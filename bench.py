@@ -46,13 +46,13 @@ def env_int(k, d):
         return d
 
 
-TRAFFIC_SRC = "profiles/r01_traffic_config4.json (ncu dram__bytes_read+write per launch, 1 GPU)"
+TRAFFIC_SRC = "profiles/r01d_traffic_config4.json (ncu dram__bytes_read+write per launch, 1 GPU)"
 
 
 def traffic_for(kernel, world):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of this
     workload (profiles/); None if absent or not the 1-GPU configuration."""
-    p = os.path.join(REPO, "profiles", "r01_traffic_config4.json")
+    p = os.path.join(REPO, "profiles", "r01d_traffic_config4.json")
     if world != 1 or not os.path.exists(p):
         return None
     with open(p) as f:
