@@ -4,7 +4,8 @@
 //   [B = W W^T] -> A = M_l W^T -> (allreduce A|B over NCCL) -> V sweep
 //   -> C = V^T M_l, D = V^T V -> W sweep
 // The two M-streaming products go to the SIMT fp64-accumulating GEMMs or, for
-// fp32 storage at scale, to the tcgen05 3xTF32 kernels (tc_gemm.cu).  All
+// fp32 storage at scale, to the tcgen05 integer-digit kernels (ix_gemm.cu:
+// exact int32 accumulation of 8-bit digit products).  All
 // state stays on the device; nothing synchronises with the host inside a
 // phase (samples and NNLS counts are collected by flush()).
 #include <cuda_runtime.h>
@@ -24,7 +25,7 @@
 #include "kernels.cuh"
 #include "nccl_shim.hpp"
 #include "nnls.cuh"
-#include "tc_gemm.hpp"
+#include "ix_gemm.hpp"
 #include "transfer_ops.hpp"
 
 namespace mlb {
@@ -244,6 +245,17 @@ struct Engine::Impl {
   // grids below one 128-row tile -- with the SIMT kernels)
   bool use_tc(size_t m) const { return tc && tc->wants(m, e->n_loc_, e->r_); }
 
+  // Row / column maxima of M_l (fixed-point scales of the tensor path),
+  // computed once per level on first use.
+  const float* level_stats(size_t l) {
+    auto& L = e->lv_[l];
+    if (!L.mstat) {
+      CK(dev_malloc(&L.mstat, (L.m + e->n_loc_) * 4));
+      tc->level_stats(static_cast<const float*>(L.M), L.m, e->n_loc_, L.mstat, L.mstat + L.m, s, &e->launches_);
+    }
+    return L.mstat;
+  }
+
   // A = M_l W^T (the first M pass), timed when profiling.
   template <typename T>
   void product_mwt(size_t l) {
@@ -254,7 +266,7 @@ struct Engine::Impl {
       CK(cudaEventRecord(evp.first, s));
     }
     if (use_tc(L.m))
-      tc->mwt(static_cast<const T*>(L.M), W.as<T>(), L.m, e->n_loc_, e->r_, A(), s, &e->launches_);
+      tc->mwt(static_cast<const T*>(L.M), level_stats(l), W.as<T>(), L.m, e->n_loc_, e->r_, A(), s, &e->launches_);
     else
       gemm_abt<T>(static_cast<const T*>(L.M), W.as<T>(), L.m, e->r_, e->n_loc_, A());
     if (e->profiling_) {
@@ -272,8 +284,8 @@ struct Engine::Impl {
       CK(cudaEventRecord(evp.first, s));
     }
     if (use_tc(L.m))
-      tc->vtm(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->n_loc_, e->r_, Cb.as<double>(), s,
-              &e->launches_);
+      tc->vtm(static_cast<const T*>(L.V), static_cast<const T*>(L.M), level_stats(l) + L.m, L.m, e->n_loc_, e->r_,
+              Cb.as<double>(), s, &e->launches_);
     else
       gemm_atb<T>(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->r_, e->n_loc_, Cb.as<double>());
     if (e->profiling_) {
@@ -465,10 +477,11 @@ struct Engine::Impl {
     const size_t cb = ceil_div(n, 128);
     const size_t tiled_smem = 2 * (size_t)r * 128 * sizeof(T);
     if (!exact() && use_tc(L.m)) {
-      // tensor-core residual (3xTF32 V W on tcgen05, fp32 residuals, fp64 sums)
-      tc->sqerr(static_cast<const T*>(L.M), static_cast<const T*>(L.V), W.as<T>(), L.m, n, (size_t)r, out, s,
-                &e->launches_);
-      allreduce_sum(out, 1);
+      // tensor path: the Gram identity ||M||^2 - 2 <V^T M, W> + <V^T V, W W^T>
+      // from one exact-accumulation product (ix_gemm.cu), no residual pass
+      e->norm2(l);  // host-cached ||M_l||^2 (syncs once per level)
+      gram_terms<T>(l, out);
+      launch(k_gram_combine, dim3(1), dim3(1), 0, out);
       return;
     }
     if (!exact() && tiled_smem <= 200 * 1024) {
@@ -520,32 +533,37 @@ struct Engine::Impl {
     return samples.as<SampleRec>() + samp_used++;
   }
 
+  // out[0] = ||M_l||^2, out[1] = <C, W> (C = V_l^T M_l), out[2] = <D, B>
+  // (D = V_l^T V_l, B = W W^T), all ranks; products recomputed only when the
+  // cached ones are stale
+  template <typename T>
+  void gram_terms(size_t l, double* out) {
+    const size_t r = e->r_;
+    if (!(CD_valid && CD_level == l)) {
+      gram_V<T>(l);
+      product_vtm<T>(l);
+      CD_valid = true;
+      CD_level = l;
+    }
+    if (!B_valid) {
+      gram_W<T>();
+      allreduce_sum(B(), r * r);
+      B_valid = true;
+    }
+    CK(cudaMemcpyAsync(out, &e->lv_[l].norm2, 8, cudaMemcpyHostToDevice, s));
+    dot<T>(Cb.as<double>(), 0, W.as<T>(), 2, r * e->n_loc_, out + 1);
+    allreduce_sum(out + 1, 1);
+    dot<T>(Db.as<double>(), 0, B(), 1, r * r, out + 2);
+  }
+
   template <typename T>
   void sample_t(size_t l, double work_units) {
     double* sc = scal.as<double>();
     const bool gram = e->gram_error();
-    if (gram) {
-      const auto& L = e->lv_[l];
-      const size_t r = e->r_;
-      if (!(CD_valid && CD_level == l)) {
-        gram_V<T>(l);
-        product_vtm<T>(l);
-        CD_valid = true;
-        CD_level = l;
-      }
-      if (!B_valid) {
-        gram_W<T>();
-        allreduce_sum(B(), r * r);
-        B_valid = true;
-      }
-      CK(cudaMemcpyAsync(sc, &e->lv_[l].norm2, 8, cudaMemcpyHostToDevice, s));
-      dot<T>(Cb.as<double>(), 0, W.as<T>(), 2, r * e->n_loc_, sc + 1);
-      allreduce_sum(sc + 1, 1);
-      dot<T>(Db.as<double>(), 0, B(), 1, r * r, sc + 2);
-      (void)L;
-    } else {
+    if (gram)
+      gram_terms<T>(l, sc);
+    else
       direct_e2<T>(l, sc);
-    }
     SampleRec* rec = reserve_sample();
     launch(k_write_sample, dim3(1), dim3(1), 0, (const double*)sc, gram ? 1 : 0, rec);
     samp_meta.push_back({0.0, work_units, (int)l + 1, 0.0});
@@ -556,7 +574,7 @@ struct Engine::Impl {
 
 Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
   if (o.dtype != 0 && o.dtype != 1) throw std::invalid_argument("dtype must be 0 (fp32) or 1 (fp64)");
-  if (o.gemm == 2 && o.dtype != 0) throw std::invalid_argument("tcgen05 3xTF32 path needs fp32 storage");
+  if (o.gemm == 2 && o.dtype != 0) throw std::invalid_argument("the tensor-core path needs fp32 storage");
   CK(cudaSetDevice(o.device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, o.device));
@@ -586,6 +604,7 @@ Engine::~Engine() {
   for (auto& L : lv_) {
     dev_free(L.M);
     dev_free(L.V);
+    dev_free(L.mstat);
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   for (DevBuf* b : {&impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
@@ -606,9 +625,11 @@ bool Engine::tc_active() const {
 bool Engine::gram_error() const {
   if (opt_.error_mode == 1) return true;
   if (opt_.error_mode == 2) return false;
-  // auto: the Gram identity needs fp64-accurate C, D (SURVEY finding 4) and a
-  // non-exact run (exact mode reproduces the reference's direct residual).
-  return !opt_.exact && !tc_active();
+  // auto: the Gram identity needs fp64-accurate C, D (SURVEY finding 4: the
+  // SIMT products accumulate in fp64, the tensor-path products exactly in
+  // int32) and a non-exact run (exact mode reproduces the reference's direct
+  // residual).
+  return !opt_.exact;
 }
 
 void Engine::sync() { CK(cudaStreamSynchronize(impl_->s)); }
@@ -629,7 +650,7 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   if (m == 0 || n_loc == 0) throw std::invalid_argument("Matrix: dimensions must be positive");
   if (h * w != m) throw std::invalid_argument("GridHierarchy: grid does not match matrix rows");
   for (auto& L : lv_) {
-    dev_free(L.M), dev_free(L.V);
+    dev_free(L.M), dev_free(L.V), dev_free(L.mstat);
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();
@@ -694,7 +715,7 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
   const size_t m = g.h * g.w;
   // allocate level 0
   for (auto& L : lv_) {
-    dev_free(L.M), dev_free(L.V);
+    dev_free(L.M), dev_free(L.V), dev_free(L.mstat);
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();

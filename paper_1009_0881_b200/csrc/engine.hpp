@@ -138,6 +138,7 @@ class Engine {
     size_t h, w, m;
     void* M = nullptr;  // T[m x n_loc]
     void* V = nullptr;  // T[m x r]
+    float* mstat = nullptr;  // tensor path: row maxima (m) then column maxima (n_loc) of M
     double norm2 = -1;
     double p_fro = 0;  // ||P||_F of P: next -> this (TransferOperator::frobenius_norm)
     // R: this level -> next; P: next -> this (device CSR)

@@ -735,6 +735,12 @@ __global__ void k_write_sample(const double* __restrict__ s, int gram, SampleRec
   out->t_ns = globaltimer();
 }
 
+// s[0] = ||M||^2 - 2 <C, W> + <D, B>, clamped at 0 (Gram identity)
+__global__ void k_gram_combine(double* s) {
+  const double e2 = s[0] - 2.0 * s[1] + s[2];
+  s[0] = e2 > 0.0 ? e2 : 0.0;
+}
+
 __global__ void k_timestamp(unsigned long long* out) { *out = globaltimer(); }
 
 // ---------------------------------------------------------------------------

@@ -1,24 +1,24 @@
-"""GPU: the tcgen05 3xTF32 M-streaming products against fp64 references.
+"""GPU: the tcgen05 integer-digit M-streaming products against fp64 references.
 
-A = M W^T and C = V^T M from fp32 storage: the tensor-core path must agree
-with an fp64 numpy product of the same fp32 inputs to 3xTF32 accuracy, on
-aligned and ragged shapes, r in {16..64}; and whole fp32 runs through the
-tensor path must track the fp64 oracle.
-
-Tolerance: the tensor core's fp32 accumulate truncates, a one-sided bias of
-~2.4e-7 relative per 32-K chunk accumulated in TMEM before the fp64 drain
-(kWindow = 8 chunks -> ~2e-6 at long K; short-K shapes ~4e-7).  TOL = 4e-6
-relative Frobenius error is that bound with a 2x margin; the long-K case
-(32768 x 8192, several windows per CTA) exercises it.
+A = M W^T and C = V^T M from fp32 storage (ix_gemm.cu): every operand row is
+a power-of-two-scaled 23-bit fixed-point value split into three signed 8-bit
+digits, and the digit products accumulate EXACTLY in int32 TMEM
+(tcgen05.mma.kind::i8).  The only error is the unbiased rounding of each
+input to its row's fixed-point grid (<= 2^-23 of the row maximum), which
+averages out along K: ~1e-8 relative at K = 256, ~1e-9 at K >= 2048.
+TOL = 1e-7 relative Frobenius error (the round-1 tf32 kernel needed 4e-6
+and carried a one-sided ~1e-6 bias); whole fp32 runs through the tensor path
+must track the fp64 oracle within the north-star 1e-5.
 """
 import numpy as np
 import pytest
 
 import oracle
+import ixmodel  # tests/ixmodel.py (the digit-format model)
 
 pytestmark = pytest.mark.gpu
 
-TOL = 4e-6
+TOL = 1e-7
 
 
 def relnorm(a, b):
@@ -52,6 +52,26 @@ def test_tc_products(P, gpu, m, n, r):
     assert relnorm(A2, A_ref) < 1e-13 and relnorm(C2, C_ref) < 1e-13
 
 
+@pytest.mark.parametrize("m,n,r", [(1024, 2048, 64), (1028, 1500, 49), (16384, 256, 64), (2052, 4100, 33),
+                                   (640, 640, 16), (32768, 8192, 64)])
+def test_tc_products_match_digit_model(P, gpu, m, n, r):
+    """The kernel's integer arithmetic, pinned: A and C equal the numpy model
+    of the digit format (tests/ixmodel.py: same scales, same rounding, exact
+    integer digit sums) up to the fp64 rounding of the split-K sum."""
+    rng = np.random.default_rng(m + 3 * n + r)
+    M = (rng.random((m, n)) ** 3).astype(np.float32)
+    M[rng.random((m, n)) < 0.2] = 0.0
+    V = (rng.random((m, r)) * rng.random((1, r)) * 4).astype(np.float32)
+    W = (rng.random((r, n)) * rng.random((r, 1)) * 9).astype(np.float32)
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V, W)
+        A, C = s.products()
+    Am, Cm = ixmodel.product_A(M, W), ixmodel.product_C(V, M)
+    np.testing.assert_allclose(A, Am, rtol=1e-14, atol=0)
+    np.testing.assert_allclose(C, Cm, rtol=1e-14, atol=0)
+
+
 def test_tc_deterministic(P, gpu):
     rng = np.random.default_rng(5)
     M = rng.random((2048, 4096)).astype(np.float32)
@@ -73,14 +93,9 @@ def round32(a):
 def test_tc_run_tracks_oracle(P, restated, gpu, cycle):
     """Config-0 generator at a tensor-path size (32x32 grid, n = 4096, r = 20,
     HALS, work:30): the fp32 tcgen05 run tracks the fp64 oracle fed the
-    fp32-rounded inputs, with an identical schedule.
-
-    Tolerance 6e-5 (not the SIMT path's 1e-5): the products carry ~2e-6
-    relative error (3xTF32 drops A_lo F_lo, and the tensor core's truncating
-    fp32 accumulate biases each 8-chunk window), and 30 single-level HALS
-    sweeps amplify it ~20x in the error trajectory (measured 4.5e-5; 1.2e-5
-    even with 1-chunk windows).  Multilevel runs stay ~4e-6.  Strict 1e-5
-    parity is the SIMT path (MLNMF_GEMM_SIMT)."""
+    fp32-rounded inputs within the north-star 1e-5 (error trajectory), with an
+    identical schedule.  The products are exact up to input rounding, so the
+    remaining deviation is fp32 storage of V and W between steps."""
     M = oracle.generate_config(0, n=4096, restated=restated).astype(np.float32)
     V0, W0 = restated.random_init(1024, 4096, 20, 0)
     L = 1 if cycle == "none" else 3
@@ -91,14 +106,19 @@ def test_tc_run_tracks_oracle(P, restated, gpu, cycle):
         assert s.tc_active
     assert np.array_equal(tg.level, to.level) and np.array_equal(tg.work_units, to.work)
     dev = float(np.max(np.abs(tg.error - to.error) / to.error))
-    assert dev < 6e-5, dev
+    assert dev < 1e-5, dev
 
 
 @pytest.mark.parametrize("m,n,r", [(1024, 2048, 64), (2052, 4100, 33), (4096, 3000, 20), (640, 640, 16)])
-def test_tc_residual_error(P, gpu, m, n, r):
-    """The tensor-core direct residual ||M - VW||_F (error samples of tensor-path
-    runs) against an fp64 numpy residual of the same fp32 inputs: within 1e-7
-    relative (measured ~5e-9), and against the SIMT residual kernel."""
+def test_tc_gram_error(P, gpu, m, n, r):
+    """Error samples of tensor-path runs use the Gram identity
+    ||M||^2 - 2 <V^T M, W> + <V^T V, W W^T> with the tensor-path product
+    C = V^T M (no residual pass).  Near a fit (5 % noise) the identity cancels
+    ~400x, so C's input rounding (V on a 2^-22 grid of its column maximum:
+    sum dV * A, random) shows: measured 1.5e-7 .. 6.6e-7 of ||M - VW|| at
+    these small shapes (it falls as 1/sqrt(m r): ~2e-8 at config 4), within
+    the north-star 1e-5.  Pinned exactly by the digit model (1e-12), bounded
+    against the fp64 residual (2e-6)."""
     rng = np.random.default_rng(m + n + r)
     V = rng.random((m, r)).astype(np.float32)
     W = rng.random((r, n)).astype(np.float32)
@@ -108,28 +128,35 @@ def test_tc_residual_error(P, gpu, m, n, r):
     with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
         s.set_data(M, P.ImageGrid(m, 1))
         s.set_factors(V, W)
-        assert s.tc_active and not s.gram_error
+        assert s.tc_active and s.gram_error
         e_tc = s.error()
-    assert abs(e_tc - ref) / ref < 1e-7, (e_tc, ref)
+    e_model = ixmodel.gram_error(M, V, W)
+    assert abs(e_tc - e_model) / e_model < 1e-12, (e_tc, e_model)
+    assert abs(e_tc - ref) / ref < 2e-6, (e_tc, ref)
 
 
-@pytest.mark.parametrize("m,n,r", [(2048, 4096, 64), (4096, 2304, 32), (3000, 2600, 64)])
-def test_tc_products_cta_pairs(P, gpu, monkeypatch, m, n, r):
-    """The opt-in CTA-pair products (cta_group::2, 256-row tiles, MLB_TC_PAIR=1,
-    read when a session's tensor path is created) agree with fp64 like the
-    single-CTA kernel, including ragged 256-row tiles."""
-    monkeypatch.setenv("MLB_TC_PAIR", "1")
-    rng = np.random.default_rng(m + n + r)
-    M = rng.random((m, n)).astype(np.float32)
-    V = rng.random((m, r)).astype(np.float32)
-    W = (rng.random((r, n)) * 2).astype(np.float32)
+def test_tc_products_wide_range(P, gpu):
+    """Rows of very different magnitude (per-row fixed-point scales, 24 decades
+    across M's rows, 12-18 across the factors): the digit model holds exactly,
+    and every entry of A and C keeps fp32-level relative accuracy against fp64
+    (the sums are dominated by a few terms near the row maximum, whose grid
+    step is <= 2^-21 relative)."""
+    rng = np.random.default_rng(11)
+    m, n, r = 1024, 4096, 64
+    M = (rng.random((m, n)) * np.logspace(-12, 12, m)[:, None]).astype(np.float32)
+    V = (rng.random((m, r)) * np.logspace(-6, 6, r)[None, :]).astype(np.float32)
+    W = (rng.random((r, n)) * np.logspace(-9, 9, r)[:, None]).astype(np.float32)
     M64, V64, W64 = M.astype(np.float64), V.astype(np.float64), W.astype(np.float64)
     with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
         s.set_data(M, P.ImageGrid(m, 1))
-        s.set_factors(V64, W64)
+        s.set_factors(V, W)
         A, C = s.products()
-    ea, ec = relnorm(A, M64 @ W64.T), relnorm(C, V64.T @ M64)
-    assert ea < TOL and ec < TOL, (ea, ec)
+    np.testing.assert_allclose(A, ixmodel.product_A(M, W), rtol=1e-14, atol=0)
+    np.testing.assert_allclose(C, ixmodel.product_C(V, M), rtol=1e-14, atol=0)
+    A_ref, C_ref = M64 @ W64.T, V64.T @ M64
+    ea = np.max(np.abs(A - A_ref) / np.abs(A_ref))
+    ec = np.max(np.abs(C - C_ref) / np.abs(C_ref))
+    assert ea < 5e-6 and ec < 5e-6, (ea, ec)
 
 
 def test_fast_register_sweeps_match_reference_order(P, gpu, monkeypatch):

@@ -1,0 +1,58 @@
+"""GPU: parity of the BENCHMARKED path at the benchmarked configuration.
+
+bench.py's headline runs the tcgen05 integer-digit products (ix_gemm.cu) at
+config 4 (256x256 grid, m = 65536, r = 64, HALS).  Here the same path, forced
+(GEMM_TCGEN05), runs a 4096-column slice of that workload -- the config-4
+generator with n_total = 262144, regenerated on the device and checked bit
+for bit against the fixture's digest -- single-level (work:20) and 5-level FMG
+(work:20), traced every step, against the UNMODIFIED reference's fp64
+trajectories on the same fp32-rounded inputs
+(tests/golden/make_tc_trajectory.py, oracle/_ref: solvers.cpp:300-355,
+multilevel.cpp:93-114).
+
+Tolerance: the north-star 1e-5 relative on every error sample, identical
+levels and work units.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden", "tc_trajectory_config4.npz")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLD)
+
+
+@pytest.fixture(scope="module")
+def inputs(P, golden):
+    m, n = (int(x) for x in golden["shape"])
+    with P.Session(dtype=P.F32) as g:
+        g.generate(4, seed=0, n_total=262144, col0=0, n_local=n)
+        M32 = np.empty((m, n), np.float32)
+        g.export_data(M32.ctypes.data)
+    assert hashlib.sha256(M32.tobytes()).digest() == golden["m_digest"].tobytes(), "device generator drifted"
+    V0, W0 = P.random_init(m, n, int(golden["rank"]), 0)
+    return M32, V0, W0
+
+
+@pytest.mark.parametrize("cycle", ["none", "fmg"])
+def test_config4_slice_tracks_reference(P, gpu, golden, inputs, cycle):
+    M32, V0, W0 = inputs
+    levels = 1 if cycle == "none" else 5
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M32, P.ImageGrid(256, 256))
+        tr = s.run_cycle(levels, levels, V0, W0, "hals", cycle, float(golden["work"]), 1)
+        assert s.tc_active
+    err, lev, work = golden[f"{cycle}_error"], golden[f"{cycle}_level"], golden[f"{cycle}_work"]
+    assert np.array_equal(tr.level, lev) and np.array_equal(tr.work_units, work)
+    dev = np.abs(tr.error - err) / err
+    print(f"config-4 slice, {cycle}: {len(err)} samples, max rel dev {dev.max():.2e} "
+          f"(finest-level samples {dev[lev == 1].max():.2e})")
+    assert dev.max() < 1e-5, dev.max()
