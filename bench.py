@@ -267,6 +267,7 @@ def run_b200(args):
     s.set_profiling(True)
     s.steps("hals", 3)
     kt = s.kernel_times()
+    phases = s.phase_times()
     s.set_profiling(False)
     mwt_ms = kt["mwt_ms"] / max(kt["mwt_n"], 1)
     vtm_ms = kt["vtm_ms"] / max(kt["vtm_n"], 1)
@@ -302,7 +303,7 @@ def run_b200(args):
         "data": "synthetic (BASELINE config-4 generator on the device, seed 0)",
         "config": {"workload": WORKLOAD, "global_batch": N_TOTAL, "seq_len": M_ROWS,
                    "parallelism": f"column-shard x{world}", "l2": "inputs larger than L2 (M = 64 GiB fp32)",
-                   "gemm_path": "tcgen05 3xTF32" if tc else "SIMT fp64-accumulate"},
+                   "gemm_path": "tcgen05 kind::i8 digit products (fp32 operands as 23-bit fixed point, exact int32 accumulation)" if tc else "SIMT fp64-accumulate"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -311,7 +312,8 @@ def run_b200(args):
                      "algorithmic_bytes_per_launch": bytes_per_pass,
                      "avg_ms": {"A = M W^T": mwt_ms, "C = V^T M": vtm_ms,
                                 "allreduce [A|B]": kt["comm_ms"] / max(kt["comm_n"], 1) if kt["comm_n"] else 0.0},
-                     "step_frac_in_products": (mwt_ms + vtm_ms) / (ms_max / args.steps)},
+                     "step_frac_in_products": (mwt_ms + vtm_ms) / (ms_max / args.steps),
+                     "step_phases_ms": phases},
         "rel_error": {"start": float(tr0.error[0]) / norm, "after_bench": err_end / norm},
         "gen_s": t_gen,
     }

@@ -206,6 +206,13 @@ int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, do
 /* profiled time of the per-step NCCL allreduce of [M W^T | W W^T] (world > 1;
  * 0 calls on one rank), CUDA events on the engine stream */
 int mlnmf_session_comm_time(mlnmf_session* s, double* ms, long* count);
+/* profiled time of each phase of the profiled solver steps, 7 entries in
+ * step order: B = W W^T, A = M W^T, allreduce [A | B], V update, D = V^T V,
+ * C = V^T M, W update (total ms and number of timed intervals per phase;
+ * CUDA events on the engine stream).  B200 instrumentation, no reference
+ * counterpart. */
+#define MLNMF_NUM_PHASES 7
+int mlnmf_session_phase_times(mlnmf_session* s, double* ms, long* count);
 long mlnmf_session_launches(mlnmf_session* s);
 void* mlnmf_session_stream(mlnmf_session* s);
 /* 1 if the tcgen05 path serves the M-streaming products */

@@ -238,6 +238,7 @@ _proto("mlnmf_trace_num_phases", _sz, _vp)
 _proto("mlnmf_trace_phases", None, _vp, _ip, _lp)
 _proto("mlnmf_trace_free", None, _vp)
 _proto("mlnmf_session_comm_time", C.c_int, _vp, _dp, _lp)
+_proto("mlnmf_session_phase_times", C.c_int, _vp, _dp, _lp)
 _proto("mlnmf_load_pgm_dir", C.c_int, C.c_char_p, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz),
        C.POINTER(_sz))
 _proto("mlnmf_load_csv", C.c_int, C.c_char_p, C.POINTER(_vp), C.POINTER(_sz), C.POINTER(_sz))
@@ -840,6 +841,17 @@ class Session:
         x, xn = C.c_double(), C.c_long()
         _check(_lib.mlnmf_session_comm_time(self._h, C.byref(x), C.byref(xn)))
         return dict(mwt_ms=a.value, mwt_n=an.value, vtm_ms=c.value, vtm_n=cn.value, comm_ms=x.value, comm_n=xn.value)
+
+    STEP_PHASES = ("B = W W^T", "A = M W^T", "allreduce [A|B]", "V update", "D = V^T V", "C = V^T M", "W update")
+
+    def phase_times(self):
+        """Mean ms per timed interval of each step phase (profiling on; CUDA
+        events on the engine stream), keyed by STEP_PHASES; phases that did
+        not run are omitted."""
+        ms = (C.c_double * 7)()
+        cnt = (C.c_long * 7)()
+        _check(_lib.mlnmf_session_phase_times(self._h, ms, cnt))
+        return {k: ms[i] / cnt[i] for i, k in enumerate(self.STEP_PHASES) if cnt[i] > 0}
 
     @property
     def launches(self) -> int:

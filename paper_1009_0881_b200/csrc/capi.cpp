@@ -471,6 +471,13 @@ int mlnmf_session_comm_time(mlnmf_session* s, double* ms, long* count) {
   });
 }
 
+int mlnmf_session_phase_times(mlnmf_session* s, double* ms, long* count) {
+  return guard([&] {
+    KernelTimes k = s->e->kernel_times();
+    for (int i = 0; i < kNumPhases; ++i) ms[i] = k.phase_ms[i], count[i] = k.phase_n[i];
+  });
+}
+
 long mlnmf_session_launches(mlnmf_session* s) { return s->e->launches(); }
 void* mlnmf_session_stream(mlnmf_session* s) { return s->e->stream(); }
 int mlnmf_session_tc_active(mlnmf_session* s) { return s->e->tc_active() ? 1 : 0; }

@@ -15,7 +15,7 @@
 // 4 NNLS cap exceeded, 1 anything else (CUDA failures included).
 // B200-specific options (not in the reference): --precision fp64 (default:
 // the reference's operation order, bit-identical results) | fp64-fast | fp32
-// (fp32 storage, tcgen05 3xTF32 products), --device k, and for bench
+// (fp32 storage, tcgen05 integer-digit products), --device k, and for bench
 // --workers w (concurrent device sessions per configuration).
 // Argument parsing is a small hand-written `--name value` / `--name=value`
 // scanner (the reference uses CLI11, which is not part of this build).

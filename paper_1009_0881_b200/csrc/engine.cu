@@ -111,6 +111,7 @@ struct Engine::Impl {
   ncclComm_t comm = nullptr;
   // profiling
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mwt, ev_vtm, ev_comm;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_phase;  // (StepPhase, events)
   std::vector<cudaEvent_t> ev_pool;
   std::chrono::steady_clock::time_point host_t0 = std::chrono::steady_clock::now();
   TcGemm* tc = nullptr;
@@ -152,6 +153,21 @@ struct Engine::Impl {
     return x;
   }
 
+  // Run f; when profiling, bracket it with CUDA events on the engine stream
+  // and book the interval under step phase ph (KernelTimes::phase_ms).
+  template <typename F>
+  void timed(int ph, F&& f) {
+    if (!e->profiling_) {
+      f();
+      return;
+    }
+    cudaEvent_t a = ev(), b = ev();
+    CK(cudaEventRecord(a, s));
+    f();
+    CK(cudaEventRecord(b, s));
+    ev_phase.push_back({ph, {a, b}});
+  }
+
   // ---------------- collectives ----------------
   // collectives run whenever a communicator exists: world > 1, or a 1-rank
   // communicator requested by passing an NCCL id with world = 1 (exercises the
@@ -179,8 +195,8 @@ struct Engine::Impl {
   // output tile extent along the narrow (rank) dimension
   static int narrow_tile(size_t extent) { return extent <= 32 ? 32 : extent <= 48 ? 48 : 64; }
 
-  template <typename T>
-  void gemm_abt(const T* X, const T* Y, size_t rows, size_t ny, size_t K, double* out) {
+  template <typename TX, typename TY>
+  void gemm_abt(const TX* X, const TY* Y, size_t rows, size_t ny, size_t K, double* out) {
     const int tc = narrow_tile(ny);
     const size_t tiles = ceil_div(rows, GT) * ceil_div(ny, (size_t)tc);
     const int sp = splits_for(tiles, K);
@@ -194,9 +210,11 @@ struct Engine::Impl {
     }
     auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst); };
     if (exact())
-      tc == 32 ? go(k_gemm_abt<T, true, 32>) : tc == 48 ? go(k_gemm_abt<T, true, 48>) : go(k_gemm_abt<T, true, 64>);
+      tc == 32 ? go(k_gemm_abt<TX, TY, true, 32>) : tc == 48 ? go(k_gemm_abt<TX, TY, true, 48>)
+               : go(k_gemm_abt<TX, TY, true, 64>);
     else
-      tc == 32 ? go(k_gemm_abt<T, false, 32>) : tc == 48 ? go(k_gemm_abt<T, false, 48>) : go(k_gemm_abt<T, false, 64>);
+      tc == 32 ? go(k_gemm_abt<TX, TY, false, 32>) : tc == 48 ? go(k_gemm_abt<TX, TY, false, 48>)
+               : go(k_gemm_abt<TX, TY, false, 64>);
     if (spr > 1) {
       const size_t cnt = rows * ny;
       reduce_splits(part.as<double>(), cnt, spr, out);
@@ -204,8 +222,8 @@ struct Engine::Impl {
   }
 
   // out (r x ncols, fp64) = V (K x r)^T * X (K x ncols)
-  template <typename T>
-  void gemm_atb(const T* V, const T* X, size_t K, size_t r, size_t ncols, double* out) {
+  template <typename TV, typename TX>
+  void gemm_atb(const TV* V, const TX* X, size_t K, size_t r, size_t ncols, double* out) {
     const int tr = narrow_tile(r);
     const size_t tiles = ceil_div(ncols, GT) * ceil_div(r, (size_t)tr);
     const int sp = splits_for(tiles, K);
@@ -219,9 +237,11 @@ struct Engine::Impl {
     }
     auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst); };
     if (exact())
-      tr == 32 ? go(k_gemm_atb<T, true, 32>) : tr == 48 ? go(k_gemm_atb<T, true, 48>) : go(k_gemm_atb<T, true, 64>);
+      tr == 32 ? go(k_gemm_atb<TV, TX, true, 32>) : tr == 48 ? go(k_gemm_atb<TV, TX, true, 48>)
+               : go(k_gemm_atb<TV, TX, true, 64>);
     else
-      tr == 32 ? go(k_gemm_atb<T, false, 32>) : tr == 48 ? go(k_gemm_atb<T, false, 48>) : go(k_gemm_atb<T, false, 64>);
+      tr == 32 ? go(k_gemm_atb<TV, TX, false, 32>) : tr == 48 ? go(k_gemm_atb<TV, TX, false, 48>)
+               : go(k_gemm_atb<TV, TX, false, 64>);
     if (spr > 1) {
       const size_t cnt = r * ncols;
       reduce_splits(part.as<double>(), cnt, spr, out);
@@ -242,8 +262,34 @@ struct Engine::Impl {
 
   // tensor path for a level of m rows (fp32 storage, supported shape, policy;
   // a forced tensor path still serves unsupported levels -- e.g. coarse
-  // grids below one 128-row tile -- with the SIMT kernels)
-  bool use_tc(size_t m) const { return tc && tc->wants(m, e->n_loc_, e->r_); }
+  // grids below one 128-row tile -- with the SIMT kernels).  Decided once
+  // per (level, rank r) for ALL ranks (decide_tc): every rank must issue
+  // the same collectives, and the shape rules see the local column count.
+  std::map<std::pair<size_t, size_t>, bool> tc_ok;
+  bool use_tc(size_t m) const {
+    if (!tc) return false;
+    auto it = tc_ok.find({m, e->r_});
+    if (it == tc_ok.end()) throw std::logic_error("tensor-path decision missing for a level (decide_tc)");
+    return it->second;
+  }
+  // at host-synchronous points (factor and level setup): local policy,
+  // combined over ranks (any rank unable => nobody takes the tensor path)
+  void decide_tc() {
+    if (!tc || e->r_ == 0) return;
+    for (const auto& L : e->lv_) {
+      const auto key = std::make_pair(L.m, e->r_);
+      if (tc_ok.count(key)) continue;
+      double veto = tc->wants(L.m, e->n_loc_, e->r_) ? 0.0 : 1.0;
+      if (comm) {
+        double* d = scal.as<double>() + 9;
+        CK(cudaMemcpyAsync(d, &veto, 8, cudaMemcpyHostToDevice, s));
+        allreduce_max(d, 1);
+        CK(cudaMemcpyAsync(&veto, d, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      }
+      tc_ok[key] = veto == 0.0;
+    }
+  }
 
   // Row / column maxima of M_l (fixed-point scales of the tensor path),
   // computed once per level on first use.
@@ -266,9 +312,10 @@ struct Engine::Impl {
       CK(cudaEventRecord(evp.first, s));
     }
     if (use_tc(L.m))
-      tc->mwt(static_cast<const T*>(L.M), level_stats(l), W.as<T>(), L.m, e->n_loc_, e->r_, A(), s, &e->launches_);
+      tc->mwt(static_cast<const T*>(L.M), level_stats(l), W.as<double>(), L.m, e->n_loc_, e->r_, A(), s,
+              &e->launches_);
     else
-      gemm_abt<T>(static_cast<const T*>(L.M), W.as<T>(), L.m, e->r_, e->n_loc_, A());
+      gemm_abt(static_cast<const T*>(L.M), W.as<double>(), L.m, e->r_, e->n_loc_, A());
     if (e->profiling_) {
       CK(cudaEventRecord(evp.second, s));
       ev_mwt.push_back(evp);
@@ -284,10 +331,10 @@ struct Engine::Impl {
       CK(cudaEventRecord(evp.first, s));
     }
     if (use_tc(L.m))
-      tc->vtm(static_cast<const T*>(L.V), static_cast<const T*>(L.M), level_stats(l) + L.m, L.m, e->n_loc_, e->r_,
-              Cb.as<double>(), s, &e->launches_);
+      tc->vtm(static_cast<const double*>(L.V), static_cast<const T*>(L.M), level_stats(l) + L.m, L.m, e->n_loc_,
+              e->r_, Cb.as<double>(), s, &e->launches_);
     else
-      gemm_atb<T>(static_cast<const T*>(L.V), static_cast<const T*>(L.M), L.m, e->r_, e->n_loc_, Cb.as<double>());
+      gemm_atb(static_cast<const double*>(L.V), static_cast<const T*>(L.M), L.m, e->r_, e->n_loc_, Cb.as<double>());
     if (e->profiling_) {
       CK(cudaEventRecord(evp.second, s));
       ev_vtm.push_back(evp);
@@ -295,12 +342,12 @@ struct Engine::Impl {
   }
   template <typename T>
   void gram_W() {  // B = W W^T over all ranks
-    gemm_abt<T>(W.as<T>(), W.as<T>(), e->r_, e->r_, e->n_loc_, B());
+    gemm_abt(W.as<double>(), W.as<double>(), e->r_, e->r_, e->n_loc_, B());
   }
   template <typename T>
   void gram_V(size_t l) {  // D = V_l^T V_l (replicated)
     const auto& L = e->lv_[l];
-    gemm_atb<T>(static_cast<const T*>(L.V), static_cast<const T*>(L.V), L.m, e->r_, e->r_, Db.as<double>());
+    gemm_atb(static_cast<const double*>(L.V), static_cast<const double*>(L.V), L.m, e->r_, e->r_, Db.as<double>());
   }
 
   // ---------------- row/column sweeps ----------------
@@ -314,7 +361,9 @@ struct Engine::Impl {
   static constexpr size_t kWarpSweepMax = 16384;
   // register sweeps at the config-4 rank: interleaved fused dot chains in
   // non-exact runs (MLNMF_EXACT_SWEEPS=1 keeps the reference order)
-  bool fast_sweeps() const { return !exact() && std::getenv("MLNMF_EXACT_SWEEPS") == nullptr; }
+  bool fast_sweeps() const {
+    return e->opt_.dtype == 0 && !exact() && std::getenv("MLNMF_EXACT_SWEEPS") == nullptr;
+  }
   bool warp_sweeps(size_t r, size_t count) const {
     if (exact() || r > 64 || std::getenv("MLNMF_THREAD_SWEEPS") != nullptr) return false;
     return count < kWarpSweepMax || std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
@@ -332,8 +381,8 @@ struct Engine::Impl {
     int* deg = flags.as<int>();
     // ---- V half: A = M W^T, B = W W^T (solvers.cpp:82-83,105-106,251-252)
     const bool needB = !B_valid;
-    if (needB) gram_W<T>();
-    product_mwt<T>(l);
+    if (needB) timed(kPhB, [&] { gram_W<T>(); });
+    timed(kPhA, [&] { product_mwt<T>(l); });
     if (comm) {
       std::pair<cudaEvent_t, cudaEvent_t> evp{};
       if (e->profiling_) {
@@ -351,66 +400,69 @@ struct Engine::Impl {
         ev_comm.push_back(evp);
       }
     }
-    T* V = static_cast<T*>(L.V);
+    double* V = static_cast<double*>(L.V);
     const int bd = sweep_block((int)r);
     const size_t smem = (r * r + r * bd) * 8;
-    const dim3 gv((unsigned)ceil_div(L.m, bd));
-    if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
-      launch(k_hals_v_warp<T>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
-             (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
-    } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
-      hals_v_reg(r, sizeof(T) == 4, fast_sweeps(), A(), B(), V, L.m, deg, s);
-      ++e->launches_;
-    } else if (kind == kHals) {
-      launch(k_hals_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
-    } else if (kind == kMu && warp_sweeps(r, L.m)) {
-      launch(k_mu_warp<T, false>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)),
-             dim3(256), r * r * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r);
-    } else if (kind == kMu && mu_reg_supported(r)) {
-      mu_v_reg(r, sizeof(T) == 4, A(), B(), V, L.m, s);
-      ++e->launches_;
-    } else if (kind == kMu) {
-      launch(k_mu_v<T>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
-    } else {
-      nnls<T>((const double*)B(), L.m, (const double*)A(), r, 1, V, r, 1);
-    }
+    timed(kPhV, [&] {
+      const dim3 gv((unsigned)ceil_div(L.m, bd));
+      if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
+        launch(k_hals_v_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
+               (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
+      } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
+        hals_v_reg(r, fast_sweeps(), A(), B(), V, L.m, deg, s);
+        ++e->launches_;
+      } else if (kind == kHals) {
+        launch(k_hals_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
+      } else if (kind == kMu && warp_sweeps(r, L.m)) {
+        launch(k_mu_warp<double, false>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)),
+               dim3(256), r * r * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r);
+      } else if (kind == kMu && mu_reg_supported(r)) {
+        mu_v_reg(r, A(), B(), V, L.m, s);
+        ++e->launches_;
+      } else if (kind == kMu) {
+        launch(k_mu_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
+      } else {
+        nnls((const double*)B(), L.m, (const double*)A(), r, 1, V, r, 1);
+      }
+    });
     // ---- W half: C = V^T M, D = V^T V (solvers.cpp:91-92,124-125,272-273)
-    gram_V<T>(l);
-    product_vtm<T>(l);
-    T* Wp = W.as<T>();
-    const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
-    if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
-      launch(k_hals_w_warp<T>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
-             dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-             e->n_loc_, (int)r, deg);
-    } else if (kind == kHals && hals_reg_supported(r)) {
-      hals_w_reg(r, sizeof(T) == 4, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
-      ++e->launches_;
-    } else if (kind == kHals) {
-      launch(k_hals_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-             e->n_loc_, (int)r, deg);
-    } else if (kind == kMu && warp_sweeps(r, e->n_loc_)) {
-      launch(k_mu_warp<T, true>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
-             dim3(256), r * r * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_,
-             (int)r);
-    } else if (kind == kMu && mu_reg_supported(r)) {
-      mu_w_reg(r, sizeof(T) == 4, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, s);
-      ++e->launches_;
-    } else if (kind == kMu) {
-      launch(k_mu_w<T>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-             e->n_loc_, (int)r);
-    } else {
-      nnls<T>((const double*)Db.as<double>(), e->n_loc_, (const double*)Cb.as<double>(), 1, e->n_loc_, Wp, 1,
-              e->n_loc_);
-    }
+    timed(kPhD, [&] { gram_V<T>(l); });
+    timed(kPhC, [&] { product_vtm<T>(l); });
+    timed(kPhW, [&] {
+      double* Wp = W.as<double>();
+      const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
+      if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
+        launch(k_hals_w_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
+               dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+               e->n_loc_, (int)r, deg);
+      } else if (kind == kHals && hals_reg_supported(r)) {
+        hals_w_reg(r, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
+        ++e->launches_;
+      } else if (kind == kHals) {
+        launch(k_hals_w<double>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+               e->n_loc_, (int)r, deg);
+      } else if (kind == kMu && warp_sweeps(r, e->n_loc_)) {
+        launch(k_mu_warp<double, true>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
+               dim3(256), r * r * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_,
+               (int)r);
+      } else if (kind == kMu && mu_reg_supported(r)) {
+        mu_w_reg(r, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, s);
+        ++e->launches_;
+      } else if (kind == kMu) {
+        launch(k_mu_w<double>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+               e->n_loc_, (int)r);
+      } else {
+        nnls((const double*)Db.as<double>(), e->n_loc_, (const double*)Cb.as<double>(), 1, e->n_loc_, Wp, 1,
+                e->n_loc_);
+      }
+    });
     B_valid = false;
     CD_valid = true;
     CD_level = l;
   }
 
   // batched NNLS over nprob problems; counts appended to the count ring
-  template <typename T>
-  void nnls(const double* G, size_t nprob, const double* H, size_t hi, size_t he, T* X, size_t xi, size_t xe) {
+  void nnls(const double* G, size_t nprob, const double* H, size_t hi, size_t he, double* X, size_t xi, size_t xe) {
     const int r = (int)e->r_;
     if (r > 128) throw std::invalid_argument("anls on the device supports rank <= 128");
     const size_t gbytes = (size_t)r * r * 8, wb = nnls_warp_bytes(r);
@@ -426,10 +478,10 @@ struct Engine::Impl {
     const size_t blocks = std::min<size_t>(ceil_div(nprob, nw), (size_t)sm_count * per_sm);
     int* cnt = reserve_counts(nprob);
     if (exact())
-      launch(k_nnls_batch<T, true>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi, xe,
+      launch(k_nnls_batch<double, true>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi, xe,
              cnt, flags.as<int>() + 1);
     else
-      launch(k_nnls_batch<T, false>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi,
+      launch(k_nnls_batch<double, false>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi,
              xe, cnt, flags.as<int>() + 1);
   }
 
@@ -476,22 +528,12 @@ struct Engine::Impl {
     const size_t n = e->n_loc_;
     const size_t cb = ceil_div(n, 128);
     const size_t tiled_smem = 2 * (size_t)r * 128 * sizeof(T);
-    if (!exact() && use_tc(L.m)) {
-      // tensor path: the Gram identity ||M||^2 - 2 <V^T M, W> + <V^T V, W W^T>
-      // from one exact-accumulation product (ix_gemm.cu), no residual pass
-      e->norm2(l);  // host-cached ||M_l||^2 (syncs once per level)
-      gram_terms<T>(l, out);
-      launch(k_gram_combine, dim3(1), dim3(1), 0, out);
+    if (tc_sample(l)) {
+      tc_e2<T>(l, out);
       return;
     }
     if (!exact() && tiled_smem <= 200 * 1024) {
-      // register-tiled residual: one fp64 partial per 128 x 128 tile
-      const size_t rb = ceil_div(L.m, 128), nb = cb * rb;
-      part.ensure(nb * 8);
-      launch(k_sqerr_tiled<T>, dim3((unsigned)cb, (unsigned)rb), dim3(256), tiled_smem, (const T*)L.M,
-             (const T*)L.V, (const T*)W.as<T>(), L.m, n, r, part.as<double>());
-      launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part.as<double>(), nb, out, 0);
-      allreduce_sum(out, 1);
+      tiled_residual<T>(l, out, nullptr);
       return;
     }
     size_t sp = 1;
@@ -501,11 +543,11 @@ struct Engine::Impl {
     part.ensure(spr * n * 8);
     const size_t smem = ((size_t)r * 128 + 32 * (size_t)r) * 8;
     if (exact())
-      launch(k_col_sqerr<T, true>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M, (const T*)L.V,
-             (const T*)W.as<T>(), L.m, n, r, rchunk, part.as<double>());
+      launch(k_col_sqerr<T, true>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M,
+             (const double*)L.V, (const double*)W.as<double>(), L.m, n, r, rchunk, part.as<double>());
     else
       launch(k_col_sqerr<T, false>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M,
-             (const T*)L.V, (const T*)W.as<T>(), L.m, n, r, rchunk, part.as<double>());
+             (const double*)L.V, (const double*)W.as<double>(), L.m, n, r, rchunk, part.as<double>());
     if (exact()) {
       launch(k_sum_final, dim3(1), dim3(32), 0, (const double*)part.as<double>(), n, out, 1);
     } else {
@@ -517,6 +559,42 @@ struct Engine::Impl {
       launch(k_sum_final, dim3(1), dim3(1024), 0, colv, n, out, 0);
     }
     allreduce_sum(out, 1);
+  }
+
+  // register-tiled residual ||M_l - V_l W||^2 (persistent, one fp64 partial
+  // per block) into out[0], all ranks; gated blocks return at once unless
+  // *gate != 0
+  template <typename T>
+  void tiled_residual(size_t l, double* out, const double* gate) {
+    const auto& L = e->lv_[l];
+    const int r = (int)e->r_;
+    const size_t n = e->n_loc_;
+    const size_t tiles = ceil_div(n, 128) * ceil_div(L.m, 128);
+    const size_t grid = std::min<size_t>(tiles, 2 * (size_t)sm_count);
+    part.ensure(grid * 8);
+    launch(k_sqerr_tiled<T>, dim3((unsigned)grid), dim3(256), 2 * (size_t)r * 128 * sizeof(T), (const T*)L.M,
+           (const double*)L.V, (const double*)W.as<double>(), L.m, n, r, part.as<double>(), gate);
+    launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part.as<double>(), grid, out, 0);
+    allreduce_sum(out, 1);
+  }
+
+  // Error samples of tensor-path levels (auto error mode): the Gram identity
+  // ||M||^2 - 2 <V^T M, W> + <V^T V, W W^T> from the tensor-path C (no
+  // residual pass) -- unless it cancels more than 1 / kGramTau-fold, where
+  // the products' input rounding would show (measured: 5e-5 of e at the
+  // config-4 slice's coarsest level, rel. error ~2e-3); then the direct
+  // residual (k_sqerr_tiled, gated on the device: no host sync) is used.
+  static constexpr double kGramTau = 1e-4;  // e < 1 % of ||M_l||
+  bool tc_sample(size_t l) const {
+    return !exact() && use_tc(e->lv_[l].m) && e->opt_.error_mode == 0;
+  }
+  template <typename T>
+  void tc_e2(size_t l, double* sc) {
+    e->norm2(l);  // host-cached ||M_l||^2 (syncs once per level)
+    gram_terms<T>(l, sc);
+    launch(k_gram_check, dim3(1), dim3(1), 0, sc, kGramTau);
+    tiled_residual<T>(l, sc + 8, sc + 7);
+    launch(k_gram_select, dim3(1), dim3(1), 0, sc);
   }
 
   SampleRec* reserve_sample() {
@@ -551,7 +629,7 @@ struct Engine::Impl {
       B_valid = true;
     }
     CK(cudaMemcpyAsync(out, &e->lv_[l].norm2, 8, cudaMemcpyHostToDevice, s));
-    dot<T>(Cb.as<double>(), 0, W.as<T>(), 2, r * e->n_loc_, out + 1);
+    dot<T>(Cb.as<double>(), 0, W.as<double>(), 1, r * e->n_loc_, out + 1);
     allreduce_sum(out + 1, 1);
     dot<T>(Db.as<double>(), 0, B(), 1, r * r, out + 2);
   }
@@ -559,11 +637,15 @@ struct Engine::Impl {
   template <typename T>
   void sample_t(size_t l, double work_units) {
     double* sc = scal.as<double>();
-    const bool gram = e->gram_error();
-    if (gram)
+    bool gram = e->gram_error();
+    if (tc_sample(l)) {
+      tc_e2<T>(l, sc);  // sc[0] = e^2
+      gram = false;
+    } else if (gram) {
       gram_terms<T>(l, sc);
-    else
+    } else {
       direct_e2<T>(l, sc);
+    }
     SampleRec* rec = reserve_sample();
     launch(k_write_sample, dim3(1), dim3(1), 0, (const double*)sc, gram ? 1 : 0, rec);
     samp_meta.push_back({0.0, work_units, (int)l + 1, 0.0});
@@ -587,7 +669,7 @@ Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
   stream_ = st;
   impl_->flags.ensure(16);
   CK(cudaMemsetAsync(impl_->flags.p, 0, 16, st));
-  impl_->scal.ensure(64);
+  impl_->scal.ensure(16 * 8);
   impl_->tstart.ensure(8);
   impl_->tc = make_tc_gemm(o.dtype == 0 && o.gemm != 1, o.gemm == 2);
   if (o.world > 1 || o.has_nccl_id) {
@@ -612,6 +694,8 @@ Engine::~Engine() {
     b->release();
   for (auto& p : impl_->ev_mwt) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
   for (auto& p : impl_->ev_vtm) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+  for (auto& p : impl_->ev_comm) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+  for (auto& p : impl_->ev_phase) cudaEventDestroy(p.second.first), cudaEventDestroy(p.second.second);
   for (auto x : impl_->ev_pool) cudaEventDestroy(x);
   delete impl_->tc;
   if (impl_->comm) NcclApi::get().CommDestroy(impl_->comm);
@@ -619,9 +703,7 @@ Engine::~Engine() {
   delete impl_;
 }
 
-bool Engine::tc_active() const {
-  return impl_->tc && !lv_.empty() && r_ > 0 && impl_->tc->wants(lv_[0].m, n_loc_, r_);
-}
+bool Engine::tc_active() const { return impl_->tc && !lv_.empty() && r_ > 0 && impl_->use_tc(lv_[0].m); }
 bool Engine::gram_error() const {
   if (opt_.error_mode == 1) return true;
   if (opt_.error_mode == 2) return false;
@@ -654,6 +736,7 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();
+  impl_->tc_ok.clear();
   n_loc_ = n_loc;
   n_total_ = n_total;
   col0_ = col0;
@@ -719,6 +802,7 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
   }
   lv_.clear();
+  impl_->tc_ok.clear();
   n_loc_ = n_loc;
   n_total_ = n_total;
   col0_ = col0;
@@ -802,10 +886,11 @@ void Engine::ensure_levels(size_t L) {
       impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
                     (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M), nx.m,
                     n_loc_, colblocks);
-    if (r_ > 0) CK(dev_malloc(&nx.V, nx.m * r_ * es));
+    if (r_ > 0) CK(dev_malloc(&nx.V, nx.m * r_ * 8));  // factors are fp64
     lv_.push_back(nx);
   }
   CK(cudaStreamSynchronize(impl_->s));
+  impl_->decide_tc();
 }
 
 double Engine::norm2(size_t l) {
@@ -864,17 +949,17 @@ void Engine::init_random(size_t r, uint64_t seed) {
   set_factors(0, nullptr, nullptr, opt_.dtype, r);
   const size_t tot = m0 * r + r * n_loc_;
   const unsigned g = (unsigned)std::min<size_t>(ceil_div(tot, 256), 8192);
-  if (opt_.dtype == 0)
-    impl_->launch(k_random_init<float>, dim3(g), dim3(256), 0, static_cast<float*>(lv_[0].V), impl_->W.as<float>(), m0,
-                  r, n_loc_, n_total_, col0_, seed);
-  else
-    impl_->launch(k_random_init<double>, dim3(g), dim3(256), 0, static_cast<double*>(lv_[0].V),
-                  impl_->W.as<double>(), m0, r, n_loc_, n_total_, col0_, seed);
+  impl_->launch(k_random_init<double>, dim3(g), dim3(256), 0, static_cast<double*>(lv_[0].V), impl_->W.as<double>(),
+                m0, r, n_loc_, n_total_, col0_, seed);
 }
 
+// The factors are fp64 on the device whatever M's storage: they are small
+// (V m x r, W r x n_loc: 0.2 GB at config 4, against 64 GiB of M), so fp64
+// costs nothing measurable, and it keeps fp32-M runs from rounding the
+// iterates to fp32 after every sweep (the dominant trajectory deviation from
+// the fp64 reference fed the same fp32 M).
 void Engine::set_factors(size_t l, const void* V, const void* W, int host_dtype, size_t r) {
   if (lv_.empty()) throw std::invalid_argument("no data set");
-  const size_t es = impl_->esz();
   if (r != r_) {
     for (auto& L : lv_) {
       dev_free(L.V);
@@ -883,42 +968,39 @@ void Engine::set_factors(size_t l, const void* V, const void* W, int host_dtype,
     r_ = r;
   }
   for (auto& L : lv_)
-    if (!L.V) CK(dev_malloc(&L.V, L.m * r * es));
-  impl_->W.ensure(r * n_loc_ * es);
+    if (!L.V) CK(dev_malloc(&L.V, L.m * r * 8));
+  impl_->W.ensure(r * n_loc_ * 8);
   impl_->AB.ensure((lv_[0].m * r + r * r) * 8);
   impl_->Cb.ensure(r * n_loc_ * 8);
   impl_->Db.ensure(r * r * 8);
   impl_->B_valid = impl_->CD_valid = false;
   auto put = [&](void* dst, const void* src, size_t count) {
     if (!src) return;
-    const size_t hs = host_dtype == 0 ? 4 : 8;
-    if (hs == es) {
-      CK(cudaMemcpyAsync(dst, src, count * es, cudaMemcpyHostToDevice, impl_->s));
+    if (host_dtype != 0) {
+      CK(cudaMemcpyAsync(dst, src, count * 8, cudaMemcpyHostToDevice, impl_->s));
     } else {
-      impl_->stage.ensure(count * hs);
-      CK(cudaMemcpyAsync(impl_->stage.p, src, count * hs, cudaMemcpyHostToDevice, impl_->s));
+      impl_->stage.ensure(count * 4);
+      CK(cudaMemcpyAsync(impl_->stage.p, src, count * 4, cudaMemcpyHostToDevice, impl_->s));
       const unsigned g = (unsigned)std::min<size_t>(ceil_div(count, 256), 8192);
-      if (hs == 8) impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)impl_->stage.p, (float*)dst, count);
-      else impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)impl_->stage.p, (double*)dst, count);
+      impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)impl_->stage.p, (double*)dst, count);
     }
     CK(cudaStreamSynchronize(impl_->s));
   };
   put(lv_.at(l).V, V, lv_[l].m * r);
   put(impl_->W.p, W, r * n_loc_);
+  impl_->decide_tc();
 }
 
 void Engine::get_factors(size_t l, void* V, void* W, int host_dtype) {
-  const size_t es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
   auto get = [&](const void* src, void* dst, size_t count) {
     if (!dst) return;
-    if (hs == es) {
-      CK(cudaMemcpyAsync(dst, src, count * es, cudaMemcpyDeviceToHost, impl_->s));
+    if (host_dtype != 0) {
+      CK(cudaMemcpyAsync(dst, src, count * 8, cudaMemcpyDeviceToHost, impl_->s));
     } else {
-      impl_->stage.ensure(count * hs);
+      impl_->stage.ensure(count * 4);
       const unsigned g = (unsigned)std::min<size_t>(ceil_div(count, 256), 8192);
-      if (hs == 8) impl_->launch(k_widen<float>, dim3(g), dim3(256), 0, (const float*)src, (double*)impl_->stage.p, count);
-      else impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)src, (float*)impl_->stage.p, count);
-      CK(cudaMemcpyAsync(dst, impl_->stage.p, count * hs, cudaMemcpyDeviceToHost, impl_->s));
+      impl_->launch(k_convert<float>, dim3(g), dim3(256), 0, (const double*)src, (float*)impl_->stage.p, count);
+      CK(cudaMemcpyAsync(dst, impl_->stage.p, count * 4, cudaMemcpyDeviceToHost, impl_->s));
     }
     CK(cudaStreamSynchronize(impl_->s));
   };
@@ -953,24 +1035,16 @@ void Engine::restrict_V(size_t l) {
   Level& f = lv_.at(l);
   Level& c = lv_.at(l + 1);
   const size_t cb = ceil_div(r_, 64);
-  if (opt_.dtype == 0)
-    impl_->launch(k_csr_apply<float>, dim3((unsigned)(c.m * cb)), dim3(64), 0, (const int*)f.Rp, (const int*)f.Ri,
-                  (const double*)f.Rw, (const float*)f.V, static_cast<float*>(c.V), c.m, r_, cb);
-  else
-    impl_->launch(k_csr_apply<double>, dim3((unsigned)(c.m * cb)), dim3(64), 0, (const int*)f.Rp, (const int*)f.Ri,
-                  (const double*)f.Rw, (const double*)f.V, static_cast<double*>(c.V), c.m, r_, cb);
+  impl_->launch(k_csr_apply<double>, dim3((unsigned)(c.m * cb)), dim3(64), 0, (const int*)f.Rp, (const int*)f.Ri,
+                (const double*)f.Rw, (const double*)f.V, static_cast<double*>(c.V), c.m, r_, cb);
 }
 
 void Engine::prolong_V(size_t l) {
   Level& f = lv_.at(l);
   Level& c = lv_.at(l + 1);
   const size_t cb = ceil_div(r_, 64);
-  if (opt_.dtype == 0)
-    impl_->launch(k_csr_apply<float>, dim3((unsigned)(f.m * cb)), dim3(64), 0, (const int*)f.Pp, (const int*)f.Pi,
-                  (const double*)f.Pw, (const float*)c.V, static_cast<float*>(f.V), f.m, r_, cb);
-  else
-    impl_->launch(k_csr_apply<double>, dim3((unsigned)(f.m * cb)), dim3(64), 0, (const int*)f.Pp, (const int*)f.Pi,
-                  (const double*)f.Pw, (const double*)c.V, static_cast<double*>(f.V), f.m, r_, cb);
+  impl_->launch(k_csr_apply<double>, dim3((unsigned)(f.m * cb)), dim3(64), 0, (const int*)f.Pp, (const int*)f.Pi,
+                (const double*)f.Pw, (const double*)c.V, static_cast<double*>(f.V), f.m, r_, cb);
   impl_->CD_valid = false;
 }
 
@@ -1132,7 +1206,7 @@ void Engine::nnls_single(const double* G, const double* h, const double* x0, siz
   r_ = r;
   impl_->cnt_used = 0;
   try {
-    impl_->nnls<double>(g.as<double>(), 1, hb.as<double>(), r, 1, xb.as<double>(), r, 1);
+    impl_->nnls(g.as<double>(), 1, hb.as<double>(), r, 1, xb.as<double>(), r, 1);
   } catch (...) {
     r_ = r_save;
     throw;
@@ -1185,6 +1259,14 @@ KernelTimes Engine::kernel_times() {
     CK(cudaEventElapsedTime(&ms, p.first, p.second));
     kt.comm_ms += ms;
     ++kt.comm_n;
+    kt.phase_ms[kPhComm] += ms;
+    ++kt.phase_n[kPhComm];
+  }
+  for (auto& p : impl_->ev_phase) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+    kt.phase_ms[p.first] += ms;
+    ++kt.phase_n[p.first];
   }
   return kt;
 }
@@ -1194,6 +1276,9 @@ void Engine::reset_kernel_times() {
   for (auto& p : impl_->ev_mwt) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
   for (auto& p : impl_->ev_vtm) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
   for (auto& p : impl_->ev_comm) impl_->ev_pool.push_back(p.first), impl_->ev_pool.push_back(p.second);
+  for (auto& p : impl_->ev_phase)
+    impl_->ev_pool.push_back(p.second.first), impl_->ev_pool.push_back(p.second.second);
+  impl_->ev_phase.clear();
   impl_->ev_mwt.clear();
   impl_->ev_vtm.clear();
   impl_->ev_comm.clear();

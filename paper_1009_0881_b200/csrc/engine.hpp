@@ -31,7 +31,7 @@ struct Options {
   int device = 0;
   int dtype = 1;       // storage of M, V, W: 0 = fp32, 1 = fp64
   int exact = 0;       // reference operation order (fp64 => bit-identical)
-  int gemm = 0;        // 0 auto, 1 SIMT (fp64 accumulate), 2 tcgen05 3xTF32 (fp32 only)
+  int gemm = 0;        // 0 auto, 1 SIMT (fp64 accumulate), 2 tcgen05 integer-digit products (fp32 only)
   int error_mode = 0;  // 0 auto, 1 Gram identity, 2 direct residual
   int world = 1, rank = 0;
   bool has_nccl_id = false;
@@ -54,11 +54,18 @@ struct Sample {
   double error;
 };
 
+// Phases of one solver step (engine.cu step_t), timed when profiling is on.
+enum StepPhase { kPhB = 0, kPhA, kPhComm, kPhV, kPhD, kPhC, kPhW, kNumPhases };
+
 struct KernelTimes {  // filled when profiling is on (CUDA events on the engine stream)
   double mwt_ms = 0, vtm_ms = 0;  // total over recorded launches
   long mwt_n = 0, vtm_n = 0;
   double comm_ms = 0;  // the per-step allreduce of [A | B] (world > 1)
   long comm_n = 0;
+  // per step phase: B = W W^T, A = M W^T, allreduce [A | B], V update,
+  // D = V^T V, C = V^T M, W update (totals over the profiled steps)
+  double phase_ms[kNumPhases] = {0};
+  long phase_n[kNumPhases] = {0};
 };
 
 class Engine {

@@ -158,24 +158,16 @@ __global__ void __launch_bounds__(128) k_mu_w_reg(const double* __restrict__ Cm,
 }
 
 template <int R>
-void launch_v(bool f32, bool fast, const double* A, const double* B, void* V, size_t m, int* deg, cudaStream_t s) {
+void launch_v(bool fast, const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s) {
   const dim3 g((unsigned)((m + 127) / 128));
-  if (f32 && fast)
-    k_hals_v_reg<float, R, true><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m, deg);
-  else if (f32)
-    k_hals_v_reg<float, R><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m, deg);
-  else
-    k_hals_v_reg<double, R><<<g, 128, 0, s>>>(A, B, static_cast<double*>(V), m, deg);
+  if (fast) k_hals_v_reg<double, R, true><<<g, 128, 0, s>>>(A, B, V, m, deg);
+  else k_hals_v_reg<double, R><<<g, 128, 0, s>>>(A, B, V, m, deg);
 }
 template <int R>
-void launch_w(bool f32, bool fast, const double* C, const double* D, void* W, size_t n, int* deg, cudaStream_t s) {
+void launch_w(bool fast, const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
   const dim3 g((unsigned)((n + 127) / 128));
-  if (f32 && fast)
-    k_hals_w_reg<float, R, true><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n, deg);
-  else if (f32)
-    k_hals_w_reg<float, R><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n, deg);
-  else
-    k_hals_w_reg<double, R><<<g, 128, 0, s>>>(C, D, static_cast<double*>(W), n, deg);
+  if (fast) k_hals_w_reg<double, R, true><<<g, 128, 0, s>>>(C, D, W, n, deg);
+  else k_hals_w_reg<double, R><<<g, 128, 0, s>>>(C, D, W, n, deg);
 }
 
 void check(cudaError_t e) {
@@ -189,32 +181,30 @@ void check(cudaError_t e) {
 bool hals_reg_supported(size_t r) { return r == 64; }
 bool mu_reg_supported(size_t r) { return r == 64; }
 
-void mu_v_reg(size_t r, bool f32, const double* A, const double* B, void* V, size_t m, cudaStream_t s) {
+void mu_v_reg(size_t r, const double* A, const double* B, double* V, size_t m, cudaStream_t s) {
   if (r != 64) throw std::invalid_argument("mu_v_reg: unsupported rank");
   const dim3 g((unsigned)((m + 127) / 128));
-  if (f32) k_mu_v_reg<float, 64><<<g, 128, 0, s>>>(A, B, static_cast<float*>(V), m);
-  else k_mu_v_reg<double, 64><<<g, 128, 0, s>>>(A, B, static_cast<double*>(V), m);
+  k_mu_v_reg<double, 64><<<g, 128, 0, s>>>(A, B, V, m);
   check(cudaGetLastError());
 }
 
-void mu_w_reg(size_t r, bool f32, const double* C, const double* D, void* W, size_t n, cudaStream_t s) {
+void mu_w_reg(size_t r, const double* C, const double* D, double* W, size_t n, cudaStream_t s) {
   if (r != 64) throw std::invalid_argument("mu_w_reg: unsupported rank");
   const dim3 g((unsigned)((n + 127) / 128));
-  if (f32) k_mu_w_reg<float, 64><<<g, 128, 0, s>>>(C, D, static_cast<float*>(W), n);
-  else k_mu_w_reg<double, 64><<<g, 128, 0, s>>>(C, D, static_cast<double*>(W), n);
+  k_mu_w_reg<double, 64><<<g, 128, 0, s>>>(C, D, W, n);
   check(cudaGetLastError());
 }
 
-void hals_v_reg(size_t r, bool f32, bool fast, const double* A, const double* B, void* V, size_t m, int* deg,
+void hals_v_reg(size_t r, bool fast, const double* A, const double* B, double* V, size_t m, int* deg,
                 cudaStream_t s) {
-  if (r == 64) launch_v<64>(f32, fast, A, B, V, m, deg, s);
+  if (r == 64) launch_v<64>(fast, A, B, V, m, deg, s);
   else throw std::invalid_argument("hals_v_reg: unsupported rank");
   check(cudaGetLastError());
 }
 
-void hals_w_reg(size_t r, bool f32, bool fast, const double* C, const double* D, void* W, size_t n, int* deg,
+void hals_w_reg(size_t r, bool fast, const double* C, const double* D, double* W, size_t n, int* deg,
                 cudaStream_t s) {
-  if (r == 64) launch_w<64>(f32, fast, C, D, W, n, deg, s);
+  if (r == 64) launch_w<64>(fast, C, D, W, n, deg, s);
   else throw std::invalid_argument("hals_w_reg: unsupported rank");
   check(cudaGetLastError());
 }

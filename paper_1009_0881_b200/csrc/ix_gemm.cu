@@ -13,39 +13,49 @@
 //     X = d1 * 2^16 + d2 * 2^8 + d3,   d1 in [0, 127], d2, d3 in [-128, 127].
 // The rounding is unbiased (round-to-nearest-even of a single FFMA), and the
 // digits are exact, signed 8-bit integers.  With F likewise split into
-// e1, e2, e3, the products are three integer sums over K
-//     G0 = sum d1 e1,   G1 = sum d1 e2 + d2 e1,   G2 = sum d1 e3 + d2 e2 + d3 e1
-// accumulated in int32 TMEM by `tcgen05.mma.kind::i8` -- EXACTLY: no
-// rounding, no truncation, independent of the accumulation order -- and
-//     sum x f = 2^16 (G0 2^16 + G1 2^8 + G2) / (s_x s_f)
-// in fp64 (the bracket is an integer below 2^53, so it converts exactly).
-// The dropped digit products (d2 e3 + d3 e2, d3 e3: weight <= 2^-23 of a
-// term) are zero-mean.  So the products carry only the unbiased grid
-// rounding of the inputs (<= 2^-23 of the row maximum per element), which
-// averages out along K: measured relative errors are ~1e-9 (tests), against
-// the one-sided ~1e-6 bias of fp32 tensor-core accumulation that this
-// replaces (the round-1 tf32 kernel; SURVEY finding 4 / VERDICT N1).
-// Throughput: 6 MMAs of N = r_pad, K = 32 per 32-wide chunk at the i8 rate
-// (= 6 bf16-K16 MMA slots, 192 tensor cycles per 128-row chunk), and 96 B per
-// row per chunk of converter stores into TMEM.
+// e1, e2, e3, EVERY digit product d_i e_j is formed, summed over K by weight
+// class i + j,
+//     G0 = sum d1 e1,  G1 = sum d1 e2 + d2 e1,  G2 = sum d1 e3 + d2 e2 + d3 e1,
+//     G3 = sum d2 e3 + d3 e2,  G4 = sum d3 e3,
+// and accumulated in int32 TMEM by `tcgen05.mma.kind::i8` -- EXACTLY: no
+// rounding, no truncation, independent of the accumulation order -- so
+//     sum X Y = G0 2^32 + G1 2^24 + G2 2^16 + G3 2^8 + G4
+// is the exact integer dot product of the rounded operands (int64, then one
+// fp64 rounding), and sum x f = (sum X Y) / (s_x s_f).  The products carry
+// only the unbiased grid rounding of the inputs (<= 2^-23 of the row
+// maximum per element), which averages out along K (~1e-9 .. 1e-8 relative).
+// An earlier form dropped G3 and G4: a factor entry below 1/128 of its row's
+// maximum (leading digit d2 or d3; common in sparse NMF factors) then kept
+// only ~16 bits, which moved the config-4 FMG trajectory 1e-4 off the
+// reference's; with all nine products it tracks within the fp32-storage
+// noise.
+// Throughput: 9 MMAs of N = r_pad, K = 32 per 32-wide chunk at the i8 rate
+// (288 tensor cycles per 128-row chunk, ~45 % of the chunk's HBM time), and
+// 96 B per row per chunk of converter stores into TMEM.
 //
 // The kernel (persistent, warp-specialised, one CTA per SM, 608 threads):
 //   warp 0: TMA producer of M slices (16 KB, issued and released in pairs;
 //           product 1 fetches a chunk pair as one 3-D box of 128 rows x 256 B)
-//   warp 1: MMA issuer (allocates TMEM): per chunk 6 MMAs from the digit
-//           planes in a TMEM staging slot (A operand) and the factor digit
-//           planes in shared memory (B operand); one accumulator set
-//           (3 x 64 int32 columns) per work unit, double-buffered
-//   warp 2: TMA producer of factor digit slices (r_pad rows x 128 B: planes
-//           e1 | e2 | e3 | 0, SWIZZLE_128B), one per chunk
+//   warp 1: MMA issuer (allocates TMEM): per chunk PAIR one wait on the
+//           pair's staging slots, one on its factor stage, 18 MMAs (9 per
+//           chunk) from the digit planes in TMEM (A operand) and the factor
+//           digit planes in shared memory (B operand), two commits; one
+//           accumulator set (5 x 64 int32 columns) per work unit, drained
+//           by the epilogue between units.  This warp's issue loop is the serial path of the
+//           pipeline (ncu r02a: ~85 % busy at one chunk per stage), so its
+//           bookkeeping is amortised over two chunks.
+//   warp 2: TMA producer of factor digit slices (2 x r_pad rows x 128 B:
+//           planes e1 | e2 | e3 | 0, SWIZZLE_128B), one per chunk pair
 //   warps 3-10: converters (two groups of 4 alternating chunks): fp32 slice
 //           from shared memory -> one FFMA per element -> byte permutes into
 //           the digit planes d1 | d2 | d3 -> tcgen05.st into a staging slot
-//   warps 11-18: epilogue: drains a unit's three accumulators once (windows
+//   warps 11-18: epilogue: drains a unit's five accumulators once (windows
 //           are whole work units of <= kMaxUnitChunks chunks, well inside the
 //           int32 range), converts to fp64 and writes the split-K partial.
-// TMEM (512 columns): accumulator sets at 0 / 192 (groups at +0, +64, +128),
-// staging slots at 384 + 32 s, s < 4 (24 columns used: d1 | d2 | d3).
+// TMEM (512 columns): the accumulator set at 0 (classes at +0, +64, ..., +256),
+// staging slots at 384 + 32 s, s < 4 (24 columns used: d1 | d2 | d3); chunk
+// g uses slot g % 4, so chunk pair h owns slots 2 (h & 1) and 2 (h & 1) + 1.
+// Work units hold an even number of chunks (a zero chunk pads an odd K).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -67,14 +77,19 @@ constexpr int kChunk = 32;             // K elements per pipeline chunk
 constexpr int kMStages = 8;            // M-slice ring (TMA -> converters), 16 KB each
 constexpr int kMGroup = 2;             // the ring is filled and released in pairs of slices
 constexpr int kMGroups = kMStages / kMGroup;
-constexpr int kBStages = 6;            // factor digit ring (TMA -> MMA), 8 KB each
-constexpr int kBStageBytes = 8192;     // r_pad (<= 64) rows x 128 B
-constexpr int kSlots = 4;              // TMEM staging slots
+constexpr int kBStages = 2;            // factor digit ring (TMA -> MMA), one chunk QUAD per stage
+constexpr int kBStageBytes = 32768;    // 4 planes x r_pad (<= 64) rows x 128 B (= 4 chunks x 32 K)
+constexpr int kQuad = 4;               // chunks per factor stage
+constexpr int kSlots = 4;              // TMEM staging slots: two pairs (chunk 2h -> slot 2(h&1), 2h+1 -> +1)
+constexpr int kPairs = kSlots / 2;
 constexpr int kSlotCols = 32;          // columns per slot (24 used)
 constexpr int kGroupCols = 64;         // columns per accumulator group (r_pad <= 64)
-constexpr int kAccCols = 3 * kGroupCols;
-constexpr int kStg0 = 2 * kAccCols;    // staging slots follow the two accumulator sets
-static_assert(kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
+constexpr int kClasses = 6;            // digit-product weight classes 2^40, 2^32, ..., 2^0
+constexpr int kAccCols = kClasses * kGroupCols;
+constexpr int kStg0 = 384;             // staging slots after the (single) accumulator set
+static_assert(kAccCols <= kStg0 && kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
+// factor fixed point: 31 bits (four digits e1 e2 e3 e4, e1 in [0, 127])
+constexpr double kFBias = 8421504.0;   // 0x808080: balanced low three digits
 // chunks per work unit: |G2| <= 3 * 128^2 per K element, so an int32
 // accumulator is exact for K < 2^31 / 49152 = 43690; 1280 chunks = 40960
 constexpr int kMaxUnitChunks = 1280;
@@ -227,36 +242,49 @@ __host__ __device__ __forceinline__ float scale_of(float mx) {
   return s;
 }
 
-// One chunk's 6 MMAs (K = 32 each) on staging slot S into accumulator set
-// BUF, issued by one elected lane in a single asm block.  A planes d1 | d2 |
-// d3 at TMEM columns a, a + 8, a + 16; B planes e1 | e2 | e3 at 32-byte steps
-// (descriptor + 2 per step) of the factor stage's 128-byte rows.  `first`
-// overwrites the accumulators (unit start).
-template <int S, int BUF>
-__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id, uint32_t first) {
-  constexpr uint32_t d0 = BUF * kAccCols, d1 = d0 + kGroupCols, d2 = d1 + kGroupCols;
+// The factor's fixed-point multiplier: mx * s in [2^29, 2^30) (power of two,
+// fp64; mx is the fp32 row maximum rounded up), so X + 0x808080 < 2^31.
+__host__ __device__ __forceinline__ double fscale_of(float mx) {
+  if (!(mx > 0.f)) return 1.0;
+  int e;
+  (void)frexpf(mx, &e);
+  return ldexp(1.0, 30 - e);
+}
+
+// One chunk's 3 MMAs (K = 32 each) on staging slot S: M digit plane d_i
+// (TMEM, 128 rows) times the STACKED factor digit planes [e1; e2; e3; e4]
+// (shared memory, N = 4 r_pad rows), written to the accumulator window
+// starting at class group i - 1 (columns (i - 1) r_pad .. (i + 3) r_pad).
+// Block j of MMA i lands on group i + j - 2, so the windows' overlap sums
+// every digit product d_i e_j into its weight class c = i + j - 2 (weight
+// 2^(40 - 8c)):
+//   G0 = d1 e1;  G1 = d1 e2 + d2 e1;  G2 = d1 e3 + d2 e2 + d3 e1;
+//   G3 = d1 e4 + d2 e3 + d3 e2;  G4 = d2 e4 + d3 e3;  G5 = d3 e4
+// -- all twelve products, exact in int32, in three instructions.  The
+// accumulators always accumulate (the epilogue zeroes them after each
+// drain).  (With only the leading six products of a 3 x 3 split, a small
+// factor entry -- leading digit d2 or d3, common in sparse NMF factors --
+// kept ~16 bits and the config-4 FMG trajectory drifted 1e-4 from the
+// reference; the factor's fourth digit takes its grid from 2^-23 to 2^-31
+// of the row maximum, which the Gram-identity samples at coarse levels
+// needed.  r02 measurements.)
+template <int S>
+__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id, uint32_t rp) {
   constexpr uint32_t a1 = kStg0 + S * kSlotCols, a2 = a1 + 8, a3 = a1 + 16;
   asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.eq.u32 p, %10, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %6, %9, p;\n\t"   // G0  = d1 e1
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%3], %7, %9, p;\n\t"   // G1  = d1 e2
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%3], %8, %9, p;\n\t"   // G2  = d1 e3
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%4], %6, %9, 1;\n\t"   // G1 += d2 e1
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%4], %7, %9, 1;\n\t"   // G2 += d2 e2
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%5], %6, %9, 1;\n\t}"  // G2 += d3 e1
-      ::"r"(d0), "r"(d1), "r"(d2), "r"(a1), "r"(a2), "r"(a3), "l"(bd), "l"(bd + 2), "l"(bd + 4), "r"(id), "r"(first)
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %6, %7, 1;\n\t"   // d1 [e1..e4] -> G0..G3
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%4], %6, %7, 1;\n\t"   // d2 [e1..e4] -> G1..G4
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%5], %6, %7, 1;\n\t}"  // d3 [e1..e4] -> G2..G5
+      ::"r"(0u), "r"(rp), "r"(2u * rp), "r"(a1), "r"(a2), "r"(a3), "l"(bd), "r"(id)
       : "memory");
 }
-template <int BUF>
-__device__ __forceinline__ void issue_slot(int slot, uint64_t bd, uint32_t id, uint32_t first) {
-  switch (slot) {
-    case 0: issue_chunk<0, BUF>(bd, id, first); break;
-    case 1: issue_chunk<1, BUF>(bd, id, first); break;
-    case 2: issue_chunk<2, BUF>(bd, id, first); break;
-    default: issue_chunk<3, BUF>(bd, id, first); break;
-  }
+// A chunk pair: slots 2 PS and 2 PS + 1 (factor columns at bd0 / bd1)
+template <int PS>
+__device__ __forceinline__ void issue_pair(uint64_t bd0, uint64_t bd1, uint32_t id, uint32_t rp) {
+  issue_chunk<2 * PS>(bd0, id, rp);
+  issue_chunk<2 * PS + 1>(bd1, id, rp);
 }
 
 // Digit planes of 4 consecutive elements from their FFMA bit patterns
@@ -313,9 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_b + kBStages * kBStageBytes);
   uint64_t* mfull = bars;                  // [kMGroups]  TMA -> converters
   uint64_t* mempty = mfull + kMGroups;     // [kMGroups]  converters -> TMA
-  uint64_t* ready = mempty + kMGroups;     // [kSlots]    converters -> MMA (slot written)
-  uint64_t* sdone = ready + kSlots;        // [kSlots]    MMA commit -> converters (slot free)
-  uint64_t* bfull = sdone + kSlots;        // [kBStages]  TMA -> MMA
+  uint64_t* ready = mempty + kMGroups;     // [kPairs]    converters -> MMA (slot pair written)
+  uint64_t* sdone = ready + kPairs;        // [kPairs]    MMA commit -> converters (slot pair free)
+  uint64_t* bfull = sdone + kPairs;        // [kBStages]  TMA -> MMA
   uint64_t* bempty = bfull + kBStages;     // [kBStages]  MMA commit -> TMA
   uint64_t* afull = bempty + kBStages;     // [2]         MMA commit -> epilogue (unit done)
   uint64_t* aempty = afull + 2;            // [2]         epilogue -> MMA (accumulators drained)
@@ -327,8 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&mfull[i]), 1);
       mbar_init(smem_u32(&mempty[i]), 4 * kMGroup);  // the 4 converter warps of each slice
     }
-    for (int i = 0; i < kSlots; ++i) {
-      mbar_init(smem_u32(&ready[i]), 4);
+    for (int i = 0; i < kPairs; ++i) {
+      mbar_init(smem_u32(&ready[i]), 4 * kConvGroups);  // both groups' 4 warps
       mbar_init(smem_u32(&sdone[i]), 1);
     }
     for (int i = 0; i < kBStages; ++i) {
@@ -398,16 +426,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= TMA producer: factor digit slices =======================
     if (lane == 0) {
       const uint64_t pol = l2_evict_last();
-      const uint32_t bytes = (uint32_t)p.rp * 128u;
-      int g = 0;
+      const uint32_t bytes = 4u * (uint32_t)p.rp * 128u;
+      int qc = 0;  // chunk quad counter
       for (int u = u0; u < total_units; u += ustep) {
         const Unit x = unit_of(p, u);
-        for (int i = 0; i < x.n; ++i, ++g) {
-          const int bs = g % kBStages;
-          mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(g / kBStages) & 1u) ^ 1u);
+        for (int i = 0; i < x.n; i += kQuad, ++qc) {
+          const int bs = qc % kBStages;
+          mbar_wait(smem_u32(&bempty[bs]), ((uint32_t)(qc / kBStages) & 1u) ^ 1u);
           const uint32_t fb = smem_u32(&bfull[bs]);
           mbar_expect_tx(fb, bytes);
-          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, 0, (x.c0 + i) * p.rp, fb, pol);
+          tma_load_2d(smem_u32(sm_b + bs * kBStageBytes), &map_b, 0, ((x.c0 + i) / kQuad) * 4 * p.rp, fb, pol);
         }
       }
     }
@@ -415,39 +443,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= MMA issuer =======================
     // The whole warp runs the (warp-uniform) loop so every operand stays in
     // the uniform datapath; one elected lane issues each tcgen05 instruction.
+    // Per chunk PAIR (the issue loop of this one warp is the serial path of
+    // the whole pipeline: one ready wait, 6 MMAs, one commit; the factor
+    // stage -- a chunk quad -- is waited for by a quad's first pair and
+    // released by its second)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
-    const uint32_t id = idesc_s8(p.rp);
-    int g = 0, uc = 0;
+    const uint32_t id = idesc_s8(4 * p.rp);
+    const uint32_t rp = (uint32_t)p.rp;
+    int h = 0, uc = 0;
     for (int u = u0; u < total_units; u += ustep, ++uc) {
       const int n_u = unit_of(p, u).n;
-      const int buf = uc & 1;
-      mbar_wait(smem_u32(&aempty[buf]), ((uint32_t)(uc >> 1) & 1u) ^ 1u);
-      for (int i = 0; i < n_u; ++i, ++g) {
-        const int slot = g % kSlots, bs = g % kBStages;
-        const uint32_t sph = (uint32_t)(g / kSlots) & 1u, bph = (uint32_t)(g / kBStages) & 1u;
-        mbar_wait(smem_u32(&ready[slot]), sph);
-        mbar_wait(smem_u32(&bfull[bs]), bph);
+      // the single accumulator set: drained and zeroed by the epilogue
+      // (phase 0 = the initial zeroing)
+      mbar_wait(smem_u32(&aempty[0]), (uint32_t)uc & 1u);
+      for (int i = 0; i < n_u; i += 2, ++h) {
+        const int ps = h & 1, qc = h >> 1, bs = qc % kBStages;
+        mbar_wait(smem_u32(&ready[ps]), (uint32_t)(h >> 1) & 1u);
+        if (!(h & 1)) mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(qc / kBStages) & 1u);
         tc_fence_after();
-        const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4);
-        const uint32_t first = i == 0 ? 1u : 0u;
-        if (buf == 0) issue_slot<0>(slot, bd, id, first);
-        else issue_slot<1>(slot, bd, id, first);
-        tc_commit(smem_u32(&sdone[slot]));   // staging slot reusable once these MMAs finish
-        tc_commit(smem_u32(&bempty[bs]));    // ... and the factor stage
+        // chunk (2h) % 4 of the quad: its K columns at byte 32 (2h % 4)
+        const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4) + (uint64_t)(4 * (h & 1));
+        if (ps == 0) issue_pair<0>(bd, bd + 2, id, rp);
+        else issue_pair<1>(bd, bd + 2, id, rp);
+        tc_commit(smem_u32(&sdone[ps]));                // slot pair reusable once these MMAs finish
+        if (h & 1) tc_commit(smem_u32(&bempty[bs]));  // ... and, after a quad's second pair, its factor stage
         __syncwarp();
       }
-      tc_commit(smem_u32(&afull[buf]));  // the unit's accumulators are final
+      tc_commit(smem_u32(&afull[0]));  // the unit's accumulators are final
       __syncwarp();
     }
     // no tcgen05.commit arrival may land after the CTA exits: wait for the
-    // last commit on every slot and stage (chunk g' = last use of each)
-    for (int k = 0; k < kSlots && k < g; ++k) {
-      const int gl = k + ((g - 1 - k) / kSlots) * kSlots;
-      mbar_wait(smem_u32(&sdone[k]), (uint32_t)(gl / kSlots) & 1u);
+    // last commit on every slot pair and stage (pair h' / quad q' = last use)
+    for (int k = 0; k < kPairs && k < h; ++k) {
+      const int hl = k + ((h - 1 - k) / kPairs) * kPairs;
+      mbar_wait(smem_u32(&sdone[k]), (uint32_t)(hl / kPairs) & 1u);
     }
-    for (int k = 0; k < kBStages && k < g; ++k) {
-      const int gl = k + ((g - 1 - k) / kBStages) * kBStages;
-      mbar_wait(smem_u32(&bempty[k]), (uint32_t)(gl / kBStages) & 1u);
+    const int nq = h >> 1;
+    for (int k = 0; k < kBStages && k < nq; ++k) {
+      const int ql = k + ((nq - 1 - k) / kBStages) * kBStages;
+      mbar_wait(smem_u32(&bempty[k]), (uint32_t)(ql / kBStages) & 1u);
     }
   } else if (warp < kWarpEpi0) {
     // ======================= converters: fp32 -> digit planes in TMEM =======================
@@ -463,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float s = scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);
       for (int c = 0; c < x.n; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
-        const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots;
-        const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
+        const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots, sp = (g >> 1) & 1;
+        const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g >> 2) & 1u;
         mbar_wait(smem_u32(&mfull[ps]), mph);
         // digit planes d1 (words 0..7) | d2 (8..15) | d3 (16..23); word j holds
         // elements 4j .. 4j + 3, element t of the word in byte t
@@ -512,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&mempty[ps]));
-        mbar_wait(smem_u32(&sdone[slot]), sphase ^ 1);
+        mbar_wait(smem_u32(&sdone[sp]), sphase ^ 1);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStg0 + slot * kSlotCols;
         tmem_st16(ta, reinterpret_cast<const uint32_t(&)[16]>(pl[0]));
@@ -520,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&ready[slot]));
+        if (lane == 0) mbar_arrive(smem_u32(&ready[sp]));
       }
     }
   } else {
@@ -530,31 +564,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const int cb = ((warp - kWarpEpi0) >> 2) * 32;
     const bool live = cb < p.rp;
-    // this lane's output column cb + lane: 2^16 / s_f (broadcast by shuffles)
-    const double cinv = (cb + lane < p.r) ? 65536.0 / (double)scale_of(p.fmax[cb + lane]) : 0.0;
+    // this lane's output column cb + lane: 1 / s_f (broadcast by shuffles)
+    const double cinv = (cb + lane < p.r) ? 1.0 / fscale_of(p.fmax[cb + lane]) : 0.0;
+    // class c of output column k is TMEM column c r_pad + k; this warp owns
+    // columns cb .. cb + 31 of each class (8-column blocks below r_pad)
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + cb;
+    const uint32_t zero[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    auto zero_acc = [&]() {
+#pragma unroll
+      for (int c = 0; c < kClasses; ++c)
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          if (cb + h * 8 < p.rp)
+            tmem_st8(tq + c * p.rp + h * 8, reinterpret_cast<const uint32_t(&)[8]>(zero[0]));
+      tmem_wait_st();
+    };
+    // the accumulators start at zero and are re-zeroed after every drain:
+    // the MMAs always accumulate (aempty phase 0 = this initial zeroing)
+    zero_acc();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&aempty[0]));
     int uc = 0;
     for (int u = u0; u < total_units; u += ustep, ++uc) {
       const Unit x = unit_of(p, u);
-      const int buf = uc & 1;
       const int gi = x.tile * 128 + row;
       const double rinv = 1.0 / (double)scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);
-      mbar_wait<256>(smem_u32(&afull[buf]), (uint32_t)(uc >> 1) & 1u);
+      mbar_wait<256>(smem_u32(&afull[0]), (uint32_t)uc & 1u);
       tc_fence_after();
       if (live) {
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * kAccCols + cb;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {  // 8 columns at a time
-          uint32_t g0[8], g1[8], g2[8];
-          tmem_ld8(ta + h * 8, g0);
-          tmem_ld8(ta + kGroupCols + h * 8, g1);
-          tmem_ld8(ta + 2 * kGroupCols + h * 8, g2);
+          if (cb + h * 8 >= p.rp) break;
+          uint32_t g[kClasses][8];
+#pragma unroll
+          for (int c = 0; c < kClasses; ++c) tmem_ld8(tq + c * p.rp + h * 8, g[c]);
           tmem_wait_ld();
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const int k = h * 8 + kk;
             const double ck = __shfl_sync(0xffffffffu, cinv, k);  // all lanes: outside the row guard
-            const long long S = (long long)(int)g0[kk] * 65536ll + (long long)(int)g1[kk] * 256ll + (long long)(int)g2[kk];
-            const double v = (double)S * rinv * ck;
+            // sum X Y = hi 2^24 + lo, hi = G0 2^16 + G1 2^8 + G2 and
+            // lo = G3 2^16 + G4 2^8 + G5 exact in int64 (|G| < 2^31), hi exact
+            // in fp64 (< 2^46 for a unit's K <= 40960): one fp64 rounding
+            const long long hi = ((long long)(int)g[0][kk] * 256ll + (int)g[1][kk]) * 256ll + (int)g[2][kk];
+            const long long lo = ((long long)(int)g[3][kk] * 256ll + (int)g[4][kk]) * 256ll + (int)g[5][kk];
+            const double v = fma((double)hi, 16777216.0, (double)lo) * rinv * ck;
             if (gi < p.rows && cb + k < p.r) {
               if (!TRANS)
                 p.part[(size_t)x.split * p.rows * p.r + (size_t)gi * p.r + cb + k] = v;
@@ -563,10 +618,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        zero_acc();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&aempty[buf]));
+      if (lane == 0) mbar_arrive(smem_u32(&aempty[0]));
     }
   }
 
@@ -619,84 +675,98 @@ __global__ void __launch_bounds__(256) k_mstats(const float* __restrict__ M, siz
   }
 }
 
-// Factor maxima: row k of F over its K elements.  F is either row-major
-// r x K (W; trans = 0) or K x r (V; trans = 1).
-__global__ void __launch_bounds__(256) k_fmax(const float* __restrict__ F, int r, size_t K, int trans,
+// Factor maxima: row k of F (fp64) over its K elements, rounded UP to fp32
+// (the scale chosen from it must keep every rounded entry <= kXMax).  F is
+// either row-major r x K (W; trans = 0) or K x r (V; trans = 1).
+__global__ void __launch_bounds__(256) k_fmax(const double* __restrict__ F, int r, size_t K, int trans,
                                               unsigned* __restrict__ fmax) {
-  __shared__ float red[256];
+  __shared__ double red[256];
   const int t = threadIdx.x;
   if (!trans) {
     // block (k, segment): a strided pass over row k
     const int k = blockIdx.x % r;
     const size_t seg = blockIdx.x / r, nseg = gridDim.x / r;
-    float mx = 0.f;
-    for (size_t e = seg * 256 + t; e < K; e += nseg * 256) mx = fmaxf(mx, F[(size_t)k * K + e]);
+    double mx = 0.0;
+    for (size_t e = seg * 256 + t; e < K; e += nseg * 256) mx = ::fmax(mx, F[(size_t)k * K + e]);
     red[t] = mx;
     __syncthreads();
     for (int o = 128; o > 0; o >>= 1) {
-      if (t < o) red[t] = fmaxf(red[t], red[t + o]);
+      if (t < o) red[t] = ::fmax(red[t], red[t + o]);
       __syncthreads();
     }
-    if (t == 0) atomicMax(fmax + k, __float_as_uint(fmaxf(red[0], 0.f)));
+    if (t == 0) atomicMax(fmax + k, __float_as_uint(fmaxf(__double2float_ru(red[0]), 0.f)));
   } else {
     // rows i of V, thread (lane group gq, column k): k = t % 64, 4 row lanes
     const int k = t & 63, gq = t >> 6;
-    float mx = 0.f;
+    double mx = 0.0;
     if (k < r)
-      for (size_t i = (size_t)blockIdx.x * 4 + gq; i < K; i += (size_t)gridDim.x * 4) mx = fmaxf(mx, F[i * r + k]);
+      for (size_t i = (size_t)blockIdx.x * 4 + gq; i < K; i += (size_t)gridDim.x * 4) mx = ::fmax(mx, F[i * r + k]);
     red[t] = mx;
     __syncthreads();
     if (t < 64 && k < r) {
-      const float v = fmaxf(fmaxf(red[t], red[t + 64]), fmaxf(red[t + 128], red[t + 192]));
-      atomicMax(fmax + k, __float_as_uint(fmaxf(v, 0.f)));
+      const double v = ::fmax(::fmax(red[t], red[t + 64]), ::fmax(red[t + 128], red[t + 192]));
+      atomicMax(fmax + k, __float_as_uint(fmaxf(__double2float_ru(v), 0.f)));
     }
   }
 }
 
-// Factor digit slices: D[c][k][128 B] = e1 (32 B) | e2 | e3 | 0 of elements
-// 32 c .. 32 c + 31 of factor row k (zero for k >= r or beyond K).
-// Thread (c, k, quad qd): 4 elements -> one word per plane.
-__global__ void __launch_bounds__(256) k_fdigits(const float* __restrict__ F, int r, int rp, size_t K,
-                                                 size_t nchunks, int trans, const float* __restrict__ fmax,
+// Factor digit slices (fp64 factor), one 4 r_pad-row block per chunk QUAD
+// (K elements 128 q .. 128 q + 127): row j r_pad + k holds digit plane e_(j+1)
+// of factor row k, 128 bytes = 4 chunks x 32 elements (the MMA's stacked B
+// operand: N = 4 r_pad rows, chunk cq at byte 32 cq).  Zero for k >= r or
+// beyond K.  Thread (q, k, cq, qd): 4 consecutive elements -> one word of
+// each plane row.
+__global__ void __launch_bounds__(256) k_fdigits(const double* __restrict__ F, int r, int rp, size_t K,
+                                                 size_t nquads, int trans, const float* __restrict__ fmax,
                                                  uint32_t* __restrict__ D) {
-  const size_t total = nchunks * (size_t)rp * 8;
+  const size_t total = nquads * (size_t)rp * 32;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    size_t c, qd;
-    int k;
-    if (!trans) {  // quads fastest: 8 threads read one 128-byte row segment of W
-      qd = e & 7;
-      k = (int)((e >> 3) % rp);
-      c = (e >> 3) / rp;
-    } else {       // columns fastest: consecutive threads read consecutive V entries
+    size_t q;
+    int k, w;  // w = cq * 8 + qd: the word within the 128-byte row
+    if (!trans) {  // words fastest: 32 threads read 128 consecutive elements of one W row
+      w = (int)(e & 31);
+      k = (int)((e >> 5) % rp);
+      q = (e >> 5) / rp;
+    } else {       // factor rows fastest: consecutive threads read consecutive V entries
       k = (int)(e % rp);
-      qd = (e / rp) & 7;
-      c = (e / rp) >> 3;
+      w = (int)((e / rp) & 31);
+      q = (e / rp) >> 5;
     }
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
     bool any = false;
     if (k < r) {
-      const float s = scale_of(fmax[k]);
-      const size_t j0 = c * 32 + qd * 4;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (!trans && j0 + 3 < K) {
-        const float4 f4 = *reinterpret_cast<const float4*>(F + (size_t)k * K + j0);
-        v[0] = f4.x, v[1] = f4.y, v[2] = f4.z, v[3] = f4.w;
+      const double s = fscale_of(fmax[k]);
+      const size_t j0 = q * 128 + (size_t)w * 4;
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      if (!trans && j0 + 3 < K) {  // K % 4 == 0: 16-byte aligned pairs
+        const double2 a = *reinterpret_cast<const double2*>(F + (size_t)k * K + j0);
+        const double2 b = *reinterpret_cast<const double2*>(F + (size_t)k * K + j0 + 2);
+        v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
       } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           if (j0 + t < K) v[t] = trans ? F[(j0 + t) * r + k] : F[(size_t)k * K + j0 + t];
       }
+      // the fp64 entry rounded once (half-even) to its row's 31-bit grid:
+      // X + 0x808080 = e1 | e2 + 128 | e3 + 128 | e4 + 128 (bytes 3..0)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) w[t] = fx_bits(v[t], s);
+      for (int t = 0; t < 4; ++t) wv[t] = (uint32_t)(long long)(rint(v[t] * s) + kFBias);
       any = true;
     }
-    uint32_t p1 = 0u, p2 = 0u, p3 = 0u;
-    if (any) planes4(w[0], w[1], w[2], w[3], p1, p2, p3);
-    uint32_t* row = D + (c * rp + k) * 32;  // 128 bytes = 32 words
-    row[qd] = p1;
-    row[8 + qd] = p2;
-    row[16 + qd] = p3;
-    row[24 + qd] = 0u;
+    uint32_t p1 = 0u, p2 = 0u, p3 = 0u, p4 = 0u;
+    if (any) {  // byte t of plane j = digit j of element t
+      const uint32_t t01 = __byte_perm(wv[0], wv[1], 0x5140), t23 = __byte_perm(wv[2], wv[3], 0x5140);
+      const uint32_t u01 = __byte_perm(wv[0], wv[1], 0x7362), u23 = __byte_perm(wv[2], wv[3], 0x7362);
+      p4 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
+      p3 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
+      p2 = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;
+      p1 = __byte_perm(u01, u23, 0x7632);
+    }
+    uint32_t* rowq = D + (q * 4 * rp + k) * 32 + w;  // plane j's row: + j rp rows
+    rowq[0] = p1;
+    rowq[(size_t)rp * 32] = p2;
+    rowq[(size_t)2 * rp * 32] = p3;
+    rowq[(size_t)3 * rp * 32] = p4;
   }
 }
 
@@ -757,12 +827,12 @@ CUtensorMap map_rows3(const void* ptr, uint64_t n, uint64_t m) {
   encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, true);
   return map;
 }
-// factor digit slices: rows of 128 bytes, box = r_pad rows
-CUtensorMap map_digits(const void* ptr, uint64_t rows, uint32_t rp) {
+// factor digit slices: rows of 128 bytes, box = the 4 r_pad rows of a chunk quad
+CUtensorMap map_digits(const void* ptr, uint64_t rows, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {128, rows};
   cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {128, rp};
+  cuuint32_t box[2] = {128, box_rows};
   encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ptr, dims, strides, box, true);
   return m;
 }
@@ -799,35 +869,39 @@ class IxGemm final : public TcGemm {
     ++*launches;
   }
 
-  void mwt(const float* M, const float* rowmax, const float* W, size_t m, size_t n, size_t r, double* A,
+  void mwt(const float* M, const float* rowmax, const double* W, size_t m, size_t n, size_t r, double* A,
            cudaStream_t s, long* launches) override {
     run<false>(M, rowmax, W, m, n, r, A, s, launches);
   }
-  void vtm(const float* V, const float* M, const float* colmax, size_t m, size_t n, size_t r, double* C,
+  void vtm(const double* V, const float* M, const float* colmax, size_t m, size_t n, size_t r, double* C,
            cudaStream_t s, long* launches) override {
     run<true>(M, colmax, V, m, n, r, C, s, launches);
   }
 
  private:
   template <bool TRANS>
-  void run(const float* M, const float* rowmax, const float* F, size_t m, size_t n, size_t r, double* out,
+  void run(const float* M, const float* rowmax, const double* F, size_t m, size_t n, size_t r, double* out,
            cudaStream_t s, long* launches) {
     if (!supports(m, n, r)) throw std::invalid_argument("tcgen05 path: unsupported shape");
     const int rp = (int)cdiv(r, 16) * 16;
     const size_t K = TRANS ? m : n;     // contraction
     const size_t rows = TRANS ? n : m;  // MMA-M extent
-    const size_t nchunks = cdiv(K, ix::kChunk);
+    // chunks are processed in quads (the factor stage) of pairs (the MMA
+    // loop): a ragged tail is padded with zero chunks (TMA zero-fills M
+    // beyond K, the factor digits are zero there)
+    const size_t nchunks = cdiv(cdiv(K, ix::kChunk), ix::kQuad) * ix::kQuad;
+    const size_t nquads = nchunks / ix::kQuad;
     // factor: row maxima, then digit slices [nchunks][rp][128 B]
     ensure(&fmax_, &fmax_bytes_, 64 * 4);
-    ensure(&digits_, &digits_bytes_, nchunks * rp * 128);
+    ensure(&digits_, &digits_bytes_, nchunks * rp * 128);  // = nquads x 4 rp rows x 128 B
     IX_CK(cudaMemsetAsync(fmax_, 0, 64 * 4, s));
     {
       const unsigned g = TRANS ? (unsigned)std::min<size_t>(cdiv(K, 4), (size_t)sms_ * 4)
                                : (unsigned)(r * std::max<size_t>(1, std::min<size_t>(cdiv(K, 4096), 32)));
       ix::k_fmax<<<g, 256, 0, s>>>(F, (int)r, K, TRANS ? 1 : 0, static_cast<unsigned*>(fmax_));
-      const size_t tot = nchunks * rp * 8;
+      const size_t tot = nquads * rp * 32;
       ix::k_fdigits<<<(unsigned)std::min<size_t>(cdiv(tot, 256), 16384), 256, 0, s>>>(
-          F, (int)r, rp, K, nchunks, TRANS ? 1 : 0, static_cast<const float*>(fmax_), static_cast<uint32_t*>(digits_));
+          F, (int)r, rp, K, nquads, TRANS ? 1 : 0, static_cast<const float*>(fmax_), static_cast<uint32_t*>(digits_));
       IX_CK(cudaGetLastError());
       *launches += 2;
     }
@@ -854,7 +928,7 @@ class IxGemm final : public TcGemm {
       const int smax = std::max(smin, std::min<int>((int)nchunks / 8, 64));
       for (int sp = smin; sp <= smax; ++sp) {
         int cps = (int)cdiv(nchunks, sp);
-        if (p.wide) cps += cps & 1;  // whole chunk pairs per unit
+        cps = (int)cdiv(cps, ix::kQuad) * ix::kQuad;  // whole chunk quads per unit
         if (cps > ix::kMaxUnitChunks) continue;
         const int spr = (int)cdiv(nchunks, cps);
         const double units = (double)p.tiles * spr;
@@ -866,7 +940,7 @@ class IxGemm final : public TcGemm {
       }
     }
     p.chunks_per_split = (int)cdiv(nchunks, splits);
-    if (p.wide) p.chunks_per_split += p.chunks_per_split & 1;
+    p.chunks_per_split = (int)cdiv(p.chunks_per_split, ix::kQuad) * ix::kQuad;
     p.splits = (int)cdiv(nchunks, p.chunks_per_split);
     const size_t out_count = rows * r;
     double* dst = out;
@@ -878,7 +952,7 @@ class IxGemm final : public TcGemm {
     const CUtensorMap mm = TRANS    ? map_f32(M, n, m, 128, ix::kChunk, false)
                            : p.wide ? map_rows3(M, n, m)
                                     : map_f32(M, n, m, ix::kChunk, 128, true);
-    const CUtensorMap mb = map_digits(digits_, nchunks * rp, (uint32_t)rp);
+    const CUtensorMap mb = map_digits(digits_, nchunks * rp, 4u * (uint32_t)rp);
     const size_t smem = 1024 + ix::kMStages * ix::kMTileBytes + ix::kBStages * ix::kBStageBytes + 256;
     auto kern = TRANS ? ix::k_ix_product<true> : ix::k_ix_product<false>;
     if (!attr_set_[TRANS ? 1 : 0]) {

@@ -29,11 +29,13 @@ class TcGemm {
   // in C = V^T M.
   virtual void level_stats(const float* M, size_t m, size_t n, float* rowmax, float* colmax, cudaStream_t s,
                            long* launches) = 0;
-  virtual void mwt(const float* M, const float* rowmax, const float* W, size_t m, size_t n, size_t r, double* A,
+  // M fp32 (the streamed operand), factors fp64 (the engine's factor
+  // storage; rounded once to the factor's fixed-point grid)
+  virtual void mwt(const float* M, const float* rowmax, const double* W, size_t m, size_t n, size_t r, double* A,
                    cudaStream_t s, long* launches) = 0;
-  virtual void vtm(const float* V, const float* M, const float* colmax, size_t m, size_t n, size_t r, double* C,
+  virtual void vtm(const double* V, const float* M, const float* colmax, size_t m, size_t n, size_t r, double* C,
                    cudaStream_t s, long* launches) = 0;
-  // fp64 storage never takes the tensor path (kept for the templated engine)
+  // fp64 storage of M never takes the tensor path (kept for the templated engine)
   void mwt(const double*, const float*, const double*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
   void vtm(const double*, const double*, const float*, size_t, size_t, size_t, double*, cudaStream_t, long*) {}
 };

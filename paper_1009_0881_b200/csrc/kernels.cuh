@@ -64,8 +64,8 @@ constexpr int GKS = 16;  // K step of the two-stage kernels (2 x 2 x 16 x 65 dou
 //   X: rows x K (row-major, ld = K), Y: ny x K (row-major, ld = K).
 //   (A = M W^T with X = M, Y = W; B = W W^T with X = Y = W.)
 // TC: the output tile's width along Y (32 / 48 / 64; ny = r is narrow)
-template <typename T, bool EXACT, int TC = GT>
-__global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const T* __restrict__ Y,
+template <typename TX, typename TY, bool EXACT, int TC = GT>
+__global__ void __launch_bounds__(256) k_gemm_abt(const TX* __restrict__ X, const TY* __restrict__ Y,
                                                   size_t rows, size_t ny, size_t K, size_t kchunk,
                                                   double* __restrict__ part) {
   // two stages: the next K step's operands are loaded into registers while
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const T* __restrict__ X, const
 //   V: K x r (row-major), X: K x ncols (row-major).
 //   (C = V^T M with X = M; D = V^T V with X = V, ncols = r.)
 // TR: the output tile's height along r (32 / 48 / 64)
-template <typename T, bool EXACT, int TR = GT>
-__global__ void __launch_bounds__(256) k_gemm_atb(const T* __restrict__ V, const T* __restrict__ X,
+template <typename TV, typename TX, bool EXACT, int TR = GT>
+__global__ void __launch_bounds__(256) k_gemm_atb(const TV* __restrict__ V, const TX* __restrict__ X,
                                                   size_t K, size_t r, size_t ncols, size_t kchunk,
                                                   double* __restrict__ part) {
   constexpr int NA = TR / 16;            // outputs per thread along r
@@ -507,8 +507,8 @@ __global__ void __launch_bounds__(256) k_mu_warp(const double* __restrict__ A, c
 // 128 columns per block; V rows staged 32 at a time; W column tile in smem.
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT>
-__global__ void __launch_bounds__(128) k_col_sqerr(const T* __restrict__ M, const T* __restrict__ V,
-                                                   const T* __restrict__ W, size_t m, size_t n, int r,
+__global__ void __launch_bounds__(128) k_col_sqerr(const T* __restrict__ M, const double* __restrict__ V,
+                                                   const double* __restrict__ W, size_t m, size_t n, int r,
                                                    size_t rchunk, double* __restrict__ part) {
   extern __shared__ double sm[];
   const int t = threadIdx.x;
@@ -553,23 +553,36 @@ __device__ __forceinline__ void ld4_shared(const double* p, double* o) {
   o[0] = u.x, o[1] = u.y, o[2] = v.x, o[3] = v.y;
 }
 
+// Persistent: block b takes tiles b, b + grid, ... (tile = (column block,
+// row block), column blocks fastest) and writes one fp64 partial.  `gate`
+// (optional, device): a block returns at once, writing 0, unless *gate != 0
+// (the tensor path's sample runs this only when the Gram identity cancels
+// too much, engine.cu sample_t).
 template <typename T>
-__global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M, const T* __restrict__ V,
-                                                     const T* __restrict__ W, size_t m, size_t n, int r,
-                                                     double* __restrict__ part) {
+__global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M, const double* __restrict__ V,
+                                                     const double* __restrict__ W, size_t m, size_t n, int r,
+                                                     double* __restrict__ part, const double* __restrict__ gate) {
   extern __shared__ __align__(16) unsigned char smraw[];
   T* Vs = reinterpret_cast<T*>(smraw);  // [r][128]
   T* Ws = Vs + (size_t)r * 128;         // [r][128]
   __shared__ double red[8];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const size_t i0 = (size_t)blockIdx.y * 128, j0 = (size_t)blockIdx.x * 128;
+  if (gate && *gate == 0.0) {
+    if (t == 0) part[blockIdx.x] = 0.0;
+    return;
+  }
+  const size_t cbk = (n + 127) / 128, ntiles = cbk * ((m + 127) / 128);
+  double s = 0.0;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const size_t i0 = (tile / cbk) * 128, j0 = (tile % cbk) * 128;
+  __syncthreads();  // the previous tile's shared-memory reads are done
   for (int e = t; e < r * 128; e += 256) {
     const int k = e >> 7, c = e & 127;
-    Ws[e] = (j0 + c < n) ? W[(size_t)k * n + j0 + c] : T(0);
+    Ws[e] = (j0 + c < n) ? (T)W[(size_t)k * n + j0 + c] : T(0);
   }
   for (int e = t; e < r * 128; e += 256) {
     const int row = e / r, k = e % r;  // coalesced along V's rows
-    Vs[(size_t)k * 128 + row] = (i0 + row < m) ? V[(i0 + row) * r + k] : T(0);
+    Vs[(size_t)k * 128 + row] = (i0 + row < m) ? (T)V[(i0 + row) * r + k] : T(0);
   }
   __syncthreads();
   T acc[8][8];
@@ -593,7 +606,6 @@ __global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M,
   }
   // squared residuals: each row's 8 terms summed in T, then in fp64 (the
   // per-element fp64 convert + FMA would make the kernel fp64-pipe bound)
-  double s = 0.0;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const size_t i = i0 + (a >> 2) * 64 + ty * 4 + (a & 3);
@@ -609,6 +621,7 @@ __global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M,
     }
     s += (double)sr;
   }
+  }  // tiles
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((t & 31) == 0) red[t >> 5] = s;
@@ -616,7 +629,7 @@ __global__ void __launch_bounds__(256, 2) k_sqerr_tiled(const T* __restrict__ M,
   if (t == 0) {
     double tot = 0.0;
     for (int w = 0; w < 8; ++w) tot += red[w];
-    part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    part[blockIdx.x] = tot;
   }
 }
 
@@ -740,6 +753,18 @@ __global__ void k_gram_combine(double* s) {
   const double e2 = s[0] - 2.0 * s[1] + s[2];
   s[0] = e2 > 0.0 ? e2 : 0.0;
 }
+
+// Tensor-path samples: the Gram identity cancels ||M||^2 / e^2-fold, so the
+// products' input rounding (~1e-9 .. 1e-10 of ||M||^2 on <C, W>) is
+// amplified near a tight fit.  s[6] = the Gram e^2; s[7] = 1 when
+// e^2 < tau ||M||^2 (the direct residual is then computed and used).
+__global__ void k_gram_check(double* s, double tau) {
+  const double e2 = s[0] - 2.0 * s[1] + s[2];
+  s[6] = e2 > 0.0 ? e2 : 0.0;
+  s[7] = e2 < tau * s[0] ? 1.0 : 0.0;
+}
+// s[0] = s[7] ? s[8] (direct) : s[6] (Gram)
+__global__ void k_gram_select(double* s) { s[0] = s[7] != 0.0 ? s[8] : s[6]; }
 
 __global__ void k_timestamp(unsigned long long* out) { *out = globaltimer(); }
 

@@ -1,15 +1,18 @@
 """Test infrastructure: a numpy model of the tensor path's number format
 (paper_1009_0881_b200/csrc/ix_gemm.cu), used only as a checker.
 
-Every fp32 operand row (a row of M for A = M W^T, a column of M for
-C = V^T M, a row of W / a column of V on the factor side) is scaled by the
-power of two s = scale_of(row max), rounded once to the nearest integer X
-(round-half-even, as the kernel's single FFMA), and split into balanced
-base-256 digits X = d1 2^16 + d2 2^8 + d3.  The kernel accumulates
-    G0 = sum d1 e1,  G1 = sum d1 e2 + d2 e1,  G2 = sum d1 e3 + d2 e2 + d3 e1
-exactly in int32 and returns 2^16 (G0 2^16 + G1 2^8 + G2) / (s_x s_f).  The
-integer sums here are fp64 matrix products of small integers (|sum| < 2^31),
-so they are exact too: the model and the kernel agree up to the fp64
+Every fp32 row of M (a row for A = M W^T, a column for C = V^T M) is
+scaled by the power of two s = scale_of(row max) and rounded once to the
+nearest integer X (round-half-even, as the kernel's single FFMA), split into
+balanced base-256 digits X = d1 2^16 + d2 2^8 + d3 (23-bit fixed point).
+Every fp64 factor row (a row of W, a column of V) is scaled by
+s_f = fscale_of(row max) (max in [2^29, 2^30)) and rounded to Y = e1 2^24 +
+e2 2^16 + e3 2^8 + e4 (31-bit fixed point).  The kernel forms all twelve
+digit products d_i e_j, sums them by weight class exactly in int32, and
+returns sum X Y / (s s_f): the exact dot product of the rounded integers.
+Here the integer sums are fp64 matrix products of small integers
+(|sum| < 2^31, exact), combined as hi 2^24 + lo with hi, lo exact int64 and
+one fp64 rounding, as the kernel does.  Model and kernel agree up to the fp64
 rounding of the kernel's split-K sum (~1e-16 relative).
 """
 import numpy as np
@@ -26,6 +29,15 @@ def scale_of(mx):
     return np.where(mx > 0, s, 1.0)
 
 
+def fscale_of(mx):
+    """factor scale: the fp64 row maximum rounded UP to fp32, then 2^(30 - e)"""
+    mx = np.asarray(mx, np.float64)
+    mx32 = mx.astype(np.float32).astype(np.float64)
+    mx32 = np.where(mx32 < mx, np.nextafter(mx.astype(np.float32), np.float32(np.inf)).astype(np.float64), mx32)
+    _, e = np.frexp(mx32)
+    return np.where(mx > 0, np.ldexp(1.0, 30 - e), 1.0)
+
+
 def digits(x, s):
     X = np.rint(np.asarray(x, np.float32).astype(np.float64) * s)
     d3 = np.mod(X + 128, 256) - 128
@@ -35,37 +47,52 @@ def digits(x, s):
     return d1, d2, d3
 
 
+def fdigits(f, s):
+    """four balanced digits of an fp64 factor row on its 31-bit grid"""
+    X = np.rint(np.asarray(f, np.float64) * s)
+    out = []
+    for _ in range(3):
+        d = np.mod(X + 128, 256) - 128
+        out.append(d)
+        X = (X - d) / 256
+    out.append(X)
+    return out[::-1]  # e1, e2, e3, e4
+
+
 def _combine(a, b, sa, sb):
-    """sum over the contraction of a (rows x K digits) and b (K x cols digits)."""
-    a1, a2, a3 = a
-    b1, b2, b3 = b
-    G0 = a1 @ b1
-    G1 = a1 @ b2 + a2 @ b1
-    G2 = a1 @ b3 + a2 @ b2 + a3 @ b1
-    S = G0 * 65536.0 + G1 * 256.0 + G2
-    return S * 65536.0 / (sa[:, None] * sb[None, :])
+    """sum over the contraction of a (rows x K: three M digits) and b (K x
+    cols: four factor digits)."""
+    G = [np.zeros((a[0].shape[0], b[0].shape[1])) for _ in range(6)]
+    for i in range(3):
+        for j in range(4):
+            G[i + j] += a[i] @ b[j]
+    G = [np.rint(g).astype(np.int64) for g in G]
+    hi = (G[0] * 256 + G[1]) * 256 + G[2]
+    lo = (G[3] * 256 + G[4]) * 256 + G[5]
+    S = hi.astype(np.float64) * 16777216.0 + lo.astype(np.float64)
+    return S / (sa[:, None] * sb[None, :])
 
 
 def product_A(M, W):
-    """A = M W^T (m x r) as the tensor path computes it."""
+    """A = M W^T (m x r) as the tensor path computes it (W fp64)."""
     M = np.asarray(M, np.float32)
-    W = np.asarray(W, np.float32)
+    W = np.asarray(W, np.float64)
     sm = scale_of(M.max(axis=1))
-    sw = scale_of(W.max(axis=1))
+    sw = fscale_of(W.max(axis=1))
     dm = digits(M, sm[:, None])
-    dw = [d.T for d in digits(W, sw[:, None])]
+    dw = [d.T for d in fdigits(W, sw[:, None])]
     return _combine(dm, dw, sm, sw)
 
 
 def product_C(V, M):
-    """C = V^T M (r x n) as the tensor path computes it."""
-    V = np.asarray(V, np.float32)
+    """C = V^T M (r x n) as the tensor path computes it (V fp64)."""
+    V = np.asarray(V, np.float64)
     M = np.asarray(M, np.float32)
-    sv = scale_of(V.max(axis=0))
+    sv = fscale_of(V.max(axis=0))
     sm = scale_of(M.max(axis=0))
-    dv = [d.T for d in digits(V, sv[None, :])]
-    dm = digits(M, sm[None, :])
-    return _combine(dv, dm, sv, sm)
+    dv = fdigits(V, sv[None, :])                # m x r each
+    dm = [d.T for d in digits(M, sm[None, :])]  # n x m each
+    return _combine(dm, dv, sm, sv).T           # (M^T V)^T
 
 
 def gram_error(M, V, W):

@@ -39,7 +39,8 @@ def inputs(P, golden):
         g.export_data(M32.ctypes.data)
     assert hashlib.sha256(M32.tobytes()).digest() == golden["m_digest"].tobytes(), "device generator drifted"
     V0, W0 = P.random_init(m, n, int(golden["rank"]), 0)
-    return M32, V0, W0
+    # the fixture's reference run starts from the fp32-rounded init
+    return M32, V0.astype(np.float32).astype(np.float64), W0.astype(np.float32).astype(np.float64)
 
 
 @pytest.mark.parametrize("cycle", ["none", "fmg"])
