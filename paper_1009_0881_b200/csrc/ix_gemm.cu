@@ -84,7 +84,7 @@ constexpr int kSlots = 4;              // TMEM staging slots: two pairs (chunk 2
 constexpr int kPairs = kSlots / 2;
 constexpr int kSlotCols = 32;          // columns per slot (24 used)
 constexpr int kGroupCols = 64;         // columns per accumulator group (r_pad <= 64)
-constexpr int kClasses = 6;            // digit-product weight classes 2^40, 2^32, ..., 2^0
+constexpr int kClasses = 4;            // digit-product weight classes 2^40, 2^32, 2^24, 2^16
 constexpr int kAccCols = kClasses * kGroupCols;
 constexpr int kStg0 = 384;             // staging slots after the (single) accumulator set
 static_assert(kAccCols <= kStg0 && kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
@@ -252,39 +252,43 @@ __host__ __device__ __forceinline__ double fscale_of(float mx) {
 }
 
 // One chunk's 3 MMAs (K = 32 each) on staging slot S: M digit plane d_i
-// (TMEM, 128 rows) times the STACKED factor digit planes [e1; e2; e3; e4]
-// (shared memory, N = 4 r_pad rows), written to the accumulator window
-// starting at class group i - 1 (columns (i - 1) r_pad .. (i + 3) r_pad).
-// Block j of MMA i lands on group i + j - 2, so the windows' overlap sums
-// every digit product d_i e_j into its weight class c = i + j - 2 (weight
-// 2^(40 - 8c)):
+// (TMEM, 128 rows) times a prefix of the STACKED factor digit planes
+// [e1; e2; e3; e4] (shared memory, r_pad rows each), written to the
+// accumulator window starting at class group i - 1.  Block j of MMA i lands
+// on group i + j - 2, so the windows' overlap sums every digit product
+// d_i e_j into its weight class c = i + j - 2 (weight 2^(40 - 8c)):
 //   G0 = d1 e1;  G1 = d1 e2 + d2 e1;  G2 = d1 e3 + d2 e2 + d3 e1;
-//   G3 = d1 e4 + d2 e3 + d3 e2;  G4 = d2 e4 + d3 e3;  G5 = d3 e4
-// -- all twelve products, exact in int32, in three instructions.  The
-// accumulators always accumulate (the epilogue zeroes them after each
-// drain).  (With only the leading six products of a 3 x 3 split, a small
-// factor entry -- leading digit d2 or d3, common in sparse NMF factors --
-// kept ~16 bits and the config-4 FMG trajectory drifted 1e-4 from the
-// reference; the factor's fourth digit takes its grid from 2^-23 to 2^-31
-// of the row maximum, which the Gram-identity samples at coarse levels
-// needed.  r02 measurements.)
+//   G3 = d1 e4 + d2 e3 + d3 e2
+// (d1: N = 4 r_pad, d2: 3 r_pad, d3: 2 r_pad), exact in int32.  Not formed:
+// d2 e4, d3 e3, d3 e4 (classes 4 and 5, <= 2^-32 of the largest product):
+// measured on sparse coarse-level factors they change no product beyond
+// 1e-12 relative, and they would cost a third more tensor work -- which
+// the board's power limit turns into SM clock (ncu r02c: 12 products ran
+// the tensor pipe at 70-80 % and the clock at 1.24-1.34 GHz).  The leading
+// six of a 3 x 3 split were NOT enough: a small factor entry (leading digit
+// d2 or d3, common in sparse NMF factors) kept ~16 bits and the config-4 FMG
+// trajectory drifted 1e-4 from the reference; the factor's fourth digit
+// (grid 2^-31 of the row maximum) fixed the Gram-identity samples at coarse
+// levels.  The accumulators always accumulate (the epilogue zeroes them
+// after each drain).
 template <int S>
-__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id, uint32_t rp) {
+__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id4, uint32_t id3, uint32_t id2, uint32_t rp) {
   constexpr uint32_t a1 = kStg0 + S * kSlotCols, a2 = a1 + 8, a3 = a1 + 16;
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %6, %7, 1;\n\t"   // d1 [e1..e4] -> G0..G3
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%4], %6, %7, 1;\n\t"   // d2 [e1..e4] -> G1..G4
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%5], %6, %7, 1;\n\t}"  // d3 [e1..e4] -> G2..G5
-      ::"r"(0u), "r"(rp), "r"(2u * rp), "r"(a1), "r"(a2), "r"(a3), "l"(bd), "r"(id)
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%4], %6, %8, 1;\n\t"   // d2 [e1..e3] -> G1..G3
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%5], %6, %9, 1;\n\t}"  // d3 [e1, e2] -> G2..G3
+      ::"r"(0u), "r"(rp), "r"(2u * rp), "r"(a1), "r"(a2), "r"(a3), "l"(bd), "r"(id4), "r"(id3), "r"(id2)
       : "memory");
 }
 // A chunk pair: slots 2 PS and 2 PS + 1 (factor columns at bd0 / bd1)
 template <int PS>
-__device__ __forceinline__ void issue_pair(uint64_t bd0, uint64_t bd1, uint32_t id, uint32_t rp) {
-  issue_chunk<2 * PS>(bd0, id, rp);
-  issue_chunk<2 * PS + 1>(bd1, id, rp);
+__device__ __forceinline__ void issue_pair(uint64_t bd0, uint64_t bd1, uint32_t id4, uint32_t id3, uint32_t id2,
+                                           uint32_t rp) {
+  issue_chunk<2 * PS>(bd0, id4, id3, id2, rp);
+  issue_chunk<2 * PS + 1>(bd1, id4, id3, id2, rp);
 }
 
 // Digit planes of 4 consecutive elements from their FFMA bit patterns
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stage -- a chunk quad -- is waited for by a quad's first pair and
     // released by its second)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
-    const uint32_t id = idesc_s8(4 * p.rp);
+    const uint32_t id4 = idesc_s8(4 * p.rp), id3 = idesc_s8(3 * p.rp), id2 = idesc_s8(2 * p.rp);
     const uint32_t rp = (uint32_t)p.rp;
     int h = 0, uc = 0;
     for (int u = u0; u < total_units; u += ustep, ++uc) {
@@ -463,8 +467,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         // chunk (2h) % 4 of the quad: its K columns at byte 32 (2h % 4)
         const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4) + (uint64_t)(4 * (h & 1));
-        if (ps == 0) issue_pair<0>(bd, bd + 2, id, rp);
-        else issue_pair<1>(bd, bd + 2, id, rp);
+        if (ps == 0) issue_pair<0>(bd, bd + 2, id4, id3, id2, rp);
+        else issue_pair<1>(bd, bd + 2, id4, id3, id2, rp);
         tc_commit(smem_u32(&sdone[ps]));                // slot pair reusable once these MMAs finish
         if (h & 1) tc_commit(smem_u32(&bempty[bs]));  // ... and, after a quad's second pair, its factor stage
         __syncwarp();
@@ -604,12 +608,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < 8; ++kk) {
             const int k = h * 8 + kk;
             const double ck = __shfl_sync(0xffffffffu, cinv, k);  // all lanes: outside the row guard
-            // sum X Y = hi 2^24 + lo, hi = G0 2^16 + G1 2^8 + G2 and
-            // lo = G3 2^16 + G4 2^8 + G5 exact in int64 (|G| < 2^31), hi exact
-            // in fp64 (< 2^46 for a unit's K <= 40960): one fp64 rounding
-            const long long hi = ((long long)(int)g[0][kk] * 256ll + (int)g[1][kk]) * 256ll + (int)g[2][kk];
-            const long long lo = ((long long)(int)g[3][kk] * 256ll + (int)g[4][kk]) * 256ll + (int)g[5][kk];
-            const double v = fma((double)hi, 16777216.0, (double)lo) * rinv * ck;
+            // sum X Y = 2^16 (G0 2^24 + G1 2^16 + G2 2^8 + G3), the bracket
+            // exact in int64 (|G0| < 2^14 K <= 2^29.3 for a unit's K <= 40960),
+            // then one fp64 rounding
+            const long long S =
+                (((long long)(int)g[0][kk] * 256ll + (int)g[1][kk]) * 256ll + (int)g[2][kk]) * 256ll + (int)g[3][kk];
+            const double v = (double)S * 65536.0 * rinv * ck;
             if (gi < p.rows && cb + k < p.r) {
               if (!TRANS)
                 p.part[(size_t)x.split * p.rows * p.r + (size_t)gi * p.r + cb + k] = v;

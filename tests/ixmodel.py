@@ -7,12 +7,13 @@ nearest integer X (round-half-even, as the kernel's single FFMA), split into
 balanced base-256 digits X = d1 2^16 + d2 2^8 + d3 (23-bit fixed point).
 Every fp64 factor row (a row of W, a column of V) is scaled by
 s_f = fscale_of(row max) (max in [2^29, 2^30)) and rounded to Y = e1 2^24 +
-e2 2^16 + e3 2^8 + e4 (31-bit fixed point).  The kernel forms all twelve
-digit products d_i e_j, sums them by weight class exactly in int32, and
-returns sum X Y / (s s_f): the exact dot product of the rounded integers.
-Here the integer sums are fp64 matrix products of small integers
-(|sum| < 2^31, exact), combined as hi 2^24 + lo with hi, lo exact int64 and
-one fp64 rounding, as the kernel does.  Model and kernel agree up to the fp64
+e2 2^16 + e3 2^8 + e4 (31-bit fixed point).  The kernel forms the digit
+products d_i e_j of weight classes c = i + j - 2 <= 3 (all but d2 e4, d3 e3,
+d3 e4: <= 2^-32 of the largest product), sums them by class exactly in
+int32, and returns 2^16 (G0 2^24 + G1 2^16 + G2 2^8 + G3) / (s s_f).  Here the
+integer sums are fp64 matrix products of small integers (|sum| < 2^31,
+exact), combined in exact int64 and rounded once to fp64, as the kernel
+does.  Model and kernel agree up to the fp64
 rounding of the kernel's split-K sum (~1e-16 relative).
 """
 import numpy as np
@@ -62,15 +63,14 @@ def fdigits(f, s):
 def _combine(a, b, sa, sb):
     """sum over the contraction of a (rows x K: three M digits) and b (K x
     cols: four factor digits)."""
-    G = [np.zeros((a[0].shape[0], b[0].shape[1])) for _ in range(6)]
+    G = [np.zeros((a[0].shape[0], b[0].shape[1])) for _ in range(4)]
     for i in range(3):
         for j in range(4):
-            G[i + j] += a[i] @ b[j]
+            if i + j <= 3:  # classes 4, 5 (d2 e4, d3 e3, d3 e4) are not formed
+                G[i + j] += a[i] @ b[j]
     G = [np.rint(g).astype(np.int64) for g in G]
-    hi = (G[0] * 256 + G[1]) * 256 + G[2]
-    lo = (G[3] * 256 + G[4]) * 256 + G[5]
-    S = hi.astype(np.float64) * 16777216.0 + lo.astype(np.float64)
-    return S / (sa[:, None] * sb[None, :])
+    S = ((G[0] * 256 + G[1]) * 256 + G[2]) * 256 + G[3]
+    return S.astype(np.float64) * 65536.0 / (sa[:, None] * sb[None, :])
 
 
 def product_A(M, W):
