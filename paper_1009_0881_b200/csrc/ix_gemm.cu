@@ -90,9 +90,10 @@ constexpr int kStg0 = 384;             // staging slots after the (single) accum
 static_assert(kAccCols <= kStg0 && kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
 // factor fixed point: 31 bits (four digits e1 e2 e3 e4, e1 in [0, 127])
 constexpr double kFBias = 8421504.0;   // 0x808080: balanced low three digits
-// chunks per work unit: |G2| <= 3 * 128^2 per K element, so an int32
-// accumulator is exact for K < 2^31 / 49152 = 43690; 1280 chunks = 40960
-constexpr int kMaxUnitChunks = 1280;
+// chunks per work unit: class G3 sums four digit products (|d e| <= 2^14) per
+// K element, so an int32 accumulator is exact for K <= 2^31 / 2^16 = 32768
+// = 1024 chunks
+constexpr int kMaxUnitChunks = 1024;
 constexpr int kConvGroups = 2;
 constexpr int kWarpM = 0, kWarpMma = 1, kWarpB = 2, kWarpConv0 = 3;
 constexpr int kWarpEpi0 = kWarpConv0 + 4 * kConvGroups;
@@ -272,23 +273,26 @@ __host__ __device__ __forceinline__ double fscale_of(float mx) {
 // levels.  The accumulators always accumulate (the epilogue zeroes them
 // after each drain).
 template <int S>
-__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id4, uint32_t id3, uint32_t id2, uint32_t rp) {
-  constexpr uint32_t a1 = kStg0 + S * kSlotCols, a2 = a1 + 8, a3 = a1 + 16;
+__device__ __forceinline__ void issue_chunk(uint64_t bd, uint32_t id4, uint32_t id3, uint32_t id2, uint32_t id1,
+                                            uint32_t rp) {
+  constexpr uint32_t a1 = kStg0 + S * kSlotCols, a2 = a1 + 8, a3 = a1 + 16, a4 = a1 + 24;
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %6, %7, 1;\n\t"   // d1 [e1..e4] -> G0..G3
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%4], %6, %8, 1;\n\t"   // d2 [e1..e3] -> G1..G3
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%5], %6, %9, 1;\n\t}"  // d3 [e1, e2] -> G2..G3
-      ::"r"(0u), "r"(rp), "r"(2u * rp), "r"(a1), "r"(a2), "r"(a3), "l"(bd), "r"(id4), "r"(id3), "r"(id2)
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%4], %8, %9, 1;\n\t"    // d1 [e1..e4] -> G0..G3
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%5], %8, %10, 1;\n\t"   // d2 [e1..e3] -> G1..G3
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%6], %8, %11, 1;\n\t"   // d3 [e1, e2] -> G2..G3
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], [%7], %8, %12, 1;\n\t}"  // d4 [e1]     -> G3
+      ::"r"(0u), "r"(rp), "r"(2u * rp), "r"(3u * rp), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "l"(bd), "r"(id4),
+      "r"(id3), "r"(id2), "r"(id1)
       : "memory");
 }
 // A chunk pair: slots 2 PS and 2 PS + 1 (factor columns at bd0 / bd1)
 template <int PS>
 __device__ __forceinline__ void issue_pair(uint64_t bd0, uint64_t bd1, uint32_t id4, uint32_t id3, uint32_t id2,
-                                           uint32_t rp) {
-  issue_chunk<2 * PS>(bd0, id4, id3, id2, rp);
-  issue_chunk<2 * PS + 1>(bd1, id4, id3, id2, rp);
+                                           uint32_t id1, uint32_t rp) {
+  issue_chunk<2 * PS>(bd0, id4, id3, id2, id1, rp);
+  issue_chunk<2 * PS + 1>(bd1, id4, id3, id2, id1, rp);
 }
 
 // Digit planes of 4 consecutive elements from their FFMA bit patterns
@@ -303,6 +307,29 @@ __device__ __forceinline__ void planes4(uint32_t w0, uint32_t w1, uint32_t w2, u
   p1 = __byte_perm(u01, u23, 0x5410);
 }
 __device__ __forceinline__ uint32_t fx_bits(float x, float s) { return __float_as_uint(__fmaf_rn(x, s, kMagic)); }
+
+// M entries on a 31-bit grid: X = round(x s) with s = 256 s_hi (x * s exact:
+// fp32 entries within 2^7 of the row maximum are represented exactly), as
+// four balanced digits X = d1 2^24 + d2 2^16 + d3 2^8 + d4.  The leading three
+// are those of X_hi = round(x s_hi) (the FFMA-magic bits, fx_bits); the
+// remainder r = x s - 256 X_hi (|r| <= 128, computed exactly by one FFMA)
+// gives d4 = round(min(r, 127)) -- the clamp (r = 128 only when x s / 256
+// is a tie rounded down) costs at most one unit of the 2^-31 grid.  The float
+// bits of d4 + 1.5 * 2^23 carry d4 as a two's-complement low byte.
+__device__ __forceinline__ void planes4x(float x0, float x1, float x2, float x3, float sh, uint32_t& p1,
+                                         uint32_t& p2, uint32_t& p3, uint32_t& p4) {
+  const float xs[4] = {x0, x1, x2, x3};
+  uint32_t w[4], lo[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float th = __fmaf_rn(xs[t], sh, kMagic);
+    w[t] = __float_as_uint(th);
+    const float r = __fmaf_rn(-(th - kMagic), 256.f, xs[t] * (256.f * sh));
+    lo[t] = __float_as_uint(fminf(r, 127.f) + 12582912.f);
+  }
+  planes4(w[0], w[1], w[2], w[3], p1, p2, p3);
+  p4 = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+}
 
 struct Params {
   int rows;        // MMA-M extent: m (product 1) or n (product 2)
@@ -452,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stage -- a chunk quad -- is waited for by a quad's first pair and
     // released by its second)
     const uint64_t bdesc0 = sdesc_sw128(smem_u32(sm_b));
-    const uint32_t id4 = idesc_s8(4 * p.rp), id3 = idesc_s8(3 * p.rp), id2 = idesc_s8(2 * p.rp);
+    const uint32_t id4 = idesc_s8(4 * p.rp), id3 = idesc_s8(3 * p.rp), id2 = idesc_s8(2 * p.rp),
+                   id1 = idesc_s8(p.rp);
     const uint32_t rp = (uint32_t)p.rp;
     int h = 0, uc = 0;
     for (int u = u0; u < total_units; u += ustep, ++uc) {
@@ -467,8 +495,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         // chunk (2h) % 4 of the quad: its K columns at byte 32 (2h % 4)
         const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4) + (uint64_t)(4 * (h & 1));
-        if (ps == 0) issue_pair<0>(bd, bd + 2, id4, id3, id2, rp);
-        else issue_pair<1>(bd, bd + 2, id4, id3, id2, rp);
+        if (ps == 0) issue_pair<0>(bd, bd + 2, id4, id3, id2, id1, rp);
+        else issue_pair<1>(bd, bd + 2, id4, id3, id2, id1, rp);
         tc_commit(smem_u32(&sdone[ps]));                // slot pair reusable once these MMAs finish
         if (h & 1) tc_commit(smem_u32(&bempty[bs]));  // ... and, after a quad's second pair, its factor stage
         __syncwarp();
@@ -504,9 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots, sp = (g >> 1) & 1;
         const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g >> 2) & 1u;
         mbar_wait(smem_u32(&mfull[ps]), mph);
-        // digit planes d1 (words 0..7) | d2 (8..15) | d3 (16..23); word j holds
-        // elements 4j .. 4j + 3, element t of the word in byte t
-        uint32_t pl[24];
+        // digit planes d1 (words 0..7) | d2 (8..15) | d3 (16..23) | d4 (24..31);
+        // word j holds elements 4j .. 4j + 3, element t of the word in byte t
+        uint32_t pl[32];
         const uint32_t tile = smem_u32(sm_m) + (uint32_t)((ps * kMGroup + g % kMGroup) * kMTileBytes);
         if (!TRANS && p.wide) {
           // pair buffer [row][half][32] (SWIZZLE_128B per 128-byte line):
@@ -521,10 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 8; ++j) {
             float a0, a1, a2, a3;
             lds128(pairb + line * 128 + ((((uint32_t)(j ^ flip)) ^ (line & 7)) << 4), a0, a1, a2, a3);
-            planes4(fx_bits(a0, s), fx_bits(a1, s), fx_bits(a2, s), fx_bits(a3, s), pl[j], pl[8 + j], pl[16 + j]);
+            planes4x(a0, a1, a2, a3, s, pl[j], pl[8 + j], pl[16 + j], pl[24 + j]);
           }
 #pragma unroll
-          for (int j = 0; j < 24; j += 2) {
+          for (int j = 0; j < 32; j += 2) {
             const uint32_t e0 = pl[j], e1 = pl[j + 1];
             pl[j] = flip ? e1 : e0;
             pl[j + 1] = flip ? e0 : e1;
@@ -535,15 +563,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 8; ++j) {
             float a0, a1, a2, a3;
             lds128(tile + row * 128 + ((j ^ (row & 7)) << 4), a0, a1, a2, a3);
-            planes4(fx_bits(a0, s), fx_bits(a1, s), fx_bits(a2, s), fx_bits(a3, s), pl[j], pl[8 + j], pl[16 + j]);
+            planes4x(a0, a1, a2, a3, s, pl[j], pl[8 + j], pl[16 + j], pl[24 + j]);
           }
         } else {
           // column `row` of a 32 x 128 (k x j) tile, no swizzle
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint32_t b0 = tile + (uint32_t)((4 * j * 128 + row) * 4);
-            planes4(fx_bits(lds32(b0), s), fx_bits(lds32(b0 + 512), s), fx_bits(lds32(b0 + 1024), s),
-                    fx_bits(lds32(b0 + 1536), s), pl[j], pl[8 + j], pl[16 + j]);
+            planes4x(lds32(b0), lds32(b0 + 512), lds32(b0 + 1024), lds32(b0 + 1536), s, pl[j], pl[8 + j], pl[16 + j],
+                     pl[24 + j]);
           }
         }
         // generic-proxy reads of the slice before the async-proxy (TMA) refill
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kStg0 + slot * kSlotCols;
         tmem_st16(ta, reinterpret_cast<const uint32_t(&)[16]>(pl[0]));
-        tmem_st8(ta + 16, reinterpret_cast<const uint32_t(&)[8]>(pl[16]));
+        tmem_st16(ta + 16, reinterpret_cast<const uint32_t(&)[16]>(pl[16]));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -608,9 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < 8; ++kk) {
             const int k = h * 8 + kk;
             const double ck = __shfl_sync(0xffffffffu, cinv, k);  // all lanes: outside the row guard
-            // sum X Y = 2^16 (G0 2^24 + G1 2^16 + G2 2^8 + G3), the bracket
-            // exact in int64 (|G0| < 2^14 K <= 2^29.3 for a unit's K <= 40960),
-            // then one fp64 rounding
+            // sum X Y = 2^24 (G0 2^24 + G1 2^16 + G2 2^8 + G3), the bracket
+            // exact in int64 (|G0| < 2^14 K <= 2^29 for a unit's K <= 32768),
+            // then one fp64 rounding; X = x * 256 s_hi, so the 2^24 / 256
+            // folds into 2^16
             const long long S =
                 (((long long)(int)g[0][kk] * 256ll + (int)g[1][kk]) * 256ll + (int)g[2][kk]) * 256ll + (int)g[3][kk];
             const double v = (double)S * 65536.0 * rinv * ck;

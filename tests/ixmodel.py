@@ -2,19 +2,18 @@
 (paper_1009_0881_b200/csrc/ix_gemm.cu), used only as a checker.
 
 Every fp32 row of M (a row for A = M W^T, a column for C = V^T M) is
-scaled by the power of two s = scale_of(row max) and rounded once to the
-nearest integer X (round-half-even, as the kernel's single FFMA), split into
-balanced base-256 digits X = d1 2^16 + d2 2^8 + d3 (23-bit fixed point).
-Every fp64 factor row (a row of W, a column of V) is scaled by
-s_f = fscale_of(row max) (max in [2^29, 2^30)) and rounded to Y = e1 2^24 +
-e2 2^16 + e3 2^8 + e4 (31-bit fixed point).  The kernel forms the digit
-products d_i e_j of weight classes c = i + j - 2 <= 3 (all but d2 e4, d3 e3,
-d3 e4: <= 2^-32 of the largest product), sums them by class exactly in
-int32, and returns 2^16 (G0 2^24 + G1 2^16 + G2 2^8 + G3) / (s s_f).  Here the
-integer sums are fp64 matrix products of small integers (|sum| < 2^31,
-exact), combined in exact int64 and rounded once to fp64, as the kernel
-does.  Model and kernel agree up to the fp64
-rounding of the kernel's split-K sum (~1e-16 relative).
+scaled by 256 s, s = scale_of(row max) (the row maximum at [2^30, 2^31)),
+and rounded to X = d1 2^24 + d2 2^16 + d3 2^8 + d4 (31-bit fixed point:
+entries within 2^7 of the maximum are exact; see digits() for the kernel's
+exact rounding).  Every fp64 factor row (a row of W, a column of V) is scaled
+by s_f = fscale_of(row max) and rounded to Y = e1 2^24 + e2 2^16 + e3 2^8 + e4
+(31-bit).  The kernel forms the digit products d_i e_j of weight classes
+c = i + j - 2 <= 3 (the rest are <= 2^-32 of the largest product), sums them
+by class exactly in int32, and returns 2^16 (G0 2^24 + G1 2^16 + G2 2^8 +
+G3) / (s s_f).  Here the integer sums are fp64 matrix products of small
+integers (|sum| < 2^31, exact), combined in exact int64 and rounded once to
+fp64, as the kernel does.  Model and kernel agree up to the fp64 rounding of
+the kernel's split-K sum (~1e-16 relative).
 """
 import numpy as np
 
@@ -40,12 +39,17 @@ def fscale_of(mx):
 
 
 def digits(x, s):
-    X = np.rint(np.asarray(x, np.float32).astype(np.float64) * s)
-    d3 = np.mod(X + 128, 256) - 128
-    Xp = (X - d3) / 256
+    """four balanced digits of fp32 M entries on the 31-bit grid X = x (256 s):
+    d1 d2 d3 from X_hi = round(x s) (half-even, the kernel's FFMA magic), the
+    low digit d4 = round(min(x 256 s - 256 X_hi, 127)) (ix_gemm.cu planes4x)"""
+    xs = np.asarray(x, np.float32).astype(np.float64) * s
+    Xh = np.rint(xs)
+    d4 = np.rint(np.minimum(xs * 256.0 - Xh * 256.0, 127.0))
+    d3 = np.mod(Xh + 128, 256) - 128
+    Xp = (Xh - d3) / 256
     d2 = np.mod(Xp + 128, 256) - 128
     d1 = (Xp - d2) / 256
-    return d1, d2, d3
+    return d1, d2, d3, d4
 
 
 def fdigits(f, s):
@@ -64,9 +68,9 @@ def _combine(a, b, sa, sb):
     """sum over the contraction of a (rows x K: three M digits) and b (K x
     cols: four factor digits)."""
     G = [np.zeros((a[0].shape[0], b[0].shape[1])) for _ in range(4)]
-    for i in range(3):
+    for i in range(4):
         for j in range(4):
-            if i + j <= 3:  # classes 4, 5 (d2 e4, d3 e3, d3 e4) are not formed
+            if i + j <= 3:  # weight classes >= 4 (<= 2^-32 of the largest product) are not formed
                 G[i + j] += a[i] @ b[j]
     G = [np.rint(g).astype(np.int64) for g in G]
     S = ((G[0] * 256 + G[1]) * 256 + G[2]) * 256 + G[3]
