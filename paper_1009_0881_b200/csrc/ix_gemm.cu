@@ -99,9 +99,7 @@ constexpr int kWarpM = 0, kWarpMma = 1, kWarpB = 2, kWarpConv0 = 3;
 constexpr int kWarpEpi0 = kWarpConv0 + 4 * kConvGroups;
 constexpr int kThreads = (kWarpEpi0 + 8) * 32;
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
-// fixed-point target: x * s + kMagic lands in [2^23, 2^24), whose float bits
-// carry round(x * s) + 0x8080 in the low 23 bits
-constexpr float kMagic = 8421504.0f;           // 2^23 + 0x8080
+// the row maximum's grid position: max * s_hi <= kXMax (then x * 256 s_hi < 2^31 - 0x808080)
 constexpr float kXMax = 8355711.0f;            // 2^23 - 0x8080 - 1
 
 #define IX_CK(x)                                                                                  \
@@ -295,40 +293,26 @@ __device__ __forceinline__ void issue_pair(uint64_t bd0, uint64_t bd1, uint32_t 
   issue_chunk<2 * PS + 1>(bd1, id4, id3, id2, id1, rp);
 }
 
-// Digit planes of 4 consecutive elements from their FFMA bit patterns
-// (byte 0 = d3 + 128, byte 1 = d2 + 128, byte 2 = d1): p1 / p2 / p3 hold
-// element t's digit in byte t.
-__device__ __forceinline__ void planes4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t& p1,
-                                        uint32_t& p2, uint32_t& p3) {
-  const uint32_t t01 = __byte_perm(w0, w1, 0x5140), t23 = __byte_perm(w2, w3, 0x5140);
-  p3 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
-  p2 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
-  const uint32_t u01 = __byte_perm(w0, w1, 0x0062), u23 = __byte_perm(w2, w3, 0x0062);
-  p1 = __byte_perm(u01, u23, 0x5410);
+// M entries on a 31-bit grid: X = round(x s) (half-even, one F2I), s =
+// 256 s_hi a power of two (x * s exact: fp32 entries within 2^7 of the row
+// maximum are represented exactly, x s <= 256 kXMax < 2^31 - 0x808080), as
+// four balanced digits X = d1 2^24 + d2 2^16 + d3 2^8 + d4: the bytes of
+// X + 0x808080 are d1 | d2 + 128 | d3 + 128 | d4 + 128 (3..0).  The four
+// planes of 4 consecutive elements (element t in byte t) by byte permutes.
+__device__ __forceinline__ void planes_of(const uint32_t (&w)[4], uint32_t& p1, uint32_t& p2, uint32_t& p3,
+                                          uint32_t& p4) {
+  const uint32_t t01 = __byte_perm(w[0], w[1], 0x5140), t23 = __byte_perm(w[2], w[3], 0x5140);
+  const uint32_t u01 = __byte_perm(w[0], w[1], 0x7362), u23 = __byte_perm(w[2], w[3], 0x7362);
+  p4 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
+  p3 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
+  p2 = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;
+  p1 = __byte_perm(u01, u23, 0x7632);
 }
-__device__ __forceinline__ uint32_t fx_bits(float x, float s) { return __float_as_uint(__fmaf_rn(x, s, kMagic)); }
-
-// M entries on a 31-bit grid: X = round(x s) with s = 256 s_hi (x * s exact:
-// fp32 entries within 2^7 of the row maximum are represented exactly), as
-// four balanced digits X = d1 2^24 + d2 2^16 + d3 2^8 + d4.  The leading three
-// are those of X_hi = round(x s_hi) (the FFMA-magic bits, fx_bits); the
-// remainder r = x s - 256 X_hi (|r| <= 128, computed exactly by one FFMA)
-// gives d4 = round(min(r, 127)) -- the clamp (r = 128 only when x s / 256
-// is a tie rounded down) costs at most one unit of the 2^-31 grid.  The float
-// bits of d4 + 1.5 * 2^23 carry d4 as a two's-complement low byte.
-__device__ __forceinline__ void planes4x(float x0, float x1, float x2, float x3, float sh, uint32_t& p1,
+__device__ __forceinline__ void planes4x(float x0, float x1, float x2, float x3, float s, uint32_t& p1,
                                          uint32_t& p2, uint32_t& p3, uint32_t& p4) {
-  const float xs[4] = {x0, x1, x2, x3};
-  uint32_t w[4], lo[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const float th = __fmaf_rn(xs[t], sh, kMagic);
-    w[t] = __float_as_uint(th);
-    const float r = __fmaf_rn(-(th - kMagic), 256.f, xs[t] * (256.f * sh));
-    lo[t] = __float_as_uint(fminf(r, 127.f) + 12582912.f);
-  }
-  planes4(w[0], w[1], w[2], w[3], p1, p2, p3);
-  p4 = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+  const uint32_t w[4] = {(uint32_t)__float2int_rn(x0 * s) + 0x808080u, (uint32_t)__float2int_rn(x1 * s) + 0x808080u,
+                         (uint32_t)__float2int_rn(x2 * s) + 0x808080u, (uint32_t)__float2int_rn(x3 * s) + 0x808080u};
+  planes_of(w, p1, p2, p3, p4);
 }
 
 struct Params {
@@ -526,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = u0; u < total_units; u += ustep) {
       const Unit x = unit_of(p, u);
       const int gi = x.tile * 128 + row;
-      const float s = scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);
+      const float s = 256.f * scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);  // the row's 31-bit grid
       for (int c = 0; c < x.n; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
         const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots, sp = (g >> 1) & 1;
@@ -787,14 +771,7 @@ __global__ void __launch_bounds__(256) k_fdigits(const double* __restrict__ F, i
       any = true;
     }
     uint32_t p1 = 0u, p2 = 0u, p3 = 0u, p4 = 0u;
-    if (any) {  // byte t of plane j = digit j of element t
-      const uint32_t t01 = __byte_perm(wv[0], wv[1], 0x5140), t23 = __byte_perm(wv[2], wv[3], 0x5140);
-      const uint32_t u01 = __byte_perm(wv[0], wv[1], 0x7362), u23 = __byte_perm(wv[2], wv[3], 0x7362);
-      p4 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
-      p3 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
-      p2 = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;
-      p1 = __byte_perm(u01, u23, 0x7632);
-    }
+    if (any) planes_of(wv, p1, p2, p3, p4);  // byte t of plane j = digit j of element t
     uint32_t* rowq = D + (q * 4 * rp + k) * 32 + w;  // plane j's row: + j rp rows
     rowq[0] = p1;
     rowq[(size_t)rp * 32] = p2;

@@ -4,8 +4,7 @@
 Every fp32 row of M (a row for A = M W^T, a column for C = V^T M) is
 scaled by 256 s, s = scale_of(row max) (the row maximum at [2^30, 2^31)),
 and rounded to X = d1 2^24 + d2 2^16 + d3 2^8 + d4 (31-bit fixed point:
-entries within 2^7 of the maximum are exact; see digits() for the kernel's
-exact rounding).  Every fp64 factor row (a row of W, a column of V) is scaled
+entries within 2^7 of the maximum are exact).  Every fp64 factor row (a row of W, a column of V) is scaled
 by s_f = fscale_of(row max) and rounded to Y = e1 2^24 + e2 2^16 + e3 2^8 + e4
 (31-bit).  The kernel forms the digit products d_i e_j of weight classes
 c = i + j - 2 <= 3 (the rest are <= 2^-32 of the largest product), sums them
@@ -39,17 +38,16 @@ def fscale_of(mx):
 
 
 def digits(x, s):
-    """four balanced digits of fp32 M entries on the 31-bit grid X = x (256 s):
-    d1 d2 d3 from X_hi = round(x s) (half-even, the kernel's FFMA magic), the
-    low digit d4 = round(min(x 256 s - 256 X_hi, 127)) (ix_gemm.cu planes4x)"""
-    xs = np.asarray(x, np.float32).astype(np.float64) * s
-    Xh = np.rint(xs)
-    d4 = np.rint(np.minimum(xs * 256.0 - Xh * 256.0, 127.0))
-    d3 = np.mod(Xh + 128, 256) - 128
-    Xp = (Xh - d3) / 256
-    d2 = np.mod(Xp + 128, 256) - 128
-    d1 = (Xp - d2) / 256
-    return d1, d2, d3, d4
+    """four balanced digits of fp32 M entries on the 31-bit grid
+    X = round(x 256 s) (half-even: the kernel's F2I; x 256 s is exact)"""
+    X = np.rint(np.asarray(x, np.float32).astype(np.float64) * (256.0 * s))
+    out = []
+    for _ in range(3):
+        d = np.mod(X + 128, 256) - 128
+        out.append(d)
+        X = (X - d) / 256
+    out.append(X)
+    return out[::-1]  # d1, d2, d3, d4
 
 
 def fdigits(f, s):
