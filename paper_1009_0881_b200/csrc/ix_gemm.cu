@@ -80,13 +80,13 @@ constexpr int kMGroups = kMStages / kMGroup;
 constexpr int kBStages = 2;            // factor digit ring (TMA -> MMA), one chunk QUAD per stage
 constexpr int kBStageBytes = 32768;    // 4 planes x r_pad (<= 64) rows x 128 B (= 4 chunks x 32 K)
 constexpr int kQuad = 4;               // chunks per factor stage
-constexpr int kSlots = 4;              // TMEM staging slots: two pairs (chunk 2h -> slot 2(h&1), 2h+1 -> +1)
+constexpr int kSlots = 8;              // TMEM staging slots: four pairs (chunk g -> slot g % 8)
 constexpr int kPairs = kSlots / 2;
 constexpr int kSlotCols = 32;          // columns per slot (24 used)
 constexpr int kGroupCols = 64;         // columns per accumulator group (r_pad <= 64)
 constexpr int kClasses = 4;            // digit-product weight classes 2^40, 2^32, 2^24, 2^16
 constexpr int kAccCols = kClasses * kGroupCols;
-constexpr int kStg0 = 384;             // staging slots after the (single) accumulator set
+constexpr int kStg0 = 256;             // staging slots after the (single) accumulator set
 static_assert(kAccCols <= kStg0 && kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
 // factor fixed point: 31 bits (four digits e1 e2 e3 e4, e1 in [0, 127])
 constexpr double kFBias = 8421504.0;   // 0x808080: balanced low three digits
@@ -94,10 +94,11 @@ constexpr double kFBias = 8421504.0;   // 0x808080: balanced low three digits
 // K element, so an int32 accumulator is exact for K <= 2^31 / 2^16 = 32768
 // = 1024 chunks
 constexpr int kMaxUnitChunks = 1024;
-constexpr int kConvGroups = 2;
+constexpr int kConvGroups = 4;         // converter groups (4 warps each), chunk g -> group g % 4
+constexpr int kEpiWarps = 4;           // epilogue: one warp per TMEM lane quarter
 constexpr int kWarpM = 0, kWarpMma = 1, kWarpB = 2, kWarpConv0 = 3;
 constexpr int kWarpEpi0 = kWarpConv0 + 4 * kConvGroups;
-constexpr int kThreads = (kWarpEpi0 + 8) * 32;
+constexpr int kThreads = (kWarpEpi0 + kEpiWarps) * 32;
 constexpr int kMTileBytes = 128 * kChunk * 4;  // 16 KB
 // the row maximum's grid position: max * s_hi <= kXMax (then x * 256 s_hi < 2^31 - 0x808080)
 constexpr float kXMax = 8355711.0f;            // 2^23 - 0x8080 - 1
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&mempty[i]), 4 * kMGroup);  // the 4 converter warps of each slice
     }
     for (int i = 0; i < kPairs; ++i) {
-      mbar_init(smem_u32(&ready[i]), 4 * kConvGroups);  // both groups' 4 warps
+      mbar_init(smem_u32(&ready[i]), 4 * 2);  // the 4 converter warps of each of the pair's chunks
       mbar_init(smem_u32(&sdone[i]), 1);
     }
     for (int i = 0; i < kBStages; ++i) {
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&afull[i]), 1);
-      mbar_init(smem_u32(&aempty[i]), 8);  // the 8 epilogue warps
+      mbar_init(smem_u32(&aempty[i]), kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_m)) : "memory");
@@ -473,14 +474,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (phase 0 = the initial zeroing)
       mbar_wait(smem_u32(&aempty[0]), (uint32_t)uc & 1u);
       for (int i = 0; i < n_u; i += 2, ++h) {
-        const int ps = h & 1, qc = h >> 1, bs = qc % kBStages;
-        mbar_wait(smem_u32(&ready[ps]), (uint32_t)(h >> 1) & 1u);
+        const int ps = h % kPairs, qc = h >> 1, bs = qc % kBStages;
+        mbar_wait(smem_u32(&ready[ps]), (uint32_t)(h / kPairs) & 1u);
         if (!(h & 1)) mbar_wait(smem_u32(&bfull[bs]), (uint32_t)(qc / kBStages) & 1u);
         tc_fence_after();
         // chunk (2h) % 4 of the quad: its K columns at byte 32 (2h % 4)
         const uint64_t bd = bdesc0 + ((uint64_t)(bs * kBStageBytes) >> 4) + (uint64_t)(4 * (h & 1));
-        if (ps == 0) issue_pair<0>(bd, bd + 2, id4, id3, id2, id1, rp);
-        else issue_pair<1>(bd, bd + 2, id4, id3, id2, id1, rp);
+        switch (ps) {
+          case 0: issue_pair<0>(bd, bd + 2, id4, id3, id2, id1, rp); break;
+          case 1: issue_pair<1>(bd, bd + 2, id4, id3, id2, id1, rp); break;
+          case 2: issue_pair<2>(bd, bd + 2, id4, id3, id2, id1, rp); break;
+          default: issue_pair<3>(bd, bd + 2, id4, id3, id2, id1, rp); break;
+        }
         tc_commit(smem_u32(&sdone[ps]));                // slot pair reusable once these MMAs finish
         if (h & 1) tc_commit(smem_u32(&bempty[bs]));  // ... and, after a quad's second pair, its factor stage
         __syncwarp();
@@ -513,8 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float s = 256.f * scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);  // the row's 31-bit grid
       for (int c = 0; c < x.n; ++c, ++g) {
         if (g % kConvGroups != grp) continue;
-        const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots, sp = (g >> 1) & 1;
-        const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g >> 2) & 1u;
+        const int pg = g / kMGroup, ps = pg % kMGroups, slot = g % kSlots, sp = (g >> 1) % kPairs;
+        const uint32_t mph = (uint32_t)(pg / kMGroups) & 1u, sphase = (uint32_t)(g / kSlots) & 1u;
         mbar_wait(smem_u32(&mfull[ps]), mph);
         // digit planes d1 (words 0..7) | d2 (8..15) | d3 (16..23) | d4 (24..31);
         // word j holds elements 4j .. 4j + 3, element t of the word in byte t
@@ -575,24 +580,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ======================= epilogue: int32 groups -> fp64 =======================
-    // 8 warps: lane quarter q (TMEM access rule), column half cb = 0 / 32.
+    // 4 warps: lane quarter q (TMEM access rule), all r_pad columns.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int cb = ((warp - kWarpEpi0) >> 2) * 32;
-    const bool live = cb < p.rp;
-    // this lane's output column cb + lane: 1 / s_f (broadcast by shuffles)
-    const double cinv = (cb + lane < p.r) ? 1.0 / fscale_of(p.fmax[cb + lane]) : 0.0;
-    // class c of output column k is TMEM column c r_pad + k; this warp owns
-    // columns cb .. cb + 31 of each class (8-column blocks below r_pad)
-    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + cb;
+    // output column k's 1 / s_f: lane holds columns lane and 32 + lane
+    // (broadcast by shuffles)
+    const double cinv0 = lane < p.r ? 1.0 / fscale_of(p.fmax[lane]) : 0.0;
+    const double cinv1 = 32 + lane < p.r ? 1.0 / fscale_of(p.fmax[32 + lane]) : 0.0;
+    // class c of output column k is TMEM column c r_pad + k (8-column blocks
+    // below r_pad)
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t zero[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     auto zero_acc = [&]() {
 #pragma unroll
       for (int c = 0; c < kClasses; ++c)
 #pragma unroll
-        for (int h = 0; h < 4; ++h)
-          if (cb + h * 8 < p.rp)
-            tmem_st8(tq + c * p.rp + h * 8, reinterpret_cast<const uint32_t(&)[8]>(zero[0]));
+        for (int h = 0; h < kGroupCols / 8; ++h)
+          if (h * 8 < p.rp) tmem_st8(tq + c * p.rp + h * 8, reinterpret_cast<const uint32_t(&)[8]>(zero[0]));
       tmem_wait_st();
     };
     // the accumulators start at zero and are re-zeroed after every drain:
@@ -608,10 +612,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double rinv = 1.0 / (double)scale_of(gi < p.rows ? p.rowmax[gi] : 0.f);
       mbar_wait<256>(smem_u32(&afull[0]), (uint32_t)uc & 1u);
       tc_fence_after();
-      if (live) {
+      {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {  // 8 columns at a time
-          if (cb + h * 8 >= p.rp) break;
+        for (int h = 0; h < kGroupCols / 8; ++h) {  // 8 columns at a time
+          if (h * 8 >= p.rp) break;
           uint32_t g[kClasses][8];
 #pragma unroll
           for (int c = 0; c < kClasses; ++c) tmem_ld8(tq + c * p.rp + h * 8, g[c]);
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const int k = h * 8 + kk;
-            const double ck = __shfl_sync(0xffffffffu, cinv, k);  // all lanes: outside the row guard
+            const double ck = __shfl_sync(0xffffffffu, k < 32 ? cinv0 : cinv1, k & 31);  // all lanes
             // sum X Y = 2^24 (G0 2^24 + G1 2^16 + G2 2^8 + G3), the bracket
             // exact in int64 (|G0| < 2^14 K <= 2^29 for a unit's K <= 32768),
             // then one fp64 rounding; X = x * 256 s_hi, so the 2^24 / 256
@@ -627,11 +631,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long S =
                 (((long long)(int)g[0][kk] * 256ll + (int)g[1][kk]) * 256ll + (int)g[2][kk]) * 256ll + (int)g[3][kk];
             const double v = (double)S * 65536.0 * rinv * ck;
-            if (gi < p.rows && cb + k < p.r) {
+            if (gi < p.rows && k < p.r) {
               if (!TRANS)
-                p.part[(size_t)x.split * p.rows * p.r + (size_t)gi * p.r + cb + k] = v;
+                p.part[(size_t)x.split * p.rows * p.r + (size_t)gi * p.r + k] = v;
               else
-                p.part[(size_t)x.split * p.r * p.rows + (size_t)(cb + k) * p.rows + gi] = v;
+                p.part[(size_t)x.split * p.r * p.rows + (size_t)k * p.rows + gi] = v;
             }
           }
         }

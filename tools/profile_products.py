@@ -30,9 +30,14 @@ def main():
         s.run_configuration(1, "hals", "none", 64, 0, 0.0, 0)  # random_init
         s.products()  # warm-up (buffer allocation)
         s.set_profiling(True)
-        for _ in range(a.reps):
-            s.products()
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import ClockSampler
+        with ClockSampler(0) as clk:
+            for _ in range(a.reps):
+                s.products()
+            s.sync()
         kt = s.kernel_times()
+        print("clocks during the products:", clk.summary())
         mb = 65536 * a.n * 4
         mw, vt = kt["mwt_ms"] / kt["mwt_n"], kt["vtm_ms"] / kt["vtm_n"]
         print(f"n={a.n} tc={s.tc_active} A=MW^T {mw:.3f} ms ({mb / mw / 1e6:.0f} GB/s)  "
