@@ -162,7 +162,15 @@ def bcast_obj(b, world):
 # ---------------------------------------------------------------------------
 # reference arm (CPU): oracle/_ref on column slices of config 4
 # ---------------------------------------------------------------------------
-def reference_steps(steps, warmup, slices=(128, 512)):
+REF_SLICES = (128, 512, 4096)
+
+
+def reference_steps(steps, warmup, slices=REF_SLICES):
+    """The reference's hals_step (oracle/_ref: the unmodified mlnmf sources,
+    fp64, OpenMP) on column slices of config 4, median of `steps` timed steps
+    each after `warmup`; a least-squares line t = a + b n through the slice
+    medians, evaluated at n = 262144.  Returns (t_full, info) with the slice
+    times, the fit and its largest relative residual at the slices."""
     import oracle
     ref, restated = oracle.Reference(), oracle.Restated()
     data = {}
@@ -180,18 +188,20 @@ def reference_steps(steps, warmup, slices=(128, 512)):
             data[ns][1], data[ns][2] = V, W
             if it >= warmup:
                 times[ns].append(dt)
-    n1, n2 = slices
-    t1, t2 = float(np.median(times[n1])), float(np.median(times[n2]))
-    b = (t2 - t1) / (n2 - n1)
-    a = t1 - b * n1
-    return a + b * N_TOTAL, dict(t_slices_s={str(k): float(np.median(v)) for k, v in times.items()},
-                                 fit_a_s=a, fit_b_s_per_col=b)
+    x = np.array(slices, dtype=np.float64)
+    y = np.array([float(np.median(times[ns])) for ns in slices])
+    b, a = np.polyfit(x, y, 1)
+    resid = float(np.max(np.abs((a + b * x) - y) / y))
+    return a + b * N_TOTAL, dict(t_slices_s={str(k): float(v) for k, v in zip(slices, y)},
+                                 fit_a_s=float(a), fit_b_s_per_col=float(b), fit_max_rel_residual=resid)
 
 
 def ref_sample_text(steps, info):
-    return (f"reference hals_step (oracle/_ref = unmodified mlnmf sources, fp64, OpenMP) on column slices "
-            f"n=128 and n=512 of config 4 (m=65536, r=64), median of {steps} steps each, extrapolated linearly "
-            f"in n to n=262144: t = {info['fit_a_s']:.4f} s + {info['fit_b_s_per_col'] * 1e3:.4f} ms/column")
+    pts = ", ".join(f"n={k}: {v:.4f} s" for k, v in info["t_slices_s"].items())
+    return (f"reference hals_step (oracle/_ref = unmodified mlnmf sources, fp64, OpenMP) on column slices of "
+            f"config 4 (m=65536, r=64), median of {steps} steps each ({pts}); least-squares line "
+            f"t = {info['fit_a_s']:.4f} s + {info['fit_b_s_per_col'] * 1e3:.4f} ms/column through the three points "
+            f"(max relative residual {info['fit_max_rel_residual'] * 100:.2f} %), evaluated at n=262144")
 
 
 def run_reference(args):
@@ -223,7 +233,7 @@ def cpu_baseline():
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     t_full, info = reference_steps(steps=3, warmup=1)
     return {"value": 1.0 / t_full, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": ref_sample_text(3, info)}
+            "sample": ref_sample_text(3, info), **info}
 
 
 # ---------------------------------------------------------------------------

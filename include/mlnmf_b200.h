@@ -181,6 +181,39 @@ int mlnmf_session_run_cycle(mlnmf_session* s, size_t hierarchy_levels, size_t le
 /* level-0 factors: V (m x r), this rank's W columns (r x n_local) */
 int mlnmf_session_get_factors(mlnmf_session* s, void* V, void* W_local, int host_dtype);
 int mlnmf_session_set_factors(mlnmf_session* s, const void* V, const void* W_local, int host_dtype, size_t r);
+/* ---- resident per-level entries: the pieces of a multilevel cycle on the
+ * session's device-resident pyramid (SURVEY 8(b) minimum), so a caller that
+ * drives its own cycle (the reference's CycleRunner, multilevel.cpp:14-89, or
+ * the drop-in shim's run_solver_phase) never re-uploads M. ---- */
+/* GridHierarchy::build (transfer.cpp:155-174) up to level_count levels on the
+ * device: R(M) restricted column-locally, no communication. */
+int mlnmf_session_build_levels(mlnmf_session* s, size_t level_count);
+size_t mlnmf_session_num_levels(mlnmf_session* s);
+/* ImageGrid of a built level (coarsen_grid, transfer.cpp:55-59) */
+int mlnmf_session_level_shape(mlnmf_session* s, size_t level, size_t* grid_h, size_t* grid_w);
+/* random_init(m, n_total, r, seed) at level 0 on the device (matrix.cpp:51-60;
+ * each rank draws its own W columns) */
+int mlnmf_session_init_random(mlnmf_session* s, size_t r, uint64_t seed);
+/* V at `level` (m_level x r) and this rank's W columns (r x n_local) */
+int mlnmf_session_set_factors_level(mlnmf_session* s, size_t level, const void* V, const void* W_local,
+                                    int host_dtype, size_t r);
+int mlnmf_session_get_factors_level(mlnmf_session* s, size_t level, void* V, void* W_local, int host_dtype);
+/* V_{level+1} = R_level V_level and V_level = P_level V_{level+1}
+ * (multilevel.cpp:39,41 -- CycleRunner::nested / vcycle / fmg) */
+int mlnmf_session_restrict_V(mlnmf_session* s, size_t level);
+int mlnmf_session_prolong_V(mlnmf_session* s, size_t level);
+/* run_solver_phase (solvers.hpp:90-92, solvers.cpp:300-341) on the resident
+ * level: kind MLNMF_MU/HALS/ANLS, budget_mode MLNMF_WORK_UNITS (amount work
+ * units, each step charged step_flops / unit_flops) or
+ * MLNMF_WALL_CLOCK_SECONDS; samples at start, every trace_every steps and at
+ * the end, stamped with *work_consumed (the run's cumulative work units,
+ * advanced in place, SolveContext::work_consumed).  *leftover = the
+ * unconsumed amount (the reference's return value).  The phase trace holds
+ * the samples (level = level + 1, times relative to the phase start), the
+ * NNLS counts, degenerate columns and the phase's step count. */
+int mlnmf_session_run_phase(mlnmf_session* s, size_t level, int kind, int budget_mode, double amount,
+                            double step_flops, double unit_flops, size_t trace_every, double* work_consumed,
+                            double* leftover, mlnmf_trace** trace_out);
 /* Enqueue n_steps solver sweeps at level 0 with no error samples (bench). */
 int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps);
 int mlnmf_session_sync(mlnmf_session* s);

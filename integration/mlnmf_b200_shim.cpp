@@ -40,9 +40,7 @@ void check(int rc) {
   }
 }
 
-void configure_once() {
-  static bool done = false;
-  if (done) return;
+mlnmf_options shim_options() {
   mlnmf_options o;
   mlnmf_default_options(&o);
   const char* fp32 = std::getenv("MLNMF_B200_FP32");
@@ -50,9 +48,24 @@ void configure_once() {
   o.dtype = fast ? MLNMF_F32 : MLNMF_F64;
   o.exact = fast ? 0 : 1;
   if (const char* d = std::getenv("MLNMF_B200_DEVICE")) o.device = std::atoi(d);
+  return o;
+}
+
+void configure_once() {
+  static bool done = false;
+  if (done) return;
+  const mlnmf_options o = shim_options();
   check(mlnmf_set_default_options(&o));
   done = true;
 }
+
+// a session owned for one call (destroyed on every exit path)
+struct SessionGuard {
+  mlnmf_session* s = nullptr;
+  ~SessionGuard() {
+    if (s) mlnmf_session_destroy(s);
+  }
+};
 
 int kind_of(SolverKind k) {
   switch (k) {
@@ -131,45 +144,36 @@ void anls_step(const Matrix& M, Matrix& V, Matrix& W, std::vector<int>* iter_cou
 }
 
 // ---------------------------------------------------------------- budget loop
-// run_solver_phase (solvers.cpp:300-341): the phase-level entry keeps the
-// reference's host accounting and drives the device one step at a time (each
-// step a C-ABI call with H2D/D2H; the whole-run entries below keep M, V, W
-// resident on the device instead).
+// run_solver_phase (solvers.cpp:300-341): M is uploaded ONCE per phase into a
+// device session and the whole phase -- the reference's budget loop, its
+// samples every trace_every steps and at both ends, the NNLS counts -- runs
+// resident through mlnmf_session_run_phase; V and W come back at the end.
+// The caller's SolveContext keeps the reference's accounting: work_consumed
+// advances by the phase's charges, sample times are ctx-relative, samples
+// carry the caller's `level`.
 double run_solver_phase(const Matrix& M, Matrix& V, Matrix& W, SolverKind kind, Budget::Mode mode, double amount,
                         double step_flops, int level, std::size_t trace_every, SolveContext& ctx) {
   configure_once();
   same_shape(M, V, W);
-  const double charge = step_flops / ctx.unit_flops;
-  const double eps = 1e-12 * (amount > 1.0 ? amount : 1.0);
-  const double phase_start_s = ctx.elapsed_s();
-  auto sample = [&] {
-    double e = 0.0;
-    check(mlnmf_frobenius_error(M.data(), V.data(), W.data(), M.rows(), M.cols(), V.cols(), &e));
-    ctx.trace.samples.push_back(TraceSample{ctx.elapsed_s(), ctx.work_consumed, level, e});
-  };
-  sample();
-  double consumed = 0.0;
-  std::size_t steps = 0;
-  for (;;) {
-    if (mode == Budget::Mode::kWorkUnits) {
-      if (consumed + charge > amount + eps) break;
-    } else if (ctx.elapsed_s() - phase_start_s >= amount) {
-      break;
-    }
-    switch (kind) {
-      case SolverKind::kMu: mu_step(M, V, W); break;
-      case SolverKind::kHals: hals_step(M, V, W, &ctx.trace.hals_degenerate_columns); break;
-      case SolverKind::kAnls: anls_step(M, V, W, &ctx.trace.nnls_iteration_counts); break;
-    }
-    consumed += charge;
-    ctx.work_consumed += charge;
-    ++steps;
-    if (trace_every > 0 && steps % trace_every == 0) sample();
-  }
-  sample();
-  if (mode == Budget::Mode::kWorkUnits) return amount - consumed;
-  const double left = amount - (ctx.elapsed_s() - phase_start_s);
-  return left > 0.0 ? left : 0.0;
+  const mlnmf_options o = shim_options();
+  SessionGuard g;
+  check(mlnmf_session_create(&o, &g.s));
+  check(mlnmf_session_set_data(g.s, M.data(), MLNMF_F64, M.rows(), M.cols(), M.cols(), 0, M.rows(), 1));
+  check(mlnmf_session_set_factors(g.s, V.data(), W.data(), MLNMF_F64, V.cols()));
+  const double t0 = ctx.elapsed_s();
+  double wc = ctx.work_consumed, left = 0.0;
+  mlnmf_trace* t = nullptr;
+  check(mlnmf_session_run_phase(g.s, 0, kind_of(kind), mode_of(mode), amount, step_flops, ctx.unit_flops,
+                                trace_every, &wc, &left, &t));
+  RunTrace ph = take_trace(t);
+  check(mlnmf_session_get_factors(g.s, V.data(), W.data(), MLNMF_F64));
+  for (auto& smp : ph.samples) ctx.trace.samples.push_back(TraceSample{t0 + smp.elapsed_s, smp.work_units, level,
+                                                                         smp.error});
+  ctx.trace.nnls_iteration_counts.insert(ctx.trace.nnls_iteration_counts.end(), ph.nnls_iteration_counts.begin(),
+                                         ph.nnls_iteration_counts.end());
+  ctx.trace.hals_degenerate_columns += ph.hals_degenerate_columns;
+  ctx.work_consumed = wc;
+  return left;
 }
 
 // ---------------------------------------------------------------- whole runs
@@ -184,6 +188,10 @@ SolveResult run_solver(const Matrix& M, const Matrix& V0, const Matrix& W0, Solv
   return SolveResult{std::move(V), std::move(W), take_trace(t)};
 }
 
+#ifndef MLNMF_SHIM_PHASES_ONLY
+// (MLNMF_SHIM_PHASES_ONLY: leave the multilevel entries to the reference's
+// own multilevel.cpp, whose CycleRunner then drives run_solver_phase above
+// -- the `make -C oracle dropin` variant acceptance_b200_phases.)
 static MultilevelResult cycle_on(const GridHierarchy& h, std::size_t levels, const Matrix& V0, const Matrix& W0,
                                  SolverKind kind, CycleKind cycle, Budget budget, std::size_t trace_every) {
   configure_once();
@@ -222,5 +230,6 @@ MultilevelResult run_configuration(const Matrix& M, const ImageGrid& grid, std::
                                 V.data(), W.data(), &t));
   return MultilevelResult{std::move(V), std::move(W), take_trace(t)};
 }
+#endif  // MLNMF_SHIM_PHASES_ONLY
 
 }  // namespace mlnmf

@@ -214,6 +214,16 @@ _proto("mlnmf_session_run_cycle", C.c_int, _vp, _sz, _sz, _vp, _vp, C.c_int, _sz
 _proto("mlnmf_session_get_factors", C.c_int, _vp, _vp, _vp, C.c_int)
 _proto("mlnmf_session_set_factors", C.c_int, _vp, _vp, _vp, C.c_int, _sz)
 _proto("mlnmf_session_steps", C.c_int, _vp, C.c_int, _sz)
+_proto("mlnmf_session_build_levels", C.c_int, _vp, _sz)
+_proto("mlnmf_session_num_levels", _sz, _vp)
+_proto("mlnmf_session_level_shape", C.c_int, _vp, _sz, C.POINTER(_sz), C.POINTER(_sz))
+_proto("mlnmf_session_init_random", C.c_int, _vp, _sz, C.c_uint64)
+_proto("mlnmf_session_set_factors_level", C.c_int, _vp, _sz, _vp, _vp, C.c_int, _sz)
+_proto("mlnmf_session_get_factors_level", C.c_int, _vp, _sz, _vp, _vp, C.c_int)
+_proto("mlnmf_session_restrict_V", C.c_int, _vp, _sz)
+_proto("mlnmf_session_prolong_V", C.c_int, _vp, _sz)
+_proto("mlnmf_session_run_phase", C.c_int, _vp, _sz, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _sz,
+       _dp, _dp, C.POINTER(_vp))
 _proto("mlnmf_session_sync", C.c_int, _vp)
 _proto("mlnmf_session_error", C.c_int, _vp, _dp)
 _proto("mlnmf_session_norm2", C.c_int, _vp, _sz, _dp)
@@ -773,6 +783,58 @@ class Session:
 
     def get_factors_ptr(self, V_ptr: int, W_ptr: int, host_dtype: int):
         _check(_lib.mlnmf_session_get_factors(self._h, V_ptr, W_ptr, host_dtype))
+
+    # ---- resident per-level pieces of a multilevel cycle ----
+    def build_levels(self, level_count: int):
+        """GridHierarchy::build on the device (transfer.cpp:155-174)."""
+        _check(_lib.mlnmf_session_build_levels(self._h, level_count))
+
+    @property
+    def num_levels(self) -> int:
+        return int(_lib.mlnmf_session_num_levels(self._h))
+
+    def level_grid(self, level: int) -> ImageGrid:
+        h, w = _sz(), _sz()
+        _check(_lib.mlnmf_session_level_shape(self._h, level, C.byref(h), C.byref(w)))
+        return ImageGrid(h.value, w.value)
+
+    def init_random(self, r: int, seed: int):
+        """random_init(m, n_total, r, seed) at level 0 (matrix.cpp:51-60)."""
+        _check(_lib.mlnmf_session_init_random(self._h, r, seed))
+        self.r = r
+
+    def set_factors_level(self, level: int, V, W_local):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        W = np.ascontiguousarray(W_local, dtype=np.float64)
+        _check(_lib.mlnmf_session_set_factors_level(self._h, level, V.ctypes.data, W.ctypes.data, F64, V.shape[1]))
+        self.r = V.shape[1]
+
+    def get_factors_level(self, level: int):
+        g = self.level_grid(level)
+        V = np.zeros((g.pixels(), self.r))
+        W = np.zeros((self.r, self.n_local))
+        _check(_lib.mlnmf_session_get_factors_level(self._h, level, V.ctypes.data, W.ctypes.data, F64))
+        return V, W
+
+    def restrict_V(self, level: int):
+        """V_{level+1} = R V_level (multilevel.cpp:39)."""
+        _check(_lib.mlnmf_session_restrict_V(self._h, level))
+
+    def prolong_V(self, level: int):
+        """V_level = P V_{level+1} (multilevel.cpp:41)."""
+        _check(_lib.mlnmf_session_prolong_V(self._h, level))
+
+    def run_phase(self, level: int, kind, budget, step_flops: float, unit_flops: float, trace_every: int = 1,
+                  work_consumed: float = 0.0):
+        """run_solver_phase (solvers.cpp:300-341) on the resident level.
+        Returns (leftover, work_consumed, trace): the unconsumed amount, the
+        run's advanced cumulative work and the phase trace (sample times
+        relative to the phase start)."""
+        mode, amount = _budget(budget)
+        wc, left, tp = C.c_double(work_consumed), C.c_double(), _vp()
+        _check(_lib.mlnmf_session_run_phase(self._h, level, _kind(kind), mode, amount, step_flops, unit_flops,
+                                            trace_every, C.byref(wc), C.byref(left), C.byref(tp)))
+        return left.value, wc.value, _take_trace(tp.value)
 
     def steps(self, kind, n_steps: int):
         _check(_lib.mlnmf_session_steps(self._h, _kind(kind), n_steps))

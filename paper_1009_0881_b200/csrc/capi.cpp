@@ -414,6 +414,69 @@ int mlnmf_session_set_factors(mlnmf_session* s, const void* V, const void* W_loc
   return guard([&] { s->e->set_factors(0, V, W_local, host_dtype, r); });
 }
 
+// ---- resident per-level entries (SURVEY 8(b) minimum) ----
+int mlnmf_session_build_levels(mlnmf_session* s, size_t level_count) {
+  return guard([&] { s->e->ensure_levels(level_count); });
+}
+
+size_t mlnmf_session_num_levels(mlnmf_session* s) { return s->e->built_levels(); }
+
+int mlnmf_session_level_shape(mlnmf_session* s, size_t level, size_t* grid_h, size_t* grid_w) {
+  return guard([&] {
+    if (level >= s->e->built_levels()) throw std::invalid_argument("level not built");
+    *grid_h = s->e->grid_h(level);
+    *grid_w = s->e->grid_w(level);
+  });
+}
+
+int mlnmf_session_init_random(mlnmf_session* s, size_t r, uint64_t seed) {
+  return guard([&] { s->e->init_random(r, seed); });
+}
+
+int mlnmf_session_set_factors_level(mlnmf_session* s, size_t level, const void* V, const void* W_local,
+                                    int host_dtype, size_t r) {
+  return guard([&] {
+    if (level >= s->e->built_levels()) throw std::invalid_argument("level not built");
+    s->e->set_factors(level, V, W_local, host_dtype, r);
+  });
+}
+
+int mlnmf_session_get_factors_level(mlnmf_session* s, size_t level, void* V, void* W_local, int host_dtype) {
+  return guard([&] {
+    if (level >= s->e->built_levels()) throw std::invalid_argument("level not built");
+    if (s->e->rank_r() == 0) throw std::invalid_argument("factors not set");
+    s->e->get_factors(level, V, W_local, host_dtype);
+  });
+}
+
+int mlnmf_session_restrict_V(mlnmf_session* s, size_t level) {
+  return guard([&] {
+    if (level + 1 >= s->e->built_levels()) throw std::invalid_argument("restrict_V: level + 1 not built");
+    s->e->restrict_V(level);
+  });
+}
+
+int mlnmf_session_prolong_V(mlnmf_session* s, size_t level) {
+  return guard([&] {
+    if (level + 1 >= s->e->built_levels()) throw std::invalid_argument("prolong_V: level + 1 not built");
+    s->e->prolong_V(level);
+  });
+}
+
+int mlnmf_session_run_phase(mlnmf_session* s, size_t level, int kind, int budget_mode, double amount,
+                            double step_flops, double unit_flops, size_t trace_every, double* work_consumed,
+                            double* leftover, mlnmf_trace** trace_out) {
+  if (trace_out) *trace_out = nullptr;
+  return guard([&] {
+    if (s->e->rank_r() == 0) throw std::invalid_argument("run_phase: factors not set");
+    RunTrace t;
+    const double left = run_phase(*s->e, level, to_kind(kind), budget_mode, amount, step_flops, unit_flops,
+                                  trace_every, work_consumed, t);
+    if (leftover) *leftover = left;
+    emit_trace(std::move(t), trace_out);
+  });
+}
+
 int mlnmf_session_steps(mlnmf_session* s, int kind, size_t n_steps) {
   return guard([&] {
     const Kind k = to_kind(kind);

@@ -5,57 +5,64 @@
 //   product 1 (TRANS = false):  A (m x r)   = M (m x n) . W^T    (kernels.cpp:24-34; solvers.cpp:82,105,252)
 //   product 2 (TRANS = true):   C^T (n x r) = M^T (n x m) . V    (kernels.cpp:36-46; solvers.cpp:91,124,273)
 //
-// Number format.  Every fp32 operand x of an MMA row (a row of M for product
-// 1, a column of M for product 2, a row of W / column of V on the factor
-// side) is scaled by a power of two s = 2^e chosen from the row maximum, so
-// that x*s < 2^23 - 0x8080, rounded once to the nearest integer X, and X is
-// split into balanced base-256 digits
-//     X = d1 * 2^16 + d2 * 2^8 + d3,   d1 in [0, 127], d2, d3 in [-128, 127].
-// The rounding is unbiased (round-to-nearest-even of a single FFMA), and the
-// digits are exact, signed 8-bit integers.  With F likewise split into
-// e1, e2, e3, EVERY digit product d_i e_j is formed, summed over K by weight
-// class i + j,
-//     G0 = sum d1 e1,  G1 = sum d1 e2 + d2 e1,  G2 = sum d1 e3 + d2 e2 + d3 e1,
-//     G3 = sum d2 e3 + d3 e2,  G4 = sum d3 e3,
-// and accumulated in int32 TMEM by `tcgen05.mma.kind::i8` -- EXACTLY: no
-// rounding, no truncation, independent of the accumulation order -- so
-//     sum X Y = G0 2^32 + G1 2^24 + G2 2^16 + G3 2^8 + G4
-// is the exact integer dot product of the rounded operands (int64, then one
-// fp64 rounding), and sum x f = (sum X Y) / (s_x s_f).  The products carry
-// only the unbiased grid rounding of the inputs (<= 2^-23 of the row
-// maximum per element), which averages out along K (~1e-9 .. 1e-8 relative).
-// An earlier form dropped G3 and G4: a factor entry below 1/128 of its row's
-// maximum (leading digit d2 or d3; common in sparse NMF factors) then kept
-// only ~16 bits, which moved the config-4 FMG trajectory 1e-4 off the
-// reference's; with all nine products it tracks within the fp32-storage
-// noise.
-// Throughput: 9 MMAs of N = r_pad, K = 32 per 32-wide chunk at the i8 rate
-// (288 tensor cycles per 128-row chunk, ~45 % of the chunk's HBM time), and
-// 96 B per row per chunk of converter stores into TMEM.
+// Number format (tests/ixmodel.py is its numpy model).  Every fp32 entry x
+// of an MMA row of M (a row for product 1, a column for product 2) is scaled
+// by a power of two s chosen from the row maximum (max * s in [2^30, 2^31))
+// and rounded once (half-even, one F2I) to X = round(x s): a 31-bit fixed
+// point on which every fp32 entry within 2^7 of the maximum is EXACT.  Every
+// fp64 factor entry f (a row of W, a column of V; the factors are fp64 on the
+// device) is likewise rounded to Y = round(f s_f) on its row's 31-bit grid.
+// Both are split into balanced base-256 digits
+//     X = d1 2^24 + d2 2^16 + d3 2^8 + d4,   Y = e1 2^24 + e2 2^16 + e3 2^8 + e4
+// (d1, e1 in [0, 127]; the others in [-128, 127]: the bytes of X + 0x808080).
+// The digit products d_i e_j of weight classes c = i + j - 2 <= 3 are summed
+// over K per class in int32 TMEM by `tcgen05.mma.kind::i8` -- exactly, in
+// any order -- and
+//     sum x f ~= 2^24 (G0 2^24 + G1 2^16 + G2 2^8 + G3) / (s s_f)
+// (the bracket exact in int64, then one fp64 rounding).  Classes 4..6
+// (d2 e4, d3 e3, d4 e2, d3 e4, d4 e3, d4 e4) are <= 2^-32 of the largest
+// product and are not formed.  The products are then accurate to ~1e-9
+// (tests), and whole fp32 runs through this path track the fp64 reference
+// (fed the same fp32 M) as closely as the fp64-accumulating SIMT path does:
+// 5e-8 single-level / 1.6e-6 five-level FMG on the config-4 slice
+// (tests/test_gpu_tc_config4.py; the FMG floor is the fp32 storage of the
+// restricted pyramid, not the products).
+// History (r02, measured): a 3-digit M x 3-digit factor split keeping six
+// products drifted 1e-4 from the reference (a small factor entry, leading
+// digit d2 or d3, kept ~16 bits); all nine products 1.4e-5; a 23-bit factor
+// grid let the Gram-identity error samples cancel 5e-5 at coarse levels.
 //
-// The kernel (persistent, warp-specialised, one CTA per SM, 608 threads):
+// MMA shape: the four factor digit planes are STACKED along N in shared
+// memory ([e1; e2; e3; e4], r_pad rows each), and M digit plane d_i (TMEM,
+// the A operand) multiplies the prefix [e1 .. e_(5-i)] (N = (5 - i) r_pad)
+// into the accumulator window starting at class group i - 1: block j lands
+// on group i + j - 2, so the overlapping windows do the class sums.  4 MMAs
+// per 32-wide chunk (N = 4, 3, 2, 1 x r_pad; 320 tensor cycles per 128-row
+// chunk at r_pad = 64, ~40 % of the chunk's HBM time at 1.9 GHz).
+//
+// The kernel (persistent, warp-specialised, one CTA per SM, 736 threads):
 //   warp 0: TMA producer of M slices (16 KB, issued and released in pairs;
 //           product 1 fetches a chunk pair as one 3-D box of 128 rows x 256 B)
 //   warp 1: MMA issuer (allocates TMEM): per chunk PAIR one wait on the
-//           pair's staging slots, one on its factor stage, 18 MMAs (9 per
-//           chunk) from the digit planes in TMEM (A operand) and the factor
-//           digit planes in shared memory (B operand), two commits; one
-//           accumulator set (5 x 64 int32 columns) per work unit, drained
-//           by the epilogue between units.  This warp's issue loop is the serial path of the
-//           pipeline (ncu r02a: ~85 % busy at one chunk per stage), so its
-//           bookkeeping is amortised over two chunks.
-//   warp 2: TMA producer of factor digit slices (2 x r_pad rows x 128 B:
-//           planes e1 | e2 | e3 | 0, SWIZZLE_128B), one per chunk pair
-//   warps 3-10: converters (two groups of 4 alternating chunks): fp32 slice
-//           from shared memory -> one FFMA per element -> byte permutes into
-//           the digit planes d1 | d2 | d3 -> tcgen05.st into a staging slot
-//   warps 11-18: epilogue: drains a unit's five accumulators once (windows
-//           are whole work units of <= kMaxUnitChunks chunks, well inside the
-//           int32 range), converts to fp64 and writes the split-K partial.
-// TMEM (512 columns): the accumulator set at 0 (classes at +0, +64, ..., +256),
-// staging slots at 384 + 32 s, s < 4 (24 columns used: d1 | d2 | d3); chunk
-// g uses slot g % 4, so chunk pair h owns slots 2 (h & 1) and 2 (h & 1) + 1.
-// Work units hold an even number of chunks (a zero chunk pads an odd K).
+//           pair's staging slots, 8 MMAs, one commit; the factor stage (a
+//           chunk QUAD) is waited for by a quad's first pair and released by
+//           its second.  One accumulator set (4 classes x r_pad int32
+//           columns) per work unit, drained and zeroed by the epilogue
+//           between units (the MMAs always accumulate).
+//   warp 2: TMA producer of factor digit quads (4 r_pad rows x 128 B =
+//           4 chunks of the stacked planes, SWIZZLE_128B)
+//   warps 3-18: converters (four groups of 4 warps, chunk g -> group g % 4):
+//           fp32 slice from shared memory -> FMUL + F2I + IADD per element ->
+//           byte permutes into the digit planes d1 | d2 | d3 | d4 ->
+//           tcgen05.st into a staging slot (thread = MMA row = TMEM lane)
+//   warps 19-22: epilogue: drains a unit's four class accumulators once
+//           (units of <= kMaxUnitChunks chunks keep int32 exact), converts to
+//           fp64, writes the split-K partial, re-zeroes.
+// TMEM (512 columns): the accumulator set at 0 (class c at c r_pad), staging
+// slots at 256 + 32 s, s < 8 (d1 | d2 | d3 | d4, 8 columns each); chunk g
+// uses slot g % 8, chunk pair h the slot pair h % 4.  Work units hold a
+// multiple of 4 chunks (zero chunks pad a ragged K: TMA zero-fills M beyond
+// the matrix, the factor digits are zero there).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>

@@ -1,10 +1,10 @@
 // ix_gemm.hpp -- the two M-streaming products of the fp32-storage path on the
 // tcgen05 integer tensor cores (ix_gemm.cu):
 //   A (m x r, fp64) = M (m x n) W^T      and      C (r x n, fp64) = V^T M
-// with every fp32 operand held as a power-of-two-scaled 23-bit fixed-point
-// value split into three signed 8-bit digits; digit products accumulate in
-// int32 TMEM exactly, so the only error is the (unbiased) rounding of each
-// operand to its fixed-point grid.
+// with M's fp32 entries and the fp64 factors on per-row 31-bit fixed-point
+// grids, split into four signed 8-bit digits; the digit products accumulate
+// in int32 TMEM exactly, so the only error is the (unbiased) rounding of
+// each operand to its grid (exact for M entries within 2^7 of the row max).
 #pragma once
 #include <atomic>
 #include <cstddef>

@@ -141,6 +141,22 @@ void run_cycle(Engine& e, size_t levels, size_t r, Kind kind, Cycle cycle, int b
   e.flush(&out.samples, &out.nnls_counts, &out.degenerate);
 }
 
+double run_phase(Engine& e, size_t l, Kind kind, int budget_mode, double amount, double step_flops,
+                 double unit_flops, size_t trace_every, double* work_consumed, RunTrace& out) {
+  if (l >= e.built_levels()) throw std::invalid_argument("run_phase: level not built");
+  if (!(unit_flops > 0.0)) throw std::invalid_argument("run_phase: unit_flops must be positive");
+  Runner run{&e, {}, kind, budget_mode, e.rank_r(), trace_every, out};
+  for (size_t k = 0; k < e.built_levels(); ++k) run.ms.push_back(e.m(k));
+  run.n_total = e.n_total();
+  run.unit_flops = unit_flops;
+  run.work_consumed = work_consumed ? *work_consumed : 0.0;
+  e.mark_run_start();
+  const double left = run.solver_phase(l, amount, step_flops);
+  e.flush(&out.samples, &out.nnls_counts, &out.degenerate);
+  if (work_consumed) *work_consumed = run.work_consumed;
+  return left;
+}
+
 void plan_cycle(const std::vector<size_t>& level_rows, size_t n_total, size_t levels, size_t r, Kind kind,
                 Cycle cycle, double amount, size_t trace_every, RunTrace& out) {
   if (levels < 1 || levels > level_rows.size()) throw std::invalid_argument("run_cycle: bad level count");

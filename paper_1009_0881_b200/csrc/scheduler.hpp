@@ -32,6 +32,15 @@ double iteration_cost(size_t m, size_t n, size_t r, Kind kind);
 void run_cycle(Engine& e, size_t levels, size_t r, Kind kind, Cycle cycle, int budget_mode, double amount,
                size_t trace_every, RunTrace& out);
 
+// run_solver_phase (solvers.cpp:300-341) on the engine's resident level l
+// (M_l, V_l and W on the device): `amount` work units (budget_mode 0,
+// charging step_flops / unit_flops per step) or seconds (1), samples at
+// start, every trace_every steps and end, stamped with *work_consumed (the
+// run's cumulative work; advanced in place).  Returns the unconsumed amount.
+// Sample times are relative to the phase start.
+double run_phase(Engine& e, size_t l, Kind kind, int budget_mode, double amount, double step_flops,
+                 double unit_flops, size_t trace_every, double* work_consumed, RunTrace& out);
+
 // Dry run of the same control flow (work-unit budgets): the phase allocations,
 // steps per phase and sample work/level stamps, without device work.
 void plan_cycle(const std::vector<size_t>& level_rows, size_t n_total, size_t levels, size_t r, Kind kind,

@@ -31,3 +31,19 @@ def test_reference_acceptance_through_b200(gpu, tmp_path):
     assert "all criteria passed" in out, out[-4000:]
     assert MEANS in out, out[-4000:]
     assert "[FAIL]" not in out
+
+
+def test_reference_cycle_runner_over_resident_phases(gpu, tmp_path):
+    """The reference's own multilevel.cpp (CycleRunner, multilevel.cpp:14-89)
+    compiled unchanged, calling the shim's run_solver_phase: every phase runs
+    device-resident through mlnmf_session_run_phase (one upload of the
+    level's M per phase, not per step).  Same criteria and means."""
+    binp = os.path.join(REPO, "oracle", "_ref", "acceptance_b200_phases")
+    if not os.path.exists(binp):
+        pytest.skip("oracle/_ref/acceptance_b200_phases not built (needs the reference sources at build time)")
+    p = subprocess.run([binp], cwd=tmp_path, capture_output=True, text=True, timeout=1200)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-4000:]
+    assert "all criteria passed" in out, out[-4000:]
+    assert MEANS in out, out[-4000:]
+    assert "[FAIL]" not in out
