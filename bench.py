@@ -302,6 +302,7 @@ def run_b200(args):
 
     ttt = time_to_target(P, local, gemm) if (args.ttt and world == 1) else None
     small = small_configs(P, local, args.cpu_baseline) if (args.small and world == 1) else None
+    ttts = ttt_small(P, local, args.cpu_baseline) if (args.ttt and args.small and world == 1) else None
 
     if rank != 0:
         return
@@ -333,6 +334,8 @@ def run_b200(args):
         line["time_to_target"] = ttt
     if small:
         line["small_configs"] = small
+    if ttts:
+        line["time_to_target_small"] = ttts
     if args.cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
@@ -413,6 +416,81 @@ def small_configs(P, local, with_cpu):
                 e["cpu_cores"] = os.cpu_count() or 1
                 e["speedup"] = e["cpu_ref_ms_per_step"] / e["gpu_ms_per_step"]
             out[f"config{cfg}_{kind}"] = e
+    return out
+
+
+def ttt_small(P, local, with_cpu):
+    """BASELINE.md section 2 for configs 0-3 at their BASELINE budgets
+    (config 0 work:100, 1 work:500, 2-3 work:100; each config's first solver
+    kind in BASELINE.json): target = the reference's single-level final
+    relative error; for none / NI / VC / FMG the time to the first finest-
+    level sample at or below it, on the reference CPU (oracle/_ref, fp64,
+    OpenMP on all host cores) and on the GPU (fp32 M storage, fp64 factors),
+    both including the pyramid build and random_init (setup = the run's wall
+    time minus its last sample's elapsed time, added to the hit time), plus
+    the GPU trajectory's largest relative deviation from the reference's on
+    the same fp32-rounded M (every sample, trace_every = 1)."""
+    import oracle
+    ref = oracle.Reference() if (with_cpu and oracle.Reference.available()) else None
+    restated = oracle.Restated()
+    out = {}
+    for cfg in (0, 1, 2, 3):
+        c, oc = P.GEN_CONFIGS[cfg], oracle.CONFIGS[cfg]
+        kind, budget = SMALL_KINDS[cfg][0], float(oc["budget"])
+        M32 = oracle.generate_config(cfg, restated=restated).astype(np.float32)
+        M64 = M32.astype(np.float64)
+        norm = float(np.sqrt((M64 * M64).sum()))
+        e = {"shape": f"{c['h']}x{c['w']} x n={c['n']}, r={c['r']}, {c['levels']} levels", "kind": kind,
+             "budget": f"work:{budget:g}"}
+        cpu, gpu = {}, {}
+        if ref is not None:
+            for cyc in ("none", "ni", "vc", "fmg"):
+                L = 1 if cyc == "none" else c["levels"]
+                t0 = time.perf_counter()
+                _, _, tr = ref.run_configuration(M64, c["h"], c["w"], L, kind, cyc, c["r"], 0, budget, 1)
+                wall = time.perf_counter() - t0
+                cpu[cyc] = (tr, wall)
+            target = float(cpu["none"][0].error[-1]) / norm
+        with P.Session(device=local, dtype=P.F32) as s:
+            s.set_data(M32, P.ImageGrid(c["h"], c["w"]))
+            s.run_configuration(c["levels"], kind, "fmg", c["r"], 0, 4.0, 1)  # warm-up (buffers, graphs)
+            for cyc in ("none", "ni", "vc", "fmg"):
+                L = 1 if cyc == "none" else c["levels"]
+                with P.Session(device=local, dtype=P.F32) as s2:  # fresh pyramid: its build is timed
+                    s2.set_data(M32, P.ImageGrid(c["h"], c["w"]))
+                    s2.sync()
+                    t0 = time.perf_counter()
+                    tr = s2.run_configuration(L, kind, cyc, c["r"], 0, budget, 1)
+                    wall = time.perf_counter() - t0
+                gpu[cyc] = (tr, wall)
+        if ref is None:
+            target = float(gpu["none"][0].error[-1]) / norm
+        e["target_rel_error"] = target
+
+        def hit(tr, wall):
+            rel = tr.error / norm
+            k = np.nonzero((tr.level == 1) & (rel <= target * (1 + 1e-9)))[0]
+            setup = wall - float(tr.elapsed_s[-1])
+            return (setup + float(tr.elapsed_s[k[0]])) if len(k) else None, wall
+
+        for cyc in ("none", "ni", "vc", "fmg"):
+            g_t, g_wall = hit(*gpu[cyc])
+            row = {"gpu_time_to_target_s": g_t, "gpu_wall_s": g_wall,
+                   "gpu_final_rel_error": float(gpu[cyc][0].error[-1]) / norm}
+            if ref is not None:
+                c_t, c_wall = hit(*cpu[cyc])
+                tg, tc = gpu[cyc][0], cpu[cyc][0]
+                same = len(tg.error) == len(tc.error) and np.array_equal(tg.level, tc.level)
+                row.update(cpu_time_to_target_s=c_t, cpu_wall_s=c_wall,
+                           cpu_final_rel_error=float(tc.error[-1]) / norm,
+                           same_schedule=bool(same and np.allclose(tg.work_units, tc.work)),
+                           max_rel_dev=float(np.max(np.abs(tg.error - tc.error) / tc.error)) if same else None)
+                if c_t and g_t:
+                    row["speedup_time_to_target"] = c_t / g_t
+            e[cyc] = row
+        if ref is not None:
+            e["cpu_cores"] = os.cpu_count() or 1
+        out[f"config{cfg}_{kind}"] = e
     return out
 
 

@@ -164,6 +164,16 @@ double mlnmf_iteration_cost(size_t m, size_t n, size_t r, int kind);
  * Sessions: device-resident data, fp32 storage, column sharding over ranks.
  * ------------------------------------------------------------------------- */
 int mlnmf_session_create(const mlnmf_options* o, mlnmf_session** out);
+/* A rank of a world > 1 problem whose collectives go through the caller
+ * instead of NCCL: fn(ctx, buf, count, op) receives this rank's `count`
+ * doubles in host memory and must leave there the element-wise sum (op 0) or
+ * max (op 1) over all ranks; every rank issues the same sequence of calls.
+ * Used to run several ranks (sessions) in one process -- e.g. on one GPU for
+ * the multi-rank parity tests -- with no device-side waits between them.
+ * options->nccl_id must be NULL. */
+typedef int (*mlnmf_host_allreduce_fn)(void* ctx, double* buf, size_t count, int op);
+int mlnmf_session_create_host_comm(const mlnmf_options* o, mlnmf_host_allreduce_fn fn, void* ctx,
+                                   mlnmf_session** out);
 void mlnmf_session_destroy(mlnmf_session* s);
 /* M_local: m x n_local row-major host buffer (host_dtype MLNMF_F32/F64),
  * columns [col0, col0 + n_local) of an n_total-column problem.  Validated like

@@ -205,6 +205,8 @@ _proto("mlnmf_smoothness", C.c_int, _dp, _sz, _sz, _sz, _sz, _dp)
 _proto("mlnmf_initialization_bound", C.c_int, _dp, _sz, _sz, _sz, _sz, _dp, _dp, _sz, _dp, _dp)
 _proto("mlnmf_session_create", C.c_int, C.POINTER(_Options), C.POINTER(_vp))
 _proto("mlnmf_session_destroy", None, _vp)
+_HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, _vp, C.POINTER(C.c_double), _sz, C.c_int)
+_proto("mlnmf_session_create_host_comm", C.c_int, C.POINTER(_Options), _HOST_ALLREDUCE, _vp, C.POINTER(_vp))
 _proto("mlnmf_session_set_data", C.c_int, _vp, _vp, C.c_int, _sz, _sz, _sz, _sz, _sz, _sz)
 _proto("mlnmf_session_generate", C.c_int, _vp, C.POINTER(_GenParams), _sz, _sz, _sz)
 _proto("mlnmf_session_run_configuration", C.c_int, _vp, _sz, C.c_int, C.c_int, _sz, C.c_uint64, C.c_int,
@@ -682,16 +684,56 @@ def shard_columns(n_total: int, world: int, rank: int):
     return col0, n_local
 
 
+class HostGroup:
+    """In-process collective for `world` sessions (ranks), each driven from
+    its own thread (mlnmf_session_create_host_comm): every allreduce deposits
+    the rank's buffer, waits for all ranks, and leaves the element-wise sum
+    (ranks added in rank order: deterministic, identical on every rank) or
+    max.  It lets the real sharded engine run world > 1 in one process, on
+    one GPU, with no device-side waits between ranks."""
+
+    def __init__(self, world: int, timeout: float = 300.0):
+        import threading
+        self.world = world
+        self._bufs = [None] * world
+        self._barrier = threading.Barrier(world, timeout=timeout)
+
+    def allreduce(self, rank: int, buf: np.ndarray, op: int):
+        self._bufs[rank] = buf.copy()
+        self._barrier.wait()
+        out = self._bufs[0].copy()
+        for b in self._bufs[1:]:
+            out = out + b if op == 0 else np.maximum(out, b)
+        self._barrier.wait()  # every rank has read the deposits before the next exchange
+        buf[:] = out
+
+    def abort(self):
+        self._barrier.abort()
+
+
 class Session:
-    """A device-resident solver instance (one per GPU / rank)."""
+    """A device-resident solver instance (one per GPU / rank).  world > 1
+    needs an NCCL id (one process per GPU) or a HostGroup (ranks as threads
+    of one process)."""
 
     def __init__(self, device=0, dtype=F64, exact=False, gemm_path=GEMM_AUTO, error_mode=ERROR_AUTO,
-                 world=1, rank=0, nccl_id: Optional[bytes] = None):
+                 world=1, rank=0, nccl_id: Optional[bytes] = None, host_group: Optional[HostGroup] = None):
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         o = _Options(device, dtype, int(bool(exact)), gemm_path, error_mode, world, rank,
                      C.cast(self._idbuf, _vp) if self._idbuf is not None else None)
         h = _vp()
-        _check(_lib.mlnmf_session_create(C.byref(o), C.byref(h)))
+        if host_group is not None:
+            def _cb(ctx, buf, count, op, _g=host_group, _r=rank):
+                try:
+                    _g.allreduce(_r, np.ctypeslib.as_array(buf, shape=(count,)), op)
+                    return 0
+                except Exception:
+                    _g.abort()  # release the other ranks (their exchange fails too)
+                    return 1
+            self._cb = _HOST_ALLREDUCE(_cb)
+            _check(_lib.mlnmf_session_create_host_comm(C.byref(o), self._cb, None, C.byref(h)))
+        else:
+            _check(_lib.mlnmf_session_create(C.byref(o), C.byref(h)))
         self._h = h.value
         self.dtype = dtype
         self.world, self.rank = world, rank

@@ -362,6 +362,26 @@ int mlnmf_session_create(const mlnmf_options* o, mlnmf_session** out) {
   });
 }
 
+int mlnmf_session_create_host_comm(const mlnmf_options* o, mlnmf_host_allreduce_fn fn, void* ctx,
+                                   mlnmf_session** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (!fn) throw std::invalid_argument("host allreduce: null function");
+    if (o && o->nccl_id) throw std::invalid_argument("host allreduce: an NCCL id was given too");
+    Options x = to_opts(o);
+    x.host_allreduce = fn;
+    x.host_allreduce_ctx = ctx;
+    auto* s = new mlnmf_session;
+    try {
+      s->e = std::make_unique<Engine>(x);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
 void mlnmf_session_destroy(mlnmf_session* s) { delete s; }
 
 int mlnmf_session_set_data(mlnmf_session* s, const void* M, int host_dtype, size_t m, size_t n_local, size_t n_total,

@@ -102,6 +102,7 @@ struct Engine::Impl {
   DevBuf tstart;  // run-start globaltimer
   DevBuf stage;   // host-transfer staging
   size_t samp_cap = 0, samp_used = 0, cnt_cap = 0, cnt_used = 0;
+  std::vector<size_t> cnt_steps;  // m_l of every ANLS step in the count ring (m_l V rows, then n_loc W columns)
   std::vector<Sample> samp_meta;  // host metadata of enqueued samples
   // validity of cached products w.r.t. current iterates
   bool B_valid = false;   // B == W W^T (allreduced) for the current W
@@ -172,15 +173,32 @@ struct Engine::Impl {
   // collectives run whenever a communicator exists: world > 1, or a 1-rank
   // communicator requested by passing an NCCL id with world = 1 (exercises the
   // NCCL path on one GPU)
+  // ranks exchange through NCCL, or (no communicator, world > 1) through the
+  // host hook: stream sync, device -> host, hook, host -> device
+  bool multi() const { return comm || e->opt_.host_allreduce; }
+  std::vector<double> hostx;
+  void host_exchange(double* p, size_t count, int op) {
+    hostx.resize(count);
+    CK(cudaMemcpyAsync(hostx.data(), p, count * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (e->opt_.host_allreduce(e->opt_.host_allreduce_ctx, hostx.data(), count, op) != 0)
+      throw std::runtime_error("host allreduce failed");
+    CK(cudaMemcpyAsync(p, hostx.data(), count * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // hostx is reused by the next exchange
+  }
   void allreduce_sum(double* p, size_t count) {
-    if (!comm) return;
-    auto& api = NcclApi::get();
-    nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclSum, comm, s), "allreduce");
+    if (comm) {
+      nccl_check(NcclApi::get().AllReduce(p, p, count, ncclFloat64, ncclSum, comm, s), "allreduce");
+    } else if (e->opt_.host_allreduce) {
+      host_exchange(p, count, 0);
+    }
   }
   void allreduce_max(double* p, size_t count) {
-    if (!comm) return;
-    auto& api = NcclApi::get();
-    nccl_check(api.AllReduce(p, p, count, ncclFloat64, ncclMax, comm, s), "allreduce max");
+    if (comm) {
+      nccl_check(NcclApi::get().AllReduce(p, p, count, ncclFloat64, ncclMax, comm, s), "allreduce max");
+    } else if (e->opt_.host_allreduce) {
+      host_exchange(p, count, 1);
+    }
   }
 
   // ---------------- GEMMs ----------------
@@ -280,7 +298,7 @@ struct Engine::Impl {
       const auto key = std::make_pair(L.m, e->r_);
       if (tc_ok.count(key)) continue;
       double veto = tc->wants(L.m, e->n_loc_, e->r_) ? 0.0 : 1.0;
-      if (comm) {
+      if (multi()) {
         double* d = scal.as<double>() + 9;
         CK(cudaMemcpyAsync(d, &veto, 8, cudaMemcpyHostToDevice, s));
         allreduce_max(d, 1);
@@ -383,7 +401,7 @@ struct Engine::Impl {
     const bool needB = !B_valid;
     if (needB) timed(kPhB, [&] { gram_W<T>(); });
     timed(kPhA, [&] { product_mwt<T>(l); });
-    if (comm) {
+    if (multi()) {
       std::pair<cudaEvent_t, cudaEvent_t> evp{};
       if (e->profiling_) {
         evp = {ev(), ev()};
@@ -422,6 +440,7 @@ struct Engine::Impl {
       } else if (kind == kMu) {
         launch(k_mu_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
       } else {
+        cnt_steps.push_back(L.m);
         nnls((const double*)B(), L.m, (const double*)A(), r, 1, V, r, 1);
       }
     });
@@ -483,6 +502,29 @@ struct Engine::Impl {
     else
       launch(k_nnls_batch<double, false>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi,
              xe, cnt, flags.as<int>() + 1);
+  }
+
+  // After an ANLS step: the reference throws at the failing step
+  // (solvers.cpp:269,294); the flag is read here (one sync per ANLS step)
+  // and max-combined over ranks, so every rank throws at the same step.
+  void check_nnls() {
+    int f = 0;
+    CK(cudaMemcpyAsync(&f, flags.as<int>() + 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (multi()) {
+      double fd = (double)f;
+      double* d = scal.as<double>() + 10;
+      CK(cudaMemcpyAsync(d, &fd, 8, cudaMemcpyHostToDevice, s));
+      allreduce_max(d, 1);
+      CK(cudaMemcpyAsync(&fd, d, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      f = (int)fd;
+    }
+    if (f) {
+      CK(cudaMemsetAsync(flags.as<int>() + 1, 0, 4, s));
+      throw NnlsCapExceeded(f & 1 ? "anls_step: NNLS exchange cap exceeded"
+                                  : "anls_step: NNLS failed (singular passive subsystem)");
+    }
   }
 
   int* reserve_counts(size_t k) {
@@ -672,8 +714,9 @@ Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
   impl_->scal.ensure(16 * 8);
   impl_->tstart.ensure(8);
   impl_->tc = make_tc_gemm(o.dtype == 0 && o.gemm != 1, o.gemm == 2);
-  if (o.world > 1 || o.has_nccl_id) {
-    if (!o.has_nccl_id) throw std::invalid_argument("world > 1 needs an NCCL unique id");
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw std::invalid_argument("bad world / rank");
+  if (o.has_nccl_id || (o.world > 1 && !o.host_allreduce)) {
+    if (!o.has_nccl_id) throw std::invalid_argument("world > 1 needs an NCCL unique id (or a host allreduce)");
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_id, sizeof(id));
     nccl_check(NcclApi::get().CommInitRank(&impl_->comm, o.world, id, o.rank), "CommInitRank");
@@ -1057,7 +1100,7 @@ void Engine::step(size_t l, Kind kind) {
   // fixed sequence of ~10 small launches, launch-bound on the L2-resident
   // configs.  (ANLS appends NNLS counts at moving offsets; multi-rank steps
   // hold NCCL calls; profiling records events: those run eagerly.)
-  const bool graphable = im.graphs_on && kind != kAnls && !im.comm && !profiling_;
+  const bool graphable = im.graphs_on && kind != kAnls && !im.multi() && !profiling_;
   if (graphable) {
     Impl::StepGraph& g = im.graphs[l * 4 + (size_t)kind];
     if (!g.exec || g.epoch != g_dev_epoch.load()) {
@@ -1106,6 +1149,7 @@ void Engine::step(size_t l, Kind kind) {
   }
   if (opt_.dtype == 0) impl_->step_t<float>(l, kind);
   else impl_->step_t<double>(l, kind);
+  if (kind == kAnls) impl_->check_nnls();
 }
 
 void Engine::sample(size_t l, double work_units) {
@@ -1122,6 +1166,7 @@ void Engine::mark_run_start() {
   impl_->samp_used = 0;
   impl_->samp_meta.clear();
   impl_->cnt_used = 0;
+  impl_->cnt_steps.clear();
 }
 
 double Engine::host_elapsed_s() const {
@@ -1150,11 +1195,39 @@ void Engine::flush(std::vector<Sample>* samples, std::vector<int>* counts, int* 
       samples->push_back(smp);
     }
   }
-  if (counts) counts->insert(counts->end(), cn.begin(), cn.end());
+  if (counts && impl_->multi() && !impl_->cnt_steps.empty()) {
+    // the reference's layout, m_l V-row counts then all n W-column counts
+    // per ANLS step (solvers.cpp:269,296): V rows are replicated, each rank
+    // holds its own columns -> one sum-exchange of zero-padded rows
+    const size_t S = impl_->cnt_steps.size();
+    std::vector<double> wc(S * n_total_, 0.0);
+    size_t off = 0;
+    for (size_t k = 0; k < S; ++k) {
+      off += impl_->cnt_steps[k];
+      for (size_t j = 0; j < n_loc_; ++j) wc[k * n_total_ + col0_ + j] = (double)cn[off + j];
+      off += n_loc_;
+    }
+    DevBuf g;
+    g.ensure(wc.size() * 8);
+    CK(cudaMemcpyAsync(g.p, wc.data(), wc.size() * 8, cudaMemcpyHostToDevice, s));
+    impl_->allreduce_sum(g.as<double>(), wc.size());
+    CK(cudaMemcpyAsync(wc.data(), g.p, wc.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    g.release();
+    off = 0;
+    for (size_t k = 0; k < S; ++k) {
+      counts->insert(counts->end(), cn.begin() + off, cn.begin() + off + impl_->cnt_steps[k]);
+      off += impl_->cnt_steps[k] + n_loc_;
+      for (size_t j = 0; j < n_total_; ++j) counts->push_back((int)wc[k * n_total_ + j]);
+    }
+  } else if (counts) {
+    counts->insert(counts->end(), cn.begin(), cn.end());
+  }
   if (degenerate) *degenerate += fl[0];
   impl_->samp_used = 0;
   impl_->samp_meta.clear();
   impl_->cnt_used = 0;
+  impl_->cnt_steps.clear();
   CK(cudaMemsetAsync(impl_->flags.p, 0, 8, s));
 }
 

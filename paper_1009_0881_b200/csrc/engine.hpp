@@ -27,6 +27,13 @@ struct DataError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// Host-side collective for ranks that share no NCCL communicator (several
+// sessions in one process, e.g. the multi-rank tests on one GPU): called with
+// this rank's `count` doubles in host memory, it must leave there the
+// element-wise sum (op 0) or max (op 1) over all ranks, every rank calling in
+// the same order.  Returns 0 on success.
+typedef int (*HostAllreduceFn)(void* ctx, double* buf, size_t count, int op);
+
 struct Options {
   int device = 0;
   int dtype = 1;       // storage of M, V, W: 0 = fp32, 1 = fp64
@@ -36,6 +43,8 @@ struct Options {
   int world = 1, rank = 0;
   bool has_nccl_id = false;
   unsigned char nccl_id[128] = {0};
+  HostAllreduceFn host_allreduce = nullptr;  // world > 1 without NCCL (see above)
+  void* host_allreduce_ctx = nullptr;
 };
 
 struct GenParams {
