@@ -1173,6 +1173,21 @@ double Engine::host_elapsed_s() const {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - impl_->host_t0).count();
 }
 
+double Engine::agreed_max(double v) {
+  if (!impl_->multi()) return v;
+  double* d = impl_->scal.as<double>() + 11;
+  CK(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, impl_->s));
+  impl_->allreduce_max(d, 1);
+  CK(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+  return v;
+}
+
+double Engine::agreed_elapsed_s() {
+  sync();
+  return agreed_max(host_elapsed_s());
+}
+
 void Engine::flush(std::vector<Sample>* samples, std::vector<int>* counts, int* degenerate) {
   cudaStream_t s = impl_->s;
   std::vector<SampleRec> recs(impl_->samp_used);

@@ -124,6 +124,10 @@ class Engine {
   void flush(std::vector<Sample>* samples, std::vector<int>* counts, int* degenerate);  // sync + collect
   void sync();
   double host_elapsed_s() const;  // host clock since mark_run_start (time-budget mode)
+  // wall-clock budgets: sync the stream and return host_elapsed_s(), the
+  // maximum over ranks (every rank then takes the same decisions)
+  double agreed_elapsed_s();
+  double agreed_max(double v);  // max of a host value over ranks (identity on one rank)
 
   // ---- standalone kernels for the step-level C-ABI ----
   double frobenius_error(size_t l);  // sync

@@ -2,6 +2,7 @@
 #include "scheduler.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <stdexcept>
 
 namespace mlb {
@@ -37,21 +38,12 @@ struct Runner {
     const double charge = sflops / unit_flops;
     const double eps = 1e-12 * std::max(1.0, amount);
     double phase_start = 0.0;
-    if (mode == 1) {
-      e->sync();
-      phase_start = e->host_elapsed_s();
-    }
+    if (mode == 1) phase_start = e->agreed_elapsed_s();
     if (e) e->sample(l, work_consumed);
     else out.samples.push_back({0.0, work_consumed, (int)l + 1, 0.0});
     double consumed = 0.0;
     size_t steps = 0;
-    while (true) {
-      if (mode == 0) {
-        if (consumed + charge > amount + eps) break;
-      } else {
-        e->sync();
-        if (e->host_elapsed_s() - phase_start >= amount) break;
-      }
+    auto one_step = [&]() {
       if (e) e->step(l, kind);
       consumed += charge;
       work_consumed += charge;
@@ -60,14 +52,37 @@ struct Runner {
         if (e) e->sample(l, work_consumed);
         else out.samples.push_back({0.0, work_consumed, (int)l + 1, 0.0});
       }
+    };
+    if (mode == 0) {
+      // work units: the step count follows from the budget arithmetic alone,
+      // so every step is enqueued without a host sync
+      while (consumed + charge <= amount + eps) one_step();
+    } else {
+      // Wall clock.  The reference checks elapsed >= amount before every
+      // step (solvers.cpp:318-320).  Here the device runs ahead in batches:
+      // after a sync (elapsed agreed over ranks: max), with R seconds left and
+      // the last batch's per-step time tau, k = floor(R / (2 tau)) steps are
+      // enqueued without a sync -- they finish by half the remaining time --
+      // so batches shrink geometrically towards the deadline and the last
+      // steps go one at a time: the same steps start as under a per-step
+      // check, with O(log(budget / step)) syncs instead of one per step.
+      double tau = -1.0;
+      double now = e->agreed_elapsed_s() - phase_start;
+      while (now < amount) {
+        size_t k = 1;
+        if (tau > 0.0) k = (size_t)std::max(1.0, std::min(4096.0, std::floor((amount - now) / (2.0 * tau))));
+        for (size_t i = 0; i < k; ++i) one_step();
+        const double after = e->agreed_elapsed_s() - phase_start;
+        tau = e->agreed_max((after - now) / (double)k);
+        now = after;
+      }
     }
     if (e) e->sample(l, work_consumed);
     else out.samples.push_back({0.0, work_consumed, (int)l + 1, 0.0});
     out.phase_level.push_back((int)l + 1);
     out.phase_steps.push_back((long)steps);
     if (mode == 0) return amount - consumed;
-    e->sync();
-    return std::max(0.0, amount - (e->host_elapsed_s() - phase_start));
+    return std::max(0.0, amount - (e->agreed_elapsed_s() - phase_start));
   }
 
   // CycleRunner::phase (multilevel.cpp:28-34)
@@ -131,8 +146,6 @@ static void drive(Runner& run, size_t levels, Cycle cycle, double amount) {
 void run_cycle(Engine& e, size_t levels, size_t r, Kind kind, Cycle cycle, int budget_mode, double amount,
                size_t trace_every, RunTrace& out) {
   if (levels < 1 || levels > e.built_levels()) throw std::invalid_argument("run_cycle: bad level count");
-  if (budget_mode == 1 && e.options().world > 1)
-    throw std::invalid_argument("wall-clock budgets are single-rank only (ranks must agree on step counts)");
   Runner run{&e, {}, kind, budget_mode, r, trace_every, out};
   for (size_t l = 0; l < e.built_levels(); ++l) run.ms.push_back(e.m(l));
   run.n_total = e.n_total();

@@ -121,3 +121,19 @@ def test_world2_tensor_path(P, gpu):
     for tr, tc in run_ranks(P, 2, n, body, dtype=P.F32, gemm_path=P.GEMM_TCGEN05):
         assert tc
         assert np.max(np.abs(tr.error - one.error) / one.error) < 1e-7
+
+
+def test_world2_wall_clock_budget_agreed(P, gpu, restated):
+    """Wall-clock budgets at world = 2: every time check uses the elapsed
+    time agreed over the ranks (max), so both ranks realise the same step
+    counts and their traces agree sample for sample."""
+    n = 400
+    M = oracle.generate_config(0, n=n, restated=restated)
+
+    def body(s, rk, col0, nl):
+        s.set_data(M[:, col0:col0 + nl], P.ImageGrid(32, 32), n_total=n, col0=col0)
+        return s.run_configuration(3, "hals", "fmg", 12, 0, P.Budget(P.BudgetMode.kWallClockSeconds, 0.2), 1)
+
+    a, b = run_ranks(P, 2, n, body, dtype=P.F64)
+    assert a.phase_steps.tolist() == b.phase_steps.tolist() and sum(a.phase_steps) > 10
+    assert np.array_equal(a.level, b.level) and np.array_equal(a.error, b.error)

@@ -19,8 +19,9 @@ pytestmark = pytest.mark.gpu
 class PyCycleRunner:
     """multilevel.cpp:14-62 over a device session's resident levels."""
 
-    def __init__(self, P, s, kind, r, trace_every):
+    def __init__(self, P, s, kind, r, trace_every, fixed_steps=None):
         self.P, self.s, self.kind, self.trace_every = P, s, kind, trace_every
+        self.fixed = iter(fixed_steps) if fixed_steps is not None else None
         n = s.n_local
         self.rows = [s.level_grid(l).pixels() for l in range(s.num_levels)]
         self.unit = P.iteration_cost(self.rows[0], n, r, kind)
@@ -30,7 +31,10 @@ class PyCycleRunner:
 
     def phase(self, cur, nominal, carry):  # CycleRunner::phase (multilevel.cpp:28-34)
         self.alloc.append((cur + 1, nominal))
-        left, self.work, tr = self.s.run_phase(cur, self.kind, nominal + carry, self.flops[cur], self.unit,
+        amount = nominal + carry
+        if self.fixed is not None:  # replay: exactly the given number of steps
+            amount = next(self.fixed) * self.flops[cur] / self.unit
+        left, self.work, tr = self.s.run_phase(cur, self.kind, amount, self.flops[cur], self.unit,
                                                self.trace_every, self.work)
         self.samples.append(tr)
         self.phases.append((cur + 1, int(tr.phase_steps.sum())))
@@ -112,3 +116,46 @@ def test_run_phase_against_oracle_and_errors(P, gpu, restated):
         left, work, tr = s.run_phase(0, "hals", 12.0, unit, unit, 2)
     assert left == pytest.approx(0.0) and work == pytest.approx(12.0)
     assert np.array_equal(tr.error, to.error) and np.array_equal(tr.work_units, to.work)
+
+
+@pytest.mark.parametrize("cycle", ["none", "vc", "fmg"])
+def test_wall_clock_budget_structure_and_replay(P, gpu, restated, cycle):
+    """Wall-clock budgets (Budget::kWallClockSeconds, solvers.cpp:318-320,340)
+    run as batched device steps with O(log) host time checks
+    (scheduler.cpp solver_phase).  For the realised step counts:
+      * the allocations equal the oracle's (nominal T/4 - 3T/4 splits);
+      * the sample structure (levels, work-unit stamps, 2 + steps/trace_every
+        per phase) follows from the step counts;
+      * the trajectory equals a deterministic replay of those step counts
+        through the resident phases (fp64, exact: bit for bit)."""
+    M = oracle.generate_config(0, n=300, restated=restated)
+    L = 1 if cycle == "none" else 3
+    T, te = 0.25, 2
+    with P.Session(dtype=P.F64, exact=True) as s:
+        s.set_data(M, P.ImageGrid(32, 32))
+        tr = s.run_configuration(L, "hals", cycle, 16, 0, P.Budget(P.BudgetMode.kWallClockSeconds, T), te)
+    _, _, to = restated.run_configuration(M, 32, 32, L, "hals", cycle, 16, 0, 0.05, te, mode=1)
+    assert np.array_equal(tr.alloc_level, to.alloc_level)
+    assert np.allclose(tr.alloc_amount / T, to.alloc_amount / 0.05, rtol=1e-12, atol=0)
+    steps = tr.phase_steps.tolist()
+    assert sum(steps) > 20 and tr.elapsed_s[-1] >= 0.9 * T
+    assert len(tr.error) == sum(2 + k // te for k in steps)
+    unit = P.iteration_cost(1024, 300, 16, "hals")
+    flops = {l + 1: P.iteration_cost(m, 300, 16, "hals") for l, m in enumerate((1024, 256, 64))}
+    w, k_ = [], 0.0
+    for lv, n_ in zip(tr.phase_level.tolist(), steps):
+        w.append(k_)
+        for i in range(1, n_ + 1):
+            if i % te == 0:
+                w.append(k_ + i * flops[lv] / unit)
+        k_ += n_ * flops[lv] / unit
+        w.append(k_)
+    assert np.allclose(tr.work_units, w, rtol=1e-12, atol=0)
+    with P.Session(dtype=P.F64, exact=True) as s:
+        s.set_data(M, P.ImageGrid(32, 32))
+        s.build_levels(L)
+        s.init_random(16, 0)
+        run = PyCycleRunner(P, s, "hals", 16, te, fixed_steps=steps)
+        {"none": run.nested, "vc": run.vcycle, "fmg": run.fmg}[cycle](0, L, T, 0.0)
+    err = np.concatenate([t.error for t in run.samples])
+    assert np.array_equal(err, tr.error)
