@@ -46,13 +46,13 @@ def env_int(k, d):
         return d
 
 
-TRAFFIC_SRC = "profiles/r01d_traffic_config4.json (ncu dram__bytes_read+write per launch, 1 GPU)"
+TRAFFIC_SRC = "profiles/r02_traffic_config4.json (ncu dram__bytes_read+write per launch, 1 GPU)"
 
 
 def traffic_for(kernel, world):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of this
     workload (profiles/); None if absent or not the 1-GPU configuration."""
-    p = os.path.join(REPO, "profiles", "r01d_traffic_config4.json")
+    p = os.path.join(REPO, "profiles", "r02_traffic_config4.json")
     if world != 1 or not os.path.exists(p):
         return None
     with open(p) as f:
@@ -469,9 +469,10 @@ def ttt_small(P, local, with_cpu):
 
         def hit(tr, wall):
             rel = tr.error / norm
+            el = tr.elapsed_s if hasattr(tr, "elapsed_s") else tr.elapsed  # product / oracle trace
             k = np.nonzero((tr.level == 1) & (rel <= target * (1 + 1e-9)))[0]
-            setup = wall - float(tr.elapsed_s[-1])
-            return (setup + float(tr.elapsed_s[k[0]])) if len(k) else None, wall
+            setup = wall - float(el[-1])
+            return (setup + float(el[k[0]])) if len(k) else None, wall
 
         for cyc in ("none", "ni", "vc", "fmg"):
             g_t, g_wall = hit(*gpu[cyc])

@@ -38,25 +38,16 @@ namespace mlb {
                                __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")");       \
   } while (0)
 
-// Device-allocation epoch: bumped by every (re)allocation of engine or
-// tensor-path buffers.  A captured step graph is valid only for the epoch it
-// was captured in (its kernels hold raw buffer pointers).
-std::atomic<uint64_t> g_dev_epoch{1};
-
 namespace {
 constexpr int kTargetBlocks = 8 * 148;  // split-K target: ~8 blocks per SM (latency-bound K loops)
 
 
 template <typename T>
 cudaError_t dev_malloc(T** p, size_t b) {
-  g_dev_epoch.fetch_add(1);
   return cudaMalloc(reinterpret_cast<void**>(p), b);
 }
 void dev_free(void* p) {
-  if (p) {
-    g_dev_epoch.fetch_add(1);
-    cudaFree(p);
-  }
+  if (p) cudaFree(p);
 }
 constexpr size_t kSmemMax = 227 * 1024;
 
@@ -119,11 +110,30 @@ struct Engine::Impl {
   // captured steady-state steps (HALS / MU, single rank): key level * 4 + kind
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
-    uint64_t epoch = 0;
+    uint64_t epoch = 0;  // graph_sig() at capture
     long nlaunch = 0;
     bool warm = false;
   };
   std::map<size_t, StepGraph> graphs;
+  // A captured step graph holds raw buffer pointers and the shapes of its
+  // launches: it is valid while the buffers it may touch are the same
+  // allocations and the problem has the same shape.  The signature hashes
+  // both (this engine's only -- other sessions' allocations never invalidate
+  // its graphs; a freed-and-reallocated buffer at the same address with a
+  // new shape does, through the shape terms).
+  uint64_t graph_sig() const {
+    uint64_t h = 1469598103934665603ull;
+    auto mixv = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    auto mix = [&](const void* p) { mixv((uint64_t)(uintptr_t)p); };
+    for (const DevBuf* b : {&AB, &Cb, &Db, &part, &red, &scal, &W, &flags}) mix(b->p);
+    mixv(e->n_loc_), mixv(e->n_total_), mixv(e->col0_), mixv(e->r_), mixv(e->lv_.size());
+    for (const auto& L : e->lv_) {
+      mixv(L.m), mixv(L.h), mixv(L.w);
+      mix(L.M), mix(L.V), mix(L.mstat), mix(L.Rp), mix(L.Ri), mix(L.Rw), mix(L.Pp), mix(L.Pi), mix(L.Pw);
+    }
+    if (tc) mix(reinterpret_cast<const void*>(tc->signature()));
+    return h;
+  }
   bool graphs_on = std::getenv("MLNMF_NO_GRAPHS") == nullptr;
 
   explicit Impl(Engine* eng) : e(eng) {}
@@ -1103,7 +1113,7 @@ void Engine::step(size_t l, Kind kind) {
   const bool graphable = im.graphs_on && kind != kAnls && !im.multi() && !profiling_;
   if (graphable) {
     Impl::StepGraph& g = im.graphs[l * 4 + (size_t)kind];
-    if (!g.exec || g.epoch != g_dev_epoch.load()) {
+    if (!g.exec || g.epoch != im.graph_sig()) {
       if (!g.warm) {  // one eager step first: buffers reach their steady-state sizes
         g.warm = true;
         im.B_valid = false;
@@ -1112,7 +1122,7 @@ void Engine::step(size_t l, Kind kind) {
         return;
       }
       if (g.exec) cudaGraphExecDestroy(g.exec), g.exec = nullptr;
-      const uint64_t ep = g_dev_epoch.load();
+      const uint64_t ep = im.graph_sig();
       const long l0 = launches_;
       cudaGraph_t graph = nullptr;
       CK(cudaStreamBeginCapture(im.s, cudaStreamCaptureModeRelaxed));
@@ -1128,7 +1138,7 @@ void Engine::step(size_t l, Kind kind) {
       CK(cudaStreamEndCapture(im.s, &graph));
       g.nlaunch = launches_ - l0;
       launches_ = l0;
-      if (g_dev_epoch.load() != ep) {  // an allocation happened during capture: run eagerly, recapture next time
+      if (im.graph_sig() != ep) {  // a buffer was reallocated during capture: run eagerly, recapture next time
         cudaGraphDestroy(graph);
         g.warm = false;
         im.B_valid = false;

@@ -871,6 +871,11 @@ class IxGemm final : public TcGemm {
     for (void* p : {digits_, part_, fmax_})
       if (p) cudaFree(p);
   }
+  uint64_t signature() const override {
+    uint64_t h = 1469598103934665603ull;
+    for (const void* p : {digits_, part_, fmax_}) h = (h ^ (uint64_t)(uintptr_t)p) * 1099511628211ull;
+    return h;
+  }
   bool supports(size_t m, size_t n, size_t r) const override {
     return r >= 1 && r <= 64 && m % 4 == 0 && n % 4 == 0 && m >= 128 && n >= 128 && m < (1u << 31) &&
            n < (1u << 31);
@@ -995,7 +1000,6 @@ class IxGemm final : public TcGemm {
 
   static void ensure(void** p, size_t* have, size_t need) {
     if (need <= *have) return;
-    g_dev_epoch.fetch_add(1);  // invalidates captured step graphs holding the old pointer
     if (*p) IX_CK(cudaFree(*p));
     *p = nullptr;
     IX_CK(cudaMalloc(p, need));

@@ -13,12 +13,12 @@
 
 namespace mlb {
 
-// device-allocation epoch (engine.cu): bumped on every buffer (re)allocation
-extern std::atomic<uint64_t> g_dev_epoch;
-
 class TcGemm {
  public:
   virtual ~TcGemm() = default;
+  // hash of the work-buffer pointers (engine.cu graph_sig: a captured step
+  // graph is valid while they are unchanged)
+  virtual uint64_t signature() const = 0;
   // shape supported by the kernels (r <= 64, 16-byte aligned rows)
   virtual bool supports(size_t m, size_t n, size_t r) const = 0;
   // policy: use the tensor path for this level (forced, or large enough)

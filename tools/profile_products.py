@@ -4,7 +4,7 @@ column slice (m = 65536, r = 64, n = --n), through the active path.
     python tools/profile_products.py --n 32768 --reps 3 [--gemm tc|simt]
 
 Prints per-product device times (CUDA events) and achieved HBM GB/s.
-Intended to be wrapped by ncu (-k regex:k_tc_product).
+Intended to be wrapped by ncu (-k regex:k_ix_product).
 """
 import argparse
 import os
