@@ -740,7 +740,7 @@ Engine::~Engine() {
     dev_free(L.M);
     dev_free(L.V);
     dev_free(L.mstat);
-    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw), dev_free(L.Rc);
   }
   for (DevBuf* b : {&impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
                     &impl_->samples, &impl_->counts, &impl_->flags, &impl_->tstart, &impl_->stage})
@@ -786,7 +786,7 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   if (h * w != m) throw std::invalid_argument("GridHierarchy: grid does not match matrix rows");
   for (auto& L : lv_) {
     dev_free(L.M), dev_free(L.V), dev_free(L.mstat);
-    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw), dev_free(L.Rc);
   }
   lv_.clear();
   impl_->tc_ok.clear();
@@ -852,7 +852,7 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
   // allocate level 0
   for (auto& L : lv_) {
     dev_free(L.M), dev_free(L.V), dev_free(L.mstat);
-    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw);
+    dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw), dev_free(L.Rc);
   }
   lv_.clear();
   impl_->tc_ok.clear();
@@ -924,21 +924,71 @@ void Engine::ensure_levels(size_t L) {
     };
     up(R, &cur.Rp, &cur.Ri, &cur.Rw);
     up(P, &cur.Pp, &cur.Pi, &cur.Pw);
+    {  // k_restrict_slab's decoded entries: fine row i and column offset dj
+      const size_t hcn = (cur.h + 1) / 2;
+      std::vector<int> code(R.idx.size());
+      for (size_t o = 0; o + 1 < R.rowptr.size(); ++o)
+        for (int e = R.rowptr[o]; e < R.rowptr[o + 1]; ++e) {
+          const long f = R.idx[e], j = f / (long)cur.h, i = f % (long)cur.h, dj = j - 2 * (long)(o / hcn);
+          code[e] = (int)(i * 4 + (dj + 1));
+        }
+      CK(dev_malloc(&cur.Rc, code.size() * 4));
+      CK(cudaMemcpy(cur.Rc, code.data(), code.size() * 4, cudaMemcpyHostToDevice));
+    }
     double pf = 0.0;
     for (double x : P.wt) pf += x * x;
     cur.p_fro = std::sqrt(pf);
     Level nx{(cur.h + 1) / 2, (cur.w + 1) / 2, 0};
     nx.m = nx.h * nx.w;
     CK(dev_malloc(&nx.M, nx.m * n_loc_ * es));
-    const size_t colblocks = ceil_div(n_loc_, 256);
-    if (opt_.dtype == 0)
-      impl_->launch(k_csr_apply<float>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
-                    (const int*)cur.Ri, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), nx.m,
-                    n_loc_, colblocks);
-    else
-      impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
-                    (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M), nx.m,
-                    n_loc_, colblocks);
+    const size_t slab_smem = 3 * cur.h * 64;
+    if (slab_smem <= 200 * 1024) {
+      // column slabs with the fine pixel columns staged once (k_restrict_slab)
+      const unsigned g = (unsigned)ceil_div(n_loc_ * es, 64);
+      const int h = (int)cur.h, w = (int)cur.w, hc = (int)nx.h, wc = (int)nx.w;
+      const bool vec = (n_loc_ * es) % 16 == 0;
+      if (opt_.dtype == 0 && !impl_->exact()) {
+        // 64-byte slabs, 3-slot ring (48 KB: 4 CTAs per SM) measured best of
+        // {128, 64, 32} B x {3, 5 (prefetch)} slots and an L1-only variant
+        // (config-4 pyramid 77 ms with the gather -> 51 ms; r02)
+        if (vec)
+          impl_->launch(k_restrict_slab<float, 4, false, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
+                        w, hc, wc, n_loc_);
+        else
+          impl_->launch(k_restrict_slab<float, 1, false, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
+                        w, hc, wc, n_loc_);
+      } else if (opt_.dtype == 0) {
+        if (vec)
+          impl_->launch(k_restrict_slab<float, 4, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
+                        w, hc, wc, n_loc_);
+        else
+          impl_->launch(k_restrict_slab<float, 1, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
+                        w, hc, wc, n_loc_);
+      } else {
+        if (vec)
+          impl_->launch(k_restrict_slab<double, 2, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
+                        h, w, hc, wc, n_loc_);
+        else
+          impl_->launch(k_restrict_slab<double, 1, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
+                        h, w, hc, wc, n_loc_);
+      }
+    } else {
+      const size_t colblocks = ceil_div(n_loc_, 256);
+      if (opt_.dtype == 0)
+        impl_->launch(k_csr_apply<float>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
+                      (const int*)cur.Ri, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), nx.m,
+                      n_loc_, colblocks);
+      else
+        impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
+                      (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
+                      nx.m, n_loc_, colblocks);
+    }
     if (r_ > 0) CK(dev_malloc(&nx.V, nx.m * r_ * 8));  // factors are fp64
     lv_.push_back(nx);
   }

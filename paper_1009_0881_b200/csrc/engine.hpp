@@ -163,6 +163,7 @@ class Engine {
     double p_fro = 0;  // ||P||_F of P: next -> this (TransferOperator::frobenius_norm)
     // R: this level -> next; P: next -> this (device CSR)
     int *Rp = nullptr, *Ri = nullptr, *Pp = nullptr, *Pi = nullptr;
+    int* Rc = nullptr;  // R's entries pre-decoded for k_restrict_slab: i * 4 + (dj + 1)
     double *Rw = nullptr, *Pw = nullptr;
   };
   Options opt_;

@@ -785,6 +785,108 @@ __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restric
   Y[o * ncols + c] = to_t<T>(y);
 }
 
+// Restriction of many columns (GridHierarchy::build, transfer.cpp:155-174):
+// Y = R X for an h x w grid, X (h w rows) x ncols row-major.  The CSR entries
+// of R and their order are the reference's (k_csr_apply applies them as a
+// gather, re-reading every fine row up to four times).  Here a CTA owns a
+// 128-byte column slab and walks the coarse pixel columns cj in order,
+// keeping the three fine pixel columns 2cj - 1 .. 2cj + 1 in a shared-memory
+// ring (NS x h x SLABB bytes; NS = 5 prefetches the next two by cp.async while
+// cj is computed): every fine element is read from HBM once, every
+// coarse element written once.  Entry e is pre-decoded as code[e] = i * 4 +
+// (dj + 1) (fine row i within its pixel column, column offset dj).  Threads:
+// VEC columns each (one 16-byte vector; VEC = 1 when ncols is not a multiple
+// of 16 B), 128 / (VEC sizeof T) threads per pixel row.  F64MATH: the
+// reference's unfused fp64 sum in entry order (bit-identical to k_csr_apply);
+// otherwise fp32 FMA in the same order (fp32 storage, non-exact runs: within
+// an ulp of the fp64 result).
+template <typename T, int VEC, bool F64MATH, int SLABB = 128, int NS = 5>
+__global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ rowptr, const int* __restrict__ code,
+                                                       const double* __restrict__ wt, const T* __restrict__ X,
+                                                       T* __restrict__ Y, int h, int w, int hc, int wc,
+                                                       size_t ncols) {
+  constexpr int SLAB = SLABB / (int)sizeof(T);  // columns per CTA
+  constexpr int TPR = SLAB / VEC;               // threads per pixel row
+  // NS ring slots: columns 2cj-1 .. 2cj+1 (+ the next two, prefetched, when NS = 5)
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* ring = reinterpret_cast<T*>(smraw);  // [NS][h][SLAB]
+  const int t = threadIdx.x, part = t % TPR, grp = t / TPR, ngrp = blockDim.x / TPR;
+  const size_t c0 = (size_t)blockIdx.x * SLAB + (size_t)part * VEC;
+  const int nact = c0 >= ncols ? 0 : (int)min((size_t)VEC, ncols - c0);
+  // fine pixel column j -> its ring slot: asynchronous 16-byte copies (or
+  // plain loads on the unaligned path), committed as one group
+  auto fetch = [&](int j) {
+    T* dst = ring + (size_t)(j % NS) * h * SLAB + part * VEC;
+    const T* src = X + (size_t)j * h * ncols + c0;
+    for (int i = grp; i < h; i += ngrp) {
+      if (VEC > 1 && nact == VEC) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + (size_t)i * SLAB);
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(sa), "l"(src + (size_t)i * ncols)
+                     : "memory");
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) dst[(size_t)i * SLAB + v] = v < nact ? src[(size_t)i * ncols + v] : T(0);
+      }
+    }
+  };
+  fetch(0);
+  if (w > 1) fetch(1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int cj = 0; cj < wc; ++cj) {
+    if (NS == 5) {
+      // prefetch coarse column cj + 1's new fine columns during this one
+      if (2 * cj + 2 < w) fetch(2 * cj + 2);
+      if (2 * cj + 3 < w) fetch(2 * cj + 3);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this column's group has landed
+    } else {
+      if (cj > 0) {
+        if (2 * cj < w) fetch(2 * cj);
+        if (2 * cj + 1 < w) fetch(2 * cj + 1);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    // ring slot of fine column 2 cj + dj, dj = -1, 0, 1
+    const int sl[3] = {((2 * cj + NS - 1) % NS) * h * SLAB, ((2 * cj) % NS) * h * SLAB,
+                       ((2 * cj + 1) % NS) * h * SLAB};
+    for (int ci = grp; ci < hc; ci += ngrp) {
+      const size_t o = (size_t)cj * hc + ci;
+      const int eb = rowptr[o], ee = rowptr[o + 1];
+      double yd[VEC];
+      float yf[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) yd[v] = 0.0, yf[v] = 0.f;
+      for (int e = eb; e < ee; ++e) {
+        const int cd = code[e];
+        const T* xs = ring + sl[cd & 3] + (size_t)(cd >> 2) * SLAB + part * VEC;
+        T xv[VEC];
+        if (VEC > 1) {
+          *reinterpret_cast<uint4*>(xv) = *reinterpret_cast<const uint4*>(xs);
+        } else {
+          xv[0] = xs[0];
+        }
+        if (F64MATH) {
+          const double we = wt[e];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) yd[v] = __dadd_rn(yd[v], __dmul_rn(we, (double)xv[v]));
+        } else {
+          const float we = (float)wt[e];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) yf[v] = fmaf(we, (float)xv[v], yf[v]);
+        }
+      }
+      T* yo = Y + o * ncols + c0;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+        if (v < nact) yo[v] = F64MATH ? to_t<T>(yd[v]) : (T)yf[v];
+    }
+    __syncthreads();  // slots of columns 2cj - 1 and 2cj are refilled by the next prefetch
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // smoothness numerator, transfer.cpp:133-139: sum_ij (M_f - P M_c)_ij^2 with
 // M_c = R M_f (the next level's resident data), P applied on the fly in the
 // reference's entry order, so P R M is never stored.  Grid (colblocks, ry):
