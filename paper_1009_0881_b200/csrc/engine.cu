@@ -125,7 +125,7 @@ struct Engine::Impl {
     uint64_t h = 1469598103934665603ull;
     auto mixv = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     auto mix = [&](const void* p) { mixv((uint64_t)(uintptr_t)p); };
-    for (const DevBuf* b : {&AB, &Cb, &Db, &part, &red, &scal, &W, &flags}) mix(b->p);
+    for (const DevBuf* b : {&AB, &Cb, &Db, &part, &red, &scal, &W, &flags, &gws}) mix(b->p);
     mixv(e->n_loc_), mixv(e->n_total_), mixv(e->col0_), mixv(e->r_), mixv(e->lv_.size());
     for (const auto& L : e->lv_) {
       mixv(L.m), mixv(L.h), mixv(L.w);
@@ -396,10 +396,19 @@ struct Engine::Impl {
     if (exact() || r > 64 || std::getenv("MLNMF_THREAD_SWEEPS") != nullptr) return false;
     return count < kWarpSweepMax || std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
   }
+  // threads per block of the thread-per-row sweeps with the Gram and the
+  // rows in shared memory; 0 when r is too large for that (r > ~160): the
+  // sweeps then read the Gram from global memory (L2) and keep the rows in a
+  // global workspace (gsweep_ws)
   int sweep_block(int r) const {
     for (int bd : {128, 64, 32})
       if ((size_t)r * r * 8 + (size_t)r * bd * 8 <= kSmemMax) return bd;
-    throw std::invalid_argument("rank too large for the device sweep kernels (r <= 128)");
+    return 0;
+  }
+  DevBuf gws;  // large-rank workspaces (sweeps, NNLS)
+  double* gsweep_ws(size_t rows, int bd, size_t r) {
+    gws.ensure(ceil_div(rows, (size_t)bd) * bd * r * 8);
+    return gws.as<double>();
   }
 
   template <typename T>
@@ -429,8 +438,10 @@ struct Engine::Impl {
       }
     }
     double* V = static_cast<double*>(L.V);
-    const int bd = sweep_block((int)r);
-    const size_t smem = (r * r + r * bd) * 8;
+    const int bd0 = sweep_block((int)r);
+    const int bd = bd0 ? bd0 : 128;
+    const size_t smem = bd0 ? (r * r + r * bd) * 8 : 0;
+    double* gv_ws = bd0 ? nullptr : gsweep_ws(std::max(L.m, e->n_loc_), bd, r);
     timed(kPhV, [&] {
       const dim3 gv((unsigned)ceil_div(L.m, bd));
       if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
@@ -440,7 +451,7 @@ struct Engine::Impl {
         hals_v_reg(r, fast_sweeps(), A(), B(), V, L.m, deg, s);
         ++e->launches_;
       } else if (kind == kHals) {
-        launch(k_hals_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
+        launch(k_hals_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg, gv_ws);
       } else if (kind == kMu && warp_sweeps(r, L.m)) {
         launch(k_mu_warp<double, false>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)),
                dim3(256), r * r * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r);
@@ -448,7 +459,7 @@ struct Engine::Impl {
         mu_v_reg(r, A(), B(), V, L.m, s);
         ++e->launches_;
       } else if (kind == kMu) {
-        launch(k_mu_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r);
+        launch(k_mu_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, gv_ws);
       } else {
         cnt_steps.push_back(L.m);
         nnls((const double*)B(), L.m, (const double*)A(), r, 1, V, r, 1);
@@ -469,7 +480,7 @@ struct Engine::Impl {
         ++e->launches_;
       } else if (kind == kHals) {
         launch(k_hals_w<double>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-               e->n_loc_, (int)r, deg);
+               e->n_loc_, (int)r, deg, gv_ws);
       } else if (kind == kMu && warp_sweeps(r, e->n_loc_)) {
         launch(k_mu_warp<double, true>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
                dim3(256), r * r * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_,
@@ -479,7 +490,7 @@ struct Engine::Impl {
         ++e->launches_;
       } else if (kind == kMu) {
         launch(k_mu_w<double>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-               e->n_loc_, (int)r);
+               e->n_loc_, (int)r, gv_ws);
       } else {
         nnls((const double*)Db.as<double>(), e->n_loc_, (const double*)Cb.as<double>(), 1, e->n_loc_, Wp, 1,
                 e->n_loc_);
@@ -493,9 +504,21 @@ struct Engine::Impl {
   // batched NNLS over nprob problems; counts appended to the count ring
   void nnls(const double* G, size_t nprob, const double* H, size_t hi, size_t he, double* X, size_t xi, size_t xe) {
     const int r = (int)e->r_;
-    if (r > 128) throw std::invalid_argument("anls on the device supports rank <= 128");
     const size_t gbytes = (size_t)r * r * 8, wb = nnls_warp_bytes(r);
-    if (gbytes + wb > kSmemMax) throw std::invalid_argument("anls: rank too large for shared memory");
+    if (gbytes + wb > kSmemMax) {
+      // large ranks: Gram from global memory, per-warp workspaces in gws
+      const int nw = 4;
+      const size_t blocks = std::min<size_t>(ceil_div(nprob, (size_t)nw), (size_t)sm_count * 4);
+      gws.ensure(blocks * nw * wb);
+      int* cnt = reserve_counts(nprob);
+      if (exact())
+        launch(k_nnls_batch<double, true>, dim3((unsigned)blocks), dim3(32 * nw), 0, G, r, nprob, H, hi, he, X, xi,
+               xe, cnt, flags.as<int>() + 1, gws.as<unsigned char>());
+      else
+        launch(k_nnls_batch<double, false>, dim3((unsigned)blocks), dim3(32 * nw), 0, G, r, nprob, H, hi, he, X, xi,
+               xe, cnt, flags.as<int>() + 1, gws.as<unsigned char>());
+      return;
+    }
     // warps per block: as many as the SM's shared memory holds (the Gram is
     // staged once per block, so one wide block per SM beats several narrow
     // ones; 8 warps per block left large-rank problems at 8 warps per SM and
@@ -508,10 +531,10 @@ struct Engine::Impl {
     int* cnt = reserve_counts(nprob);
     if (exact())
       launch(k_nnls_batch<double, true>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi, xe,
-             cnt, flags.as<int>() + 1);
+             cnt, flags.as<int>() + 1, (unsigned char*)nullptr);
     else
       launch(k_nnls_batch<double, false>, dim3((unsigned)blocks), dim3(32 * nw), smem, G, r, nprob, H, hi, he, X, xi,
-             xe, cnt, flags.as<int>() + 1);
+             xe, cnt, flags.as<int>() + 1, (unsigned char*)nullptr);
   }
 
   // After an ANLS step: the reference throws at the failing step
@@ -594,12 +617,13 @@ struct Engine::Impl {
     const size_t spr = ceil_div(L.m, rchunk);
     part.ensure(spr * n * 8);
     const size_t smem = ((size_t)r * 128 + 32 * (size_t)r) * 8;
-    if (exact())
-      launch(k_col_sqerr<T, true>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M,
-             (const double*)L.V, (const double*)W.as<double>(), L.m, n, r, rchunk, part.as<double>());
-    else
-      launch(k_col_sqerr<T, false>, dim3((unsigned)cb, (unsigned)spr), dim3(128), smem, (const T*)L.M,
-             (const double*)L.V, (const double*)W.as<double>(), L.m, n, r, rchunk, part.as<double>());
+    const bool gm = smem > kSmemMax;  // large ranks: V and W straight from global memory
+    auto go = [&](auto kern) {
+      launch(kern, dim3((unsigned)cb, (unsigned)spr), dim3(128), gm ? 0 : smem, (const T*)L.M, (const double*)L.V,
+             (const double*)W.as<double>(), L.m, n, r, rchunk, part.as<double>());
+    };
+    if (exact()) gm ? go(k_col_sqerr<T, true, true>) : go(k_col_sqerr<T, true, false>);
+    else gm ? go(k_col_sqerr<T, false, true>) : go(k_col_sqerr<T, false, false>);
     if (exact()) {
       launch(k_sum_final, dim3(1), dim3(32), 0, (const double*)part.as<double>(), n, out, 1);
     } else {
@@ -742,7 +766,7 @@ Engine::~Engine() {
     dev_free(L.mstat);
     dev_free(L.Rp), dev_free(L.Ri), dev_free(L.Rw), dev_free(L.Pp), dev_free(L.Pi), dev_free(L.Pw), dev_free(L.Rc);
   }
-  for (DevBuf* b : {&impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
+  for (DevBuf* b : {&impl_->gws, &impl_->AB, &impl_->Cb, &impl_->Db, &impl_->part, &impl_->red, &impl_->scal, &impl_->W,
                     &impl_->samples, &impl_->counts, &impl_->flags, &impl_->tstart, &impl_->stage})
     b->release();
   for (auto& p : impl_->ev_mwt) cudaEventDestroy(p.first), cudaEventDestroy(p.second);

@@ -258,12 +258,15 @@ __global__ void __launch_bounds__(256) k_reduce_splits_wide(const double* __rest
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void k_hals_v(const double* __restrict__ A, const double* __restrict__ B, T* __restrict__ V,
-                         size_t m, int r, int* __restrict__ degenerate) {
+                         size_t m, int r, int* __restrict__ degenerate, double* __restrict__ gws) {
+  // gws (ranks too large for shared memory): the Gram is read from global
+  // memory (L2-resident) and the block's rows live in gws[block][l][thread]
   extern __shared__ double sm[];
   const int bd = blockDim.x, t = threadIdx.x;
-  double* Bs = sm;
-  double* vs = sm + (size_t)r * r;
-  for (int e = t; e < r * r; e += bd) Bs[e] = B[e];
+  const double* Bs = gws ? B : sm;
+  double* vs = gws ? gws + (size_t)blockIdx.x * bd * r : sm + (size_t)r * r;
+  if (!gws)
+    for (int e = t; e < r * r; e += bd) sm[e] = B[e];
   const size_t i = (size_t)blockIdx.x * bd + t;
   const bool act = i < m;
   if (act)
@@ -287,12 +290,13 @@ __global__ void k_hals_v(const double* __restrict__ A, const double* __restrict_
 
 template <typename T>
 __global__ void k_hals_w(const double* __restrict__ Cm, const double* __restrict__ D, T* __restrict__ W,
-                         size_t n, int r, int* __restrict__ degenerate) {
+                         size_t n, int r, int* __restrict__ degenerate, double* __restrict__ gws) {
   extern __shared__ double sm[];
   const int bd = blockDim.x, t = threadIdx.x;
-  double* Ds = sm;
-  double* ws = sm + (size_t)r * r;
-  for (int e = t; e < r * r; e += bd) Ds[e] = D[e];
+  const double* Ds = gws ? D : sm;
+  double* ws = gws ? gws + (size_t)blockIdx.x * bd * r : sm + (size_t)r * r;
+  if (!gws)
+    for (int e = t; e < r * r; e += bd) sm[e] = D[e];
   const size_t j = (size_t)blockIdx.x * bd + t;
   const bool act = j < n;
   if (act)
@@ -431,12 +435,13 @@ __device__ __forceinline__ double mu_floor(double v) { return v < 1e-16 ? 1e-16 
 
 template <typename T>
 __global__ void k_mu_v(const double* __restrict__ A, const double* __restrict__ B, T* __restrict__ V,
-                       size_t m, int r) {
+                       size_t m, int r, double* __restrict__ gws) {
   extern __shared__ double sm[];
   const int bd = blockDim.x, t = threadIdx.x;
-  double* Bs = sm;
-  double* vs = sm + (size_t)r * r;
-  for (int e = t; e < r * r; e += bd) Bs[e] = B[e];
+  const double* Bs = gws ? B : sm;
+  double* vs = gws ? gws + (size_t)blockIdx.x * bd * r : sm + (size_t)r * r;
+  if (!gws)
+    for (int e = t; e < r * r; e += bd) sm[e] = B[e];
   const size_t i = (size_t)blockIdx.x * bd + t;
   const bool act = i < m;
   if (act)
@@ -453,12 +458,13 @@ __global__ void k_mu_v(const double* __restrict__ A, const double* __restrict__ 
 // W(:,j) *= C(:,j) / max(D W(:,j), 1e-16)
 template <typename T>
 __global__ void k_mu_w(const double* __restrict__ Cm, const double* __restrict__ D, T* __restrict__ W,
-                       size_t n, int r) {
+                       size_t n, int r, double* __restrict__ gws) {
   extern __shared__ double sm[];
   const int bd = blockDim.x, t = threadIdx.x;
-  double* Ds = sm;
-  double* ws = sm + (size_t)r * r;
-  for (int e = t; e < r * r; e += bd) Ds[e] = D[e];
+  const double* Ds = gws ? D : sm;
+  double* ws = gws ? gws + (size_t)blockIdx.x * bd * r : sm + (size_t)r * r;
+  if (!gws)
+    for (int e = t; e < r * r; e += bd) sm[e] = D[e];
   const size_t j = (size_t)blockIdx.x * bd + t;
   const bool act = j < n;
   if (act)
@@ -506,32 +512,39 @@ __global__ void __launch_bounds__(256) k_mu_warp(const double* __restrict__ A, c
 //   part[z][j] = sum_{i in split z} (M_ij - sum_k V_ik W_kj)^2
 // 128 columns per block; V rows staged 32 at a time; W column tile in smem.
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT>
+template <typename T, bool EXACT, bool GM = false>
 __global__ void __launch_bounds__(128) k_col_sqerr(const T* __restrict__ M, const double* __restrict__ V,
                                                    const double* __restrict__ W, size_t m, size_t n, int r,
                                                    size_t rchunk, double* __restrict__ part) {
+  // GM (ranks too large for the shared-memory staging): V and W are read
+  // from global memory directly, in the same operation order
   extern __shared__ double sm[];
   const int t = threadIdx.x;
   double* Ws = sm;                    // r x 128
   double* Vs = sm + (size_t)r * 128;  // 32 x r
   const size_t j = (size_t)blockIdx.x * 128 + t;
   const bool act = j < n;
-  for (int k = 0; k < r; ++k) Ws[k * 128 + t] = act ? (double)W[(size_t)k * n + j] : 0.0;
+  if (!GM)
+    for (int k = 0; k < r; ++k) Ws[k * 128 + t] = act ? (double)W[(size_t)k * n + j] : 0.0;
   const size_t ib = (size_t)blockIdx.y * rchunk;
   const size_t ie = ib + rchunk < m ? ib + rchunk : m;
   double acc = 0.0;
   for (size_t i0 = ib; i0 < ie; i0 += 32) {
-    __syncthreads();
-    for (int e = t; e < 32 * r; e += 128) {
-      const size_t i = i0 + e / r;
-      Vs[e] = i < ie ? (double)V[i * r + (e % r)] : 0.0;
+    if (!GM) {
+      __syncthreads();
+      for (int e = t; e < 32 * r; e += 128) {
+        const size_t i = i0 + e / r;
+        Vs[e] = i < ie ? (double)V[i * r + (e % r)] : 0.0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (!act) continue;
     const int cnt = (int)((ie - i0) < 32 ? (ie - i0) : 32);
     for (int ii = 0; ii < cnt; ++ii) {
       double pred = 0.0;
-      for (int k = 0; k < r; ++k) pred = madd<EXACT>(pred, Vs[ii * r + k], Ws[k * 128 + t]);
+      for (int k = 0; k < r; ++k)
+        pred = GM ? madd<EXACT>(pred, V[(i0 + ii) * r + k], W[(size_t)k * n + j])
+                  : madd<EXACT>(pred, Vs[ii * r + k], Ws[k * 128 + t]);
       const double d = EXACT ? __dsub_rn((double)M[(i0 + ii) * n + j], pred) : (double)M[(i0 + ii) * n + j] - pred;
       acc = madd<EXACT>(acc, d, d);
     }

@@ -157,11 +157,14 @@ __device__ inline bool warp_solve_passive(const double* Gs, int r, const NnlsWar
 template <typename T, bool EXACT>
 __global__ void k_nnls_batch(const double* __restrict__ G, int r, size_t nprob, const double* __restrict__ H,
                              size_t hi, size_t he, T* __restrict__ X, size_t xi, size_t xe,
-                             int* __restrict__ counts, int* __restrict__ err) {
+                             int* __restrict__ counts, int* __restrict__ err, unsigned char* __restrict__ gws) {
+  // gws (ranks too large for shared memory): the Gram is read from global
+  // memory and each warp's workspace is gws + (global warp) * nnls_warp_bytes
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* Gs = reinterpret_cast<double*>(smraw);
+  const double* Gs = gws ? G : reinterpret_cast<const double*>(smraw);
   const int nwarps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = G[e];
+  if (!gws)
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) reinterpret_cast<double*>(smraw)[e] = G[e];
   __syncthreads();
   // ridge base: 1e-12 * tr(G) / r (solvers.cpp:64-67)
   double trace = 0.0;
@@ -169,7 +172,8 @@ __global__ void k_nnls_batch(const double* __restrict__ G, int r, size_t nprob, 
   double ridge0 = 1e-12 * trace / (double)r;
   if (ridge0 <= 0.0) ridge0 = 1e-12;
 
-  unsigned char* base = smraw + (size_t)r * r * 8 + (size_t)warp * nnls_warp_bytes(r);
+  unsigned char* base = gws ? gws + ((size_t)blockIdx.x * nwarps + warp) * nnls_warp_bytes(r)
+                            : smraw + (size_t)r * r * 8 + (size_t)warp * nnls_warp_bytes(r);
   NnlsWarpMem wm;
   wm.L = reinterpret_cast<double*>(base);
   wm.b = wm.L + (size_t)r * (r + 1) / 2;
