@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "engine.hpp"
@@ -294,9 +295,9 @@ struct Engine::Impl {
   // per (level, rank r) for ALL ranks (decide_tc): every rank must issue
   // the same collectives, and the shape rules see the local column count.
   std::map<std::pair<size_t, size_t>, bool> tc_ok;
-  bool use_tc(size_t m) const {
-    if (!tc) return false;
-    auto it = tc_ok.find({m, e->r_});
+  bool use_tc(size_t l) const {
+    if (!tc || e->lv_[l].dt != 0) return false;
+    auto it = tc_ok.find({e->lv_[l].m, e->r_});
     if (it == tc_ok.end()) throw std::logic_error("tensor-path decision missing for a level (decide_tc)");
     return it->second;
   }
@@ -305,6 +306,7 @@ struct Engine::Impl {
   void decide_tc() {
     if (!tc || e->r_ == 0) return;
     for (const auto& L : e->lv_) {
+      if (L.dt != 0) continue;  // fp64 levels never take the tensor path
       const auto key = std::make_pair(L.m, e->r_);
       if (tc_ok.count(key)) continue;
       double veto = tc->wants(L.m, e->n_loc_, e->r_) ? 0.0 : 1.0;
@@ -339,7 +341,7 @@ struct Engine::Impl {
       evp = {ev(), ev()};
       CK(cudaEventRecord(evp.first, s));
     }
-    if (use_tc(L.m))
+    if (use_tc(l))
       tc->mwt(static_cast<const T*>(L.M), level_stats(l), W.as<double>(), L.m, e->n_loc_, e->r_, A(), s,
               &e->launches_);
     else
@@ -358,7 +360,7 @@ struct Engine::Impl {
       evp = {ev(), ev()};
       CK(cudaEventRecord(evp.first, s));
     }
-    if (use_tc(L.m))
+    if (use_tc(l))
       tc->vtm(static_cast<const double*>(L.V), static_cast<const T*>(L.M), level_stats(l) + L.m, L.m, e->n_loc_,
               e->r_, Cb.as<double>(), s, &e->launches_);
     else
@@ -662,7 +664,7 @@ struct Engine::Impl {
   // residual (k_sqerr_tiled, gated on the device: no host sync) is used.
   static constexpr double kGramTau = 1e-4;  // e < 1 % of ||M_l||
   bool tc_sample(size_t l) const {
-    return !exact() && use_tc(e->lv_[l].m) && e->opt_.error_mode == 0;
+    return !exact() && use_tc(l) && e->opt_.error_mode == 0;
   }
   template <typename T>
   void tc_e2(size_t l, double* sc) {
@@ -780,7 +782,7 @@ Engine::~Engine() {
   delete impl_;
 }
 
-bool Engine::tc_active() const { return impl_->tc && !lv_.empty() && r_ > 0 && impl_->use_tc(lv_[0].m); }
+bool Engine::tc_active() const { return impl_->tc && !lv_.empty() && r_ > 0 && impl_->use_tc(0); }
 bool Engine::gram_error() const {
   if (opt_.error_mode == 1) return true;
   if (opt_.error_mode == 2) return false;
@@ -818,6 +820,7 @@ void Engine::set_data(const void* M, int host_dtype, bool is_device, size_t m, s
   n_total_ = n_total;
   col0_ = col0;
   Level L0{h, w, m};
+  L0.dt = opt_.dtype;
   const size_t count = m * n_loc, es = impl_->esz();
   CK(dev_malloc(&L0.M, count * es));
   lv_.push_back(L0);
@@ -884,6 +887,7 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
   n_total_ = n_total;
   col0_ = col0;
   Level L0{g.h, g.w, m};
+  L0.dt = opt_.dtype;
   CK(dev_malloc(&L0.M, m * n_loc * impl_->esz()));
   lv_.push_back(L0);
   cudaStream_t s = impl_->s;
@@ -933,7 +937,6 @@ void Engine::generate(const GenParams& g, size_t n_total, size_t col0, size_t n_
 void Engine::ensure_levels(size_t L) {
   if (lv_.empty()) throw std::invalid_argument("no data set");
   if (L < 1) throw std::invalid_argument("GridHierarchy: need at least one level");
-  const size_t es = impl_->esz();
   while (lv_.size() < L) {
     Level& cur = lv_.back();
     if (cur.h < 2 || cur.w < 2) throw std::invalid_argument("GridHierarchy: too many levels for this grid");
@@ -964,55 +967,47 @@ void Engine::ensure_levels(size_t L) {
     cur.p_fro = std::sqrt(pf);
     Level nx{(cur.h + 1) / 2, (cur.w + 1) / 2, 0};
     nx.m = nx.h * nx.w;
-    CK(dev_malloc(&nx.M, nx.m * n_loc_ * es));
+    // Storage of the restricted level: fp32 only where the tensor path will
+    // stream it (its input format); otherwise fp64, so an fp32 session's
+    // small pyramids are not rounded to fp32 (the oracle restricts in fp64:
+    // config 3's 5-level runs deviated 9e-5 with fp32 levels, r02)
+    nx.dt = (cur.dt == 0 && impl_->tc && impl_->tc->wants(nx.m, n_loc_, 64)) ? 0 : 1;
+    const size_t esn = nx.dt == 0 ? 4 : 8, esc = cur.dt == 0 ? 4 : 8;
+    CK(dev_malloc(&nx.M, nx.m * n_loc_ * esn));
     const size_t slab_smem = 3 * cur.h * 64;
-    if (slab_smem <= 200 * 1024) {
-      // column slabs with the fine pixel columns staged once (k_restrict_slab)
-      const unsigned g = (unsigned)ceil_div(n_loc_ * es, 64);
-      const int h = (int)cur.h, w = (int)cur.w, hc = (int)nx.h, wc = (int)nx.w;
-      const bool vec = (n_loc_ * es) % 16 == 0;
-      if (opt_.dtype == 0 && !impl_->exact()) {
-        // 64-byte slabs, 3-slot ring (48 KB: 4 CTAs per SM) measured best of
-        // {128, 64, 32} B x {3, 5 (prefetch)} slots and an L1-only variant
-        // (config-4 pyramid 77 ms with the gather -> 51 ms; r02)
-        if (vec)
-          impl_->launch(k_restrict_slab<float, 4, false, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
-                        w, hc, wc, n_loc_);
+    const int h = (int)cur.h, w = (int)cur.w, hc = (int)nx.h, wc = (int)nx.w;
+    // column slabs with the fine pixel columns staged once (k_restrict_slab;
+    // 64-byte slabs, 3-slot ring: 48 KB, 4 CTAs per SM -- measured best of
+    // {128, 64, 32} B x {3, 5 (prefetch)} slots and an L1-only variant,
+    // config-4 pyramid 77 ms with the gather -> 51 ms, r02), else the gather
+    auto restrict_to = [&](auto tin, auto tout, auto f64math) {
+      using TI = decltype(tin);
+      using TO = decltype(tout);
+      constexpr bool F64 = decltype(f64math)::value;
+      const TI* X = static_cast<const TI*>(cur.M);
+      TO* Y = static_cast<TO*>(nx.M);
+      if (slab_smem <= 200 * 1024) {
+        const unsigned g = (unsigned)ceil_div(n_loc_ * esc, 64);
+        if ((n_loc_ * esc) % 16 == 0)
+          impl_->launch(k_restrict_slab<TI, TO, 16 / sizeof(TI), F64>, dim3(g), dim3(256), slab_smem,
+                        (const int*)cur.Rp, (const int*)cur.Rc, (const double*)cur.Rw, X, Y, h, w, hc, wc, n_loc_);
         else
-          impl_->launch(k_restrict_slab<float, 1, false, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
-                        w, hc, wc, n_loc_);
-      } else if (opt_.dtype == 0) {
-        if (vec)
-          impl_->launch(k_restrict_slab<float, 4, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
-                        w, hc, wc, n_loc_);
-        else
-          impl_->launch(k_restrict_slab<float, 1, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), h,
-                        w, hc, wc, n_loc_);
+          impl_->launch(k_restrict_slab<TI, TO, 1, F64>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
+                        (const int*)cur.Rc, (const double*)cur.Rw, X, Y, h, w, hc, wc, n_loc_);
       } else {
-        if (vec)
-          impl_->launch(k_restrict_slab<double, 2, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
-                        h, w, hc, wc, n_loc_);
-        else
-          impl_->launch(k_restrict_slab<double, 1, true, 64, 3>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
-                        h, w, hc, wc, n_loc_);
+        const size_t colblocks = ceil_div(n_loc_, 256);
+        impl_->launch(k_csr_apply<TI, TO>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
+                      (const int*)cur.Ri, (const double*)cur.Rw, X, Y, nx.m, n_loc_, colblocks);
       }
-    } else {
-      const size_t colblocks = ceil_div(n_loc_, 256);
-      if (opt_.dtype == 0)
-        impl_->launch(k_csr_apply<float>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
-                      (const int*)cur.Ri, (const double*)cur.Rw, (const float*)cur.M, static_cast<float*>(nx.M), nx.m,
-                      n_loc_, colblocks);
-      else
-        impl_->launch(k_csr_apply<double>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
-                      (const int*)cur.Ri, (const double*)cur.Rw, (const double*)cur.M, static_cast<double*>(nx.M),
-                      nx.m, n_loc_, colblocks);
-    }
+    };
+    if (cur.dt == 1)
+      restrict_to(double(), double(), std::true_type());
+    else if (nx.dt == 1)
+      restrict_to(float(), double(), std::true_type());
+    else if (impl_->exact())
+      restrict_to(float(), float(), std::true_type());
+    else
+      restrict_to(float(), float(), std::false_type());
     if (r_ > 0) CK(dev_malloc(&nx.V, nx.m * r_ * 8));  // factors are fp64
     lv_.push_back(nx);
   }
@@ -1024,7 +1019,7 @@ double Engine::norm2(size_t l) {
   Level& L = lv_.at(l);
   if (L.norm2 < 0) {
     double* sc = impl_->scal.as<double>();
-    if (opt_.dtype == 0) impl_->dot<float>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
+    if (L.dt == 0) impl_->dot<float>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
     else impl_->dot<double>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
     impl_->allreduce_sum(sc + 4, 1);
     CK(cudaMemcpyAsync(&L.norm2, sc + 4, 8, cudaMemcpyDeviceToHost, impl_->s));
@@ -1043,12 +1038,15 @@ double Engine::smoothness(size_t l) {
   impl_->part.ensure(cb * ry * 8);
   double* part = impl_->part.as<double>();
   double* sc = impl_->scal.as<double>();
-  if (opt_.dtype == 0)
-    impl_->launch(k_csr_residual<float>, dim3((unsigned)cb, (unsigned)ry), dim3(256), 0, (const int*)F.Pp,
-                  (const int*)F.Pi, (const double*)F.Pw, (const float*)Cl.M, (const float*)F.M, F.m, n_loc_, part);
-  else
-    impl_->launch(k_csr_residual<double>, dim3((unsigned)cb, (unsigned)ry), dim3(256), 0, (const int*)F.Pp,
-                  (const int*)F.Pi, (const double*)F.Pw, (const double*)Cl.M, (const double*)F.M, F.m, n_loc_, part);
+  auto go = [&](auto tc_, auto tf_) {
+    using TC = decltype(tc_);
+    using TF = decltype(tf_);
+    impl_->launch(k_csr_residual<TC, TF>, dim3((unsigned)cb, (unsigned)ry), dim3(256), 0, (const int*)F.Pp,
+                  (const int*)F.Pi, (const double*)F.Pw, (const TC*)Cl.M, (const TF*)F.M, F.m, n_loc_, part);
+  };
+  if (F.dt == 0 && Cl.dt == 0) go(float(), float());
+  else if (F.dt == 0) go(double(), float());
+  else go(double(), double());
   impl_->launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part, cb * ry, sc + 5, 0);
   impl_->allreduce_sum(sc + 5, 1);
   double s = 0;
@@ -1191,7 +1189,7 @@ void Engine::step(size_t l, Kind kind) {
       if (!g.warm) {  // one eager step first: buffers reach their steady-state sizes
         g.warm = true;
         im.B_valid = false;
-        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        if (lv_[l].dt == 0) im.step_t<float>(l, kind);
         else im.step_t<double>(l, kind);
         return;
       }
@@ -1202,7 +1200,7 @@ void Engine::step(size_t l, Kind kind) {
       CK(cudaStreamBeginCapture(im.s, cudaStreamCaptureModeRelaxed));
       im.B_valid = false;  // the captured step always recomputes B = W W^T
       try {
-        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        if (lv_[l].dt == 0) im.step_t<float>(l, kind);
         else im.step_t<double>(l, kind);
       } catch (...) {
         cudaStreamEndCapture(im.s, &graph);
@@ -1216,7 +1214,7 @@ void Engine::step(size_t l, Kind kind) {
         cudaGraphDestroy(graph);
         g.warm = false;
         im.B_valid = false;
-        if (opt_.dtype == 0) im.step_t<float>(l, kind);
+        if (lv_[l].dt == 0) im.step_t<float>(l, kind);
         else im.step_t<double>(l, kind);
         return;
       }
@@ -1231,7 +1229,7 @@ void Engine::step(size_t l, Kind kind) {
     im.CD_level = l;
     return;
   }
-  if (opt_.dtype == 0) impl_->step_t<float>(l, kind);
+  if (lv_[l].dt == 0) impl_->step_t<float>(l, kind);
   else impl_->step_t<double>(l, kind);
   if (kind == kAnls) impl_->check_nnls();
 }
@@ -1239,7 +1237,7 @@ void Engine::step(size_t l, Kind kind) {
 void Engine::sample(size_t l, double work_units) {
   norm2(l);  // host-cached after first use (one sync per level per run)
   if (impl_->CD_valid && impl_->CD_level != l) impl_->CD_valid = false;
-  if (opt_.dtype == 0) impl_->sample_t<float>(l, work_units);
+  if (lv_[l].dt == 0) impl_->sample_t<float>(l, work_units);
   else impl_->sample_t<double>(l, work_units);
 }
 
@@ -1332,7 +1330,7 @@ void Engine::flush(std::vector<Sample>* samples, std::vector<int>* counts, int* 
 
 double Engine::frobenius_error(size_t l) {
   double* sc = impl_->scal.as<double>();
-  if (opt_.dtype == 0) impl_->direct_e2<float>(l, sc);
+  if (lv_.at(l).dt == 0) impl_->direct_e2<float>(l, sc);
   else impl_->direct_e2<double>(l, sc);
   double e2 = 0;
   CK(cudaMemcpyAsync(&e2, sc, 8, cudaMemcpyDeviceToHost, impl_->s));

@@ -156,6 +156,7 @@ class Engine {
  private:
   struct Level {
     size_t h, w, m;
+    int dt = 1;  // storage of M at this level: 0 fp32, 1 fp64 (level 0: the session's dtype)
     void* M = nullptr;  // T[m x n_loc]
     void* V = nullptr;  // T[m x r]
     float* mstat = nullptr;  // tensor path: row maxima (m) then column maxima (n_loc) of M

@@ -785,9 +785,9 @@ __global__ void k_timestamp(unsigned long long* out) { *out = globaltimer(); }
 // Transfer operators (transfer.cpp:17-33): Y[o,:] = sum_e w_e X[idx_e,:],
 // entries in the reference's order, unfused multiply-add, fp64 math.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, typename TO = T>
 __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restrict__ idx,
-                            const double* __restrict__ wt, const T* __restrict__ X, T* __restrict__ Y,
+                            const double* __restrict__ wt, const T* __restrict__ X, TO* __restrict__ Y,
                             size_t out_rows, size_t ncols, size_t colblocks) {
   const size_t o = blockIdx.x / colblocks;
   const size_t c = (blockIdx.x % colblocks) * blockDim.x + threadIdx.x;
@@ -795,7 +795,7 @@ __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restric
   const int eb = rowptr[o], ee = rowptr[o + 1];
   double y = 0.0;
   for (int e = eb; e < ee; ++e) y = __dadd_rn(y, __dmul_rn(wt[e], (double)X[(size_t)idx[e] * ncols + c]));
-  Y[o * ncols + c] = to_t<T>(y);
+  Y[o * ncols + c] = to_t<TO>(y);
 }
 
 // Restriction of many columns (GridHierarchy::build, transfer.cpp:155-174):
@@ -813,10 +813,10 @@ __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restric
 // reference's unfused fp64 sum in entry order (bit-identical to k_csr_apply);
 // otherwise fp32 FMA in the same order (fp32 storage, non-exact runs: within
 // an ulp of the fp64 result).
-template <typename T, int VEC, bool F64MATH, int SLABB = 128, int NS = 5>
+template <typename T, typename TO, int VEC, bool F64MATH, int SLABB = 64, int NS = 3>
 __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ rowptr, const int* __restrict__ code,
                                                        const double* __restrict__ wt, const T* __restrict__ X,
-                                                       T* __restrict__ Y, int h, int w, int hc, int wc,
+                                                       TO* __restrict__ Y, int h, int w, int hc, int wc,
                                                        size_t ncols) {
   constexpr int SLAB = SLABB / (int)sizeof(T);  // columns per CTA
   constexpr int TPR = SLAB / VEC;               // threads per pixel row
@@ -890,10 +890,10 @@ __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ r
           for (int v = 0; v < VEC; ++v) yf[v] = fmaf(we, (float)xv[v], yf[v]);
         }
       }
-      T* yo = Y + o * ncols + c0;
+      TO* yo = Y + o * ncols + c0;
 #pragma unroll
       for (int v = 0; v < VEC; ++v)
-        if (v < nact) yo[v] = F64MATH ? to_t<T>(yd[v]) : (T)yf[v];
+        if (v < nact) yo[v] = F64MATH ? to_t<TO>(yd[v]) : (TO)yf[v];
     }
     __syncthreads();  // slots of columns 2cj - 1 and 2cj are refilled by the next prefetch
   }
@@ -904,10 +904,10 @@ __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ r
 // M_c = R M_f (the next level's resident data), P applied on the fly in the
 // reference's entry order, so P R M is never stored.  Grid (colblocks, ry):
 // column-coalesced, rows strided by ry; one fp64 partial per CTA.
-template <typename T>
+template <typename TC, typename TF>
 __global__ void __launch_bounds__(256) k_csr_residual(const int* __restrict__ rowptr, const int* __restrict__ idx,
-                                                      const double* __restrict__ wt, const T* __restrict__ Mc,
-                                                      const T* __restrict__ Mf, size_t rows, size_t ncols,
+                                                      const double* __restrict__ wt, const TC* __restrict__ Mc,
+                                                      const TF* __restrict__ Mf, size_t rows, size_t ncols,
                                                       double* __restrict__ part) {
   __shared__ double ws[8];
   const size_t c = (size_t)blockIdx.x * 256 + threadIdx.x;
