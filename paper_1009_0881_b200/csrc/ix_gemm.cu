@@ -82,7 +82,7 @@ namespace ix {
 
 constexpr int kChunk = 32;             // K elements per pipeline chunk
 constexpr int kMStages = 8;            // M-slice ring (TMA -> converters), 16 KB each
-constexpr int kMGroup = 2;             // the ring is filled and released in pairs of slices
+constexpr int kMGroup = 2;             // the ring is filled and released in pairs of slices (one TMA each; 4 measured slower, r02)
 constexpr int kMGroups = kMStages / kMGroup;
 constexpr int kBStages = 2;            // factor digit ring (TMA -> MMA), one chunk QUAD per stage
 constexpr int kBStageBytes = 32768;    // 4 planes x r_pad (<= 64) rows x 128 B (= 4 chunks x 32 K)
@@ -94,6 +94,7 @@ constexpr int kGroupCols = 64;         // columns per accumulator group (r_pad <
 constexpr int kClasses = 4;            // digit-product weight classes 2^40, 2^32, 2^24, 2^16
 constexpr int kAccCols = kClasses * kGroupCols;
 constexpr int kStg0 = 256;             // staging slots after the (single) accumulator set
+static_assert(kQuad % kMGroup == 0, "units (whole quads) hold whole M groups");
 static_assert(kAccCols <= kStg0 && kStg0 + kSlots * kSlotCols <= 512, "TMEM map");
 // factor fixed point: 31 bits (four digits e1 e2 e3 e4, e1 in [0, 127])
 constexpr double kFBias = 8421504.0;   // 0x808080: balanced low three digits
@@ -421,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t fm = smem_u32(&mfull[ps]);
         mbar_expect_tx(fm, npend * kMTileBytes);
         unsigned char* dst = sm_m + ps * kMGroup * kMTileBytes;
-        if (!TRANS && p.wide) {
-          // chunk pair (c, c + 1), c even, same tile: each row's 256
-          // contiguous bytes in one request stream
+        if (!TRANS && p.wide && npend == kMGroup) {
+          // chunks c .. c + 3 of one tile: each row's 512 contiguous bytes
+          // in one request stream, one 3-D box
           tma_load_3d(smem_u32(dst), &map_m, 0, pc[0], pt[0] * 128, fm, pol);
         } else {
           for (int k = 0; k < npend; ++k) {
@@ -533,13 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pl[32];
         const uint32_t tile = smem_u32(sm_m) + (uint32_t)((ps * kMGroup + g % kMGroup) * kMTileBytes);
         if (!TRANS && p.wide) {
-          // pair buffer [row][half][32] (SWIZZLE_128B per 128-byte line):
-          // this chunk's row is line 2 row + h, 16-byte piece j at j ^ (line & 7);
-          // lanes 4..7 of each quarter-warp walk the pieces flipped (j ^ 1) so
-          // the 8 lanes of a wavefront hit 8 distinct bank groups; the planes
-          // of adjacent pieces are swapped back afterwards
+          // group buffer [row][chunk][32] (SWIZZLE_128B per 128-byte line):
+          // this chunk's row is line kMGroup row + c, 16-byte piece j at
+          // j ^ (line & 7); lanes 4..7 of each quarter-warp walk the pieces
+          // flipped (j ^ 1) to spread the wavefront over the bank groups;
+          // the planes of adjacent pieces are swapped back afterwards
           const uint32_t pairb = smem_u32(sm_m) + (uint32_t)(ps * kMGroup * kMTileBytes);
-          const uint32_t line = 2u * (uint32_t)row + (uint32_t)(g & 1);
+          const uint32_t line = (uint32_t)kMGroup * (uint32_t)row + (uint32_t)(g % kMGroup);
           const int flip = (lane >> 2) & 1;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -837,14 +838,14 @@ CUtensorMap map_f32(const void* ptr, uint64_t inner, uint64_t outer, uint32_t bi
   encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, swz);
   return m;
 }
-// 3-D view of a row-major fp32 matrix (n % 64 == 0): (32 columns, n / 32
-// column blocks, m rows), box (32, 2, 128): one 128-row x 256-byte slab laid
-// out [row][block][32] with the 128-byte swizzle.
+// 3-D view of a row-major fp32 matrix (n % (32 kMGroup) == 0): (32 columns,
+// n / 32 column blocks, m rows), box (32, kMGroup, 128): one 128-row x
+// (128 kMGroup)-byte slab laid out [row][block][32] with the 128-byte swizzle.
 CUtensorMap map_rows3(const void* ptr, uint64_t n, uint64_t m) {
   CUtensorMap map;
   cuuint64_t dims[3] = {32, n / 32, m};
   cuuint64_t strides[2] = {128, n * 4};
-  cuuint32_t box[3] = {32, 2, 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)ix::kMGroup, 128};
   encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, true);
   return map;
 }
@@ -938,7 +939,7 @@ class IxGemm final : public TcGemm {
     p.rp = rp;
     p.tiles = (int)cdiv(rows, 128);
     p.nchunks = (int)nchunks;
-    p.wide = (!TRANS && n % 64 == 0) ? 1 : 0;
+    p.wide = (!TRANS && n % (32 * ix::kMGroup) == 0) ? 1 : 0;
     p.rowmax = rowmax;
     p.fmax = static_cast<const float*>(fmax_);
     // split-K: units (tile, K range) are dealt round-robin to the persistent
