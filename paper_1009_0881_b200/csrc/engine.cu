@@ -693,7 +693,7 @@ struct Engine::Impl {
   // (D = V_l^T V_l, B = W W^T), all ranks; products recomputed only when the
   // cached ones are stale
   template <typename T>
-  void gram_terms(size_t l, double* out) {
+  void gram_prepare(size_t l) {
     const size_t r = e->r_;
     if (!(CD_valid && CD_level == l)) {
       gram_V<T>(l);
@@ -706,7 +706,12 @@ struct Engine::Impl {
       allreduce_sum(B(), r * r);
       B_valid = true;
     }
-    CK(cudaMemcpyAsync(out, &e->lv_[l].norm2, 8, cudaMemcpyHostToDevice, s));
+  }
+  template <typename T>
+  void gram_terms(size_t l, double* out) {
+    const size_t r = e->r_;
+    gram_prepare<T>(l);
+    launch(k_set1, dim3(1), dim3(1), 0, out, e->lv_[l].norm2);  // host-cached ||M_l||^2
     dot<T>(Cb.as<double>(), 0, W.as<double>(), 1, r * e->n_loc_, out + 1);
     allreduce_sum(out + 1, 1);
     dot<T>(Db.as<double>(), 0, B(), 1, r * r, out + 2);
@@ -719,6 +724,15 @@ struct Engine::Impl {
     if (tc_sample(l)) {
       tc_e2<T>(l, sc);  // sc[0] = e^2
       gram = false;
+    } else if (gram && e->opt_.world == 1 && e->r_ * e->n_loc_ <= ((size_t)1 << 20)) {
+      // small, one rank: the whole identity and the record in one launch
+      gram_prepare<T>(l);
+      SampleRec* rec = reserve_sample();
+      launch(k_gram_sample, dim3(1), dim3(1024), 0, (const double*)Cb.as<double>(), (const double*)W.as<double>(),
+             e->r_ * e->n_loc_, (const double*)Db.as<double>(), (const double*)B(), e->r_ * e->r_, e->lv_[l].norm2, sc,
+             rec);
+      samp_meta.push_back({0.0, work_units, (int)l + 1, 0.0});
+      return;
     } else if (gram) {
       gram_terms<T>(l, sc);
     } else {

@@ -761,6 +761,35 @@ __global__ void k_write_sample(const double* __restrict__ s, int gram, SampleRec
   out->t_ns = globaltimer();
 }
 
+__global__ void k_set1(double* out, double v) { *out = v; }
+
+// A whole Gram-identity sample in one launch (small problems, one rank):
+// s[0] = ||M||^2 (argument), s[1] = <C, W> (count_cw elements), s[2] =
+// <D, B> (count_db), each a fixed-order strided sum over the block's threads
+// and a fixed tree; rec = sqrt(max(s0 - 2 s1 + s2, 0)) and the time stamp.
+// (The general path takes 5 launches and a host-to-device copy.)
+__global__ void __launch_bounds__(1024) k_gram_sample(const double* __restrict__ C, const double* __restrict__ W,
+                                                      size_t count_cw, const double* __restrict__ D,
+                                                      const double* __restrict__ B, size_t count_db, double norm2,
+                                                      double* __restrict__ s, SampleRec* __restrict__ rec) {
+  __shared__ double w1[32], w2[32];
+  double a = 0.0, b = 0.0;
+  for (size_t e = threadIdx.x; e < count_cw; e += blockDim.x) a = fma(C[e], W[e], a);
+  for (size_t e = threadIdx.x; e < count_db; e += blockDim.x) b = fma(D[e], B[e], b);
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) w1[threadIdx.x >> 5] = a, w2[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s1 += w1[w], s2 += w2[w];
+    s[0] = norm2, s[1] = s1, s[2] = s2;
+    const double e2 = norm2 - 2.0 * s1 + s2;
+    rec->error = sqrt(e2 > 0.0 ? e2 : 0.0);
+    rec->t_ns = globaltimer();
+  }
+}
+
 // s[0] = ||M||^2 - 2 <C, W> + <D, B>, clamped at 0 (Gram identity)
 __global__ void k_gram_combine(double* s) {
   const double e2 = s[0] - 2.0 * s[1] + s[2];
