@@ -23,7 +23,7 @@ from typing import NamedTuple, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# MLNMF_B200_LIB: a kernel-variant build of the same library (tools/build_variant.sh)
+# MLNMF_B200_LIB: a kernel-variant build of the same library (tools/ab_variant.sh)
 LIB_PATH = os.environ.get("MLNMF_B200_LIB") or os.path.join(_HERE, "_lib", "libmlnmf_b200.so")
 
 if not os.path.exists(LIB_PATH):
