@@ -27,6 +27,7 @@
 #include "nccl_shim.hpp"
 #include "nnls.cuh"
 #include "ix_gemm.hpp"
+#include "restrict_tma.hpp"
 #include "transfer_ops.hpp"
 
 namespace mlb {
@@ -988,12 +989,18 @@ void Engine::ensure_levels(size_t L) {
     nx.dt = (cur.dt == 0 && impl_->tc && impl_->tc->wants(nx.m, n_loc_, 64)) ? 0 : 1;
     const size_t esn = nx.dt == 0 ? 4 : 8, esc = cur.dt == 0 ? 4 : 8;
     CK(dev_malloc(&nx.M, nx.m * n_loc_ * esn));
-    const size_t slab_smem = 3 * cur.h * 64;
     const int h = (int)cur.h, w = (int)cur.w, hc = (int)nx.h, wc = (int)nx.w;
-    // column slabs with the fine pixel columns staged once (k_restrict_slab;
-    // 64-byte slabs, 3-slot ring: 48 KB, 4 CTAs per SM -- measured best of
-    // {128, 64, 32} B x {3, 5 (prefetch)} slots and an L1-only variant,
-    // config-4 pyramid 77 ms with the gather -> 51 ms, r02), else the gather
+    // Narrow or unaligned matrices (the wide ones take restrict_tma.cu below):
+    // column slabs x coarse-row strips with the strip's fine pixel columns
+    // staged once by cp.async (k_restrict_slab), else the gather.  256-byte
+    // slabs (narrower while that leaves fewer than 8 slabs), 8-row strips,
+    // 5-slot ring: measured on the config-4 pyramid (r02: 60 ms for 64-byte
+    // slabs of whole pixel columns -> 40 ms; profiles/README.md).
+    int slabb = 256, strip = 8;
+    constexpr int ns = 5;
+    while (slabb > 64 && n_loc_ * esc < (size_t)slabb * 8) slabb /= 2;
+    if (strip > hc) strip = hc;
+    const size_t slab_smem = (size_t)ns * (2 * strip + 1) * slabb;
     auto restrict_to = [&](auto tin, auto tout, auto f64math) {
       using TI = decltype(tin);
       using TO = decltype(tout);
@@ -1001,20 +1008,37 @@ void Engine::ensure_levels(size_t L) {
       const TI* X = static_cast<const TI*>(cur.M);
       TO* Y = static_cast<TO*>(nx.M);
       if (slab_smem <= 200 * 1024) {
-        const unsigned g = (unsigned)ceil_div(n_loc_ * esc, 64);
-        if ((n_loc_ * esc) % 16 == 0)
-          impl_->launch(k_restrict_slab<TI, TO, 16 / sizeof(TI), F64>, dim3(g), dim3(256), slab_smem,
-                        (const int*)cur.Rp, (const int*)cur.Rc, (const double*)cur.Rw, X, Y, h, w, hc, wc, n_loc_);
-        else
-          impl_->launch(k_restrict_slab<TI, TO, 1, F64>, dim3(g), dim3(256), slab_smem, (const int*)cur.Rp,
-                        (const int*)cur.Rc, (const double*)cur.Rw, X, Y, h, w, hc, wc, n_loc_);
+        const dim3 g((unsigned)ceil_div(n_loc_ * esc, (size_t)slabb), (unsigned)ceil_div((size_t)hc, (size_t)strip));
+        auto go = [&](auto kern) {
+          impl_->launch(kern, g, dim3(256), slab_smem, (const int*)cur.Rp, (const int*)cur.Rc,
+                        (const double*)cur.Rw, X, Y, h, w, hc, wc, n_loc_, strip);
+        };
+        auto with = [&](auto sb, auto nsv) {
+          constexpr int SB = decltype(sb)::value, NSV = decltype(nsv)::value;
+          if ((n_loc_ * esc) % 16 == 0) go(k_restrict_slab<TI, TO, 16 / sizeof(TI), F64, SB, NSV>);
+          else go(k_restrict_slab<TI, TO, 1, F64, SB, NSV>);
+        };
+        auto with_ns = [&](auto sb) { with(sb, std::integral_constant<int, ns>()); };
+        if (slabb == 256) with_ns(std::integral_constant<int, 256>());
+        else if (slabb == 128) with_ns(std::integral_constant<int, 128>());
+        else with_ns(std::integral_constant<int, 64>());
       } else {
         const size_t colblocks = ceil_div(n_loc_, 256);
         impl_->launch(k_csr_apply<TI, TO>, dim3((unsigned)(nx.m * colblocks)), dim3(256), 0, (const int*)cur.Rp,
                       (const int*)cur.Ri, (const double*)cur.Rw, X, Y, nx.m, n_loc_, colblocks);
       }
     };
-    if (cur.dt == 1)
+    RestrictArgs ra{cur.M, nx.M, h, w, hc, wc, n_loc_,
+                    cur.dt == 1, cur.dt == 0 && nx.dt == 1, impl_->exact()};
+    // 8 coarse rows per CTA, 6-slot ring (52 KB, 4 CTAs per SM): level 0 of
+    // config 4 in 14.1 ms = 6.1 TB/s of algorithmic bytes (r02 sweep: rings
+    // of 4-5 or >= 8 slots and 4- or 32-row strips were 1.5-3x slower)
+    const int tma_strip = 8, tma_slots = 6;
+    if (restrict_tma_supported(ra)) {
+      // the TMA-pipelined stream (restrict_tma.cu): wide matrices
+      restrict_tma(ra, tma_strip, tma_slots, impl_->s);
+      ++launches_;
+    } else if (cur.dt == 1)
       restrict_to(double(), double(), std::true_type());
     else if (nx.dt == 1)
       restrict_to(float(), double(), std::true_type());

@@ -831,36 +831,45 @@ __global__ void k_csr_apply(const int* __restrict__ rowptr, const int* __restric
 // Y = R X for an h x w grid, X (h w rows) x ncols row-major.  The CSR entries
 // of R and their order are the reference's (k_csr_apply applies them as a
 // gather, re-reading every fine row up to four times).  Here a CTA owns a
-// 128-byte column slab and walks the coarse pixel columns cj in order,
-// keeping the three fine pixel columns 2cj - 1 .. 2cj + 1 in a shared-memory
-// ring (NS x h x SLABB bytes; NS = 5 prefetches the next two by cp.async while
-// cj is computed): every fine element is read from HBM once, every
-// coarse element written once.  Entry e is pre-decoded as code[e] = i * 4 +
-// (dj + 1) (fine row i within its pixel column, column offset dj).  Threads:
-// VEC columns each (one 16-byte vector; VEC = 1 when ncols is not a multiple
-// of 16 B), 128 / (VEC sizeof T) threads per pixel row.  F64MATH: the
-// reference's unfused fp64 sum in entry order (bit-identical to k_csr_apply);
-// otherwise fp32 FMA in the same order (fp32 storage, non-exact runs: within
-// an ulp of the fp64 result).
+// SLABB-byte column slab and a STRIP of `strip` coarse pixel rows
+// (blockIdx.y), and walks the coarse pixel columns cj in order, keeping the
+// strip's 2 strip + 1 fine pixel rows of the three fine pixel columns
+// 2cj - 1 .. 2cj + 1 in a shared-memory ring (NS x (2 strip + 1) x SLABB
+// bytes; NS = 5 prefetches the next two columns by cp.async while cj is
+// computed).  Every fine element is read from HBM once (plus one shared row
+// per strip boundary: 1 / (2 strip)), every coarse element written once, and
+// -- the point of the strips -- each fine row is fetched as one SLABB-byte
+// piece: strips keep the ring small enough for 256- and 512-byte pieces
+// (whole-column rings allowed 64 bytes, one DRAM burst pair per row).  Entry e
+// is pre-decoded as code[e] = i * 4 + (dj + 1) (fine row i within its pixel
+// column, column offset dj).  Threads: VEC columns each (one 16-byte vector;
+// VEC = 1 when ncols is not a multiple of 16 B), SLABB / 16 threads per pixel
+// row.  F64MATH: the reference's unfused fp64 sum in entry order
+// (bit-identical to k_csr_apply); otherwise fp32 FMA in the same order (fp32
+// storage, non-exact runs: within an ulp of the fp64 result).
 template <typename T, typename TO, int VEC, bool F64MATH, int SLABB = 64, int NS = 3>
 __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ rowptr, const int* __restrict__ code,
                                                        const double* __restrict__ wt, const T* __restrict__ X,
                                                        TO* __restrict__ Y, int h, int w, int hc, int wc,
-                                                       size_t ncols) {
+                                                       size_t ncols, int strip) {
   constexpr int SLAB = SLABB / (int)sizeof(T);  // columns per CTA
   constexpr int TPR = SLAB / VEC;               // threads per pixel row
   // NS ring slots: columns 2cj-1 .. 2cj+1 (+ the next two, prefetched, when NS = 5)
   extern __shared__ __align__(16) unsigned char smraw[];
-  T* ring = reinterpret_cast<T*>(smraw);  // [NS][h][SLAB]
+  T* ring = reinterpret_cast<T*>(smraw);  // [NS][2 strip + 1][SLAB]
   const int t = threadIdx.x, part = t % TPR, grp = t / TPR, ngrp = blockDim.x / TPR;
   const size_t c0 = (size_t)blockIdx.x * SLAB + (size_t)part * VEC;
   const int nact = c0 >= ncols ? 0 : (int)min((size_t)VEC, ncols - c0);
+  // the strip: coarse rows [ca, cb), fine rows [i0, i0 + hs)
+  const int ca = (int)blockIdx.y * strip, cb = min(ca + strip, hc);
+  const int i0 = max(2 * ca - 1, 0), hs = min(2 * (cb - 1) + 1, h - 1) - i0 + 1;
+  const size_t slot = (size_t)(2 * strip + 1) * SLAB;
   // fine pixel column j -> its ring slot: asynchronous 16-byte copies (or
   // plain loads on the unaligned path), committed as one group
   auto fetch = [&](int j) {
-    T* dst = ring + (size_t)(j % NS) * h * SLAB + part * VEC;
-    const T* src = X + (size_t)j * h * ncols + c0;
-    for (int i = grp; i < h; i += ngrp) {
+    T* dst = ring + (size_t)(j % NS) * slot + part * VEC;
+    const T* src = X + ((size_t)j * h + i0) * ncols + c0;
+    for (int i = grp; i < hs; i += ngrp) {
       if (VEC > 1 && nact == VEC) {
         const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + (size_t)i * SLAB);
         asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(sa), "l"(src + (size_t)i * ncols)
@@ -890,10 +899,11 @@ __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ r
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    // ring slot of fine column 2 cj + dj, dj = -1, 0, 1
-    const int sl[3] = {((2 * cj + NS - 1) % NS) * h * SLAB, ((2 * cj) % NS) * h * SLAB,
-                       ((2 * cj + 1) % NS) * h * SLAB};
-    for (int ci = grp; ci < hc; ci += ngrp) {
+    // ring slot of fine column 2 cj + dj, dj = -1, 0, 1 (rows relative to i0)
+    const T* sl[3] = {ring + (size_t)((2 * cj + NS - 1) % NS) * slot - (size_t)i0 * SLAB,
+                      ring + (size_t)((2 * cj) % NS) * slot - (size_t)i0 * SLAB,
+                      ring + (size_t)((2 * cj + 1) % NS) * slot - (size_t)i0 * SLAB};
+    for (int ci = ca + grp; ci < cb; ci += ngrp) {
       const size_t o = (size_t)cj * hc + ci;
       const int eb = rowptr[o], ee = rowptr[o + 1];
       double yd[VEC];
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ r
       for (int v = 0; v < VEC; ++v) yd[v] = 0.0, yf[v] = 0.f;
       for (int e = eb; e < ee; ++e) {
         const int cd = code[e];
-        const T* xs = ring + sl[cd & 3] + (size_t)(cd >> 2) * SLAB + part * VEC;
+        const T* xs = sl[cd & 3] + (size_t)(cd >> 2) * SLAB + part * VEC;
         T xv[VEC];
         if (VEC > 1) {
           *reinterpret_cast<uint4*>(xv) = *reinterpret_cast<const uint4*>(xs);
@@ -920,9 +930,19 @@ __global__ void __launch_bounds__(256) k_restrict_slab(const int* __restrict__ r
         }
       }
       TO* yo = Y + o * ncols + c0;
+      if (VEC > 1 && nact == VEC) {
+        // one vector store (ncols sizeof(T) % 16 == 0 aligns every row of Y)
+        struct alignas(sizeof(TO) * VEC) Pack {
+          TO v[VEC];
+        } pk;
 #pragma unroll
-      for (int v = 0; v < VEC; ++v)
-        if (v < nact) yo[v] = F64MATH ? to_t<TO>(yd[v]) : (TO)yf[v];
+        for (int v = 0; v < VEC; ++v) pk.v[v] = F64MATH ? to_t<TO>(yd[v]) : (TO)yf[v];
+        *reinterpret_cast<Pack*>(yo) = pk;
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (v < nact) yo[v] = F64MATH ? to_t<TO>(yd[v]) : (TO)yf[v];
+      }
     }
     __syncthreads();  // slots of columns 2cj - 1 and 2cj are refilled by the next prefetch
   }
