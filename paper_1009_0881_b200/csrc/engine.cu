@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -302,6 +303,12 @@ struct Engine::Impl {
     if (it == tc_ok.end()) throw std::logic_error("tensor-path decision missing for a level (decide_tc)");
     return it->second;
   }
+  // use_tc(l) where the decision exists (norm2 may precede factor setup)
+  bool use_tc_known(size_t l) const {
+    if (!tc || e->lv_[l].dt != 0) return false;
+    auto it = tc_ok.find({e->lv_[l].m, e->r_});
+    return it != tc_ok.end() && it->second;
+  }
   // at host-synchronous points (factor and level setup): local policy,
   // combined over ranks (any rank unable => nobody takes the tensor path)
   void decide_tc() {
@@ -324,11 +331,23 @@ struct Engine::Impl {
 
   // Row / column maxima of M_l (fixed-point scales of the tensor path),
   // computed once per level on first use.
-  const float* level_stats(size_t l) {
+  // With sq_out (a device double), the same pass also sums ||M_l||_F^2 into
+  // it (Engine::norm2 asks first on a tensor-path level: one pass over M_l
+  // instead of two).
+  const float* level_stats(size_t l, double* sq_out = nullptr) {
     auto& L = e->lv_[l];
     if (!L.mstat) {
       CK(dev_malloc(&L.mstat, (L.m + e->n_loc_) * 4));
-      tc->level_stats(static_cast<const float*>(L.M), L.m, e->n_loc_, L.mstat, L.mstat + L.m, s, &e->launches_);
+      double* part = nullptr;
+      size_t nb = 0;
+      if (sq_out) {
+        nb = tc->level_stats_blocks(L.m, e->n_loc_);
+        red.ensure(nb * 8);
+        part = red.as<double>();
+      }
+      tc->level_stats(static_cast<const float*>(L.M), L.m, e->n_loc_, L.mstat, L.mstat + L.m, part, s,
+                      &e->launches_);
+      if (sq_out) launch(k_sum_final, dim3(1), dim3(1024), 0, (const double*)part, nb, sq_out, 0);
     }
     return L.mstat;
   }
@@ -765,6 +784,10 @@ Engine::Engine(const Options& o) : opt_(o), impl_(new Impl(this)) {
   impl_->scal.ensure(16 * 8);
   impl_->tstart.ensure(8);
   impl_->tc = make_tc_gemm(o.dtype == 0 && o.gemm != 1, o.gemm == 2);
+  {
+    static std::once_flag once;  // per process: load the restriction kernels before any timed build
+    std::call_once(once, [] { restrict_tma_prepare(); });
+  }
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw std::invalid_argument("bad world / rank");
   if (o.has_nccl_id || (o.world > 1 && !o.host_allreduce)) {
     if (!o.has_nccl_id) throw std::invalid_argument("world > 1 needs an NCCL unique id (or a host allreduce)");
@@ -1057,7 +1080,8 @@ double Engine::norm2(size_t l) {
   Level& L = lv_.at(l);
   if (L.norm2 < 0) {
     double* sc = impl_->scal.as<double>();
-    if (L.dt == 0) impl_->dot<float>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
+    if (L.dt == 0 && !L.mstat && impl_->use_tc_known(l)) impl_->level_stats(l, sc + 4);  // fused with the tensor path's maxima
+    else if (L.dt == 0) impl_->dot<float>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
     else impl_->dot<double>(L.M, 1, nullptr, 0, L.m * n_loc_, sc + 4);
     impl_->allreduce_sum(sc + 4, 1);
     CK(cudaMemcpyAsync(&L.norm2, sc + 4, 8, cudaMemcpyDeviceToHost, impl_->s));

@@ -671,8 +671,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ----------------------------------------------------------------------------
 constexpr int kStatRows = 512;
 __global__ void __launch_bounds__(256) k_mstats(const float* __restrict__ M, size_t m, size_t n,
-                                                unsigned* __restrict__ rowmax, unsigned* __restrict__ colmax) {
+                                                unsigned* __restrict__ rowmax, unsigned* __restrict__ colmax,
+                                                double* __restrict__ sqpart) {
   __shared__ float part[kStatRows][8];
+  __shared__ double sqw[8];
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;  // the block's share of ||M||_F^2 (fp64, as k_sq_partial_v4)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const size_t j = (size_t)blockIdx.x * 1024 + (size_t)t * 4;
   const size_t i0 = (size_t)blockIdx.y * kStatRows;
@@ -684,6 +687,10 @@ __global__ void __launch_bounds__(256) k_mstats(const float* __restrict__ M, siz
       const float4 v = __ldcs(reinterpret_cast<const float4*>(M + (i0 + ii) * n + j));
       c0 = fmaxf(c0, v.x), c1 = fmaxf(c1, v.y), c2 = fmaxf(c2, v.z), c3 = fmaxf(c3, v.w);
       tm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+      if (sqpart) {
+        q0 = fma((double)v.x, (double)v.x, q0), q1 = fma((double)v.y, (double)v.y, q1);
+        q2 = fma((double)v.z, (double)v.z, q2), q3 = fma((double)v.w, (double)v.w, q3);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
@@ -701,6 +708,18 @@ __global__ void __launch_bounds__(256) k_mstats(const float* __restrict__ M, siz
 #pragma unroll
     for (int w = 1; w < 8; ++w) tm = fmaxf(tm, part[ii][w]);
     atomicMax(rowmax + i0 + ii, __float_as_uint(tm));
+  }
+  if (sqpart) {  // one partial per block, summed in block order by the caller (deterministic)
+    double q = (q0 + q1) + (q2 + q3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (lane == 0) sqw[warp] = q;
+    __syncthreads();
+    if (t == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < 8; ++w) tot += sqw[w];
+      sqpart[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    }
   }
 }
 
@@ -886,12 +905,14 @@ class IxGemm final : public TcGemm {
     return forced_ || m * n >= ((size_t)1 << 24);
   }
 
-  void level_stats(const float* M, size_t m, size_t n, float* rowmax, float* colmax, cudaStream_t s,
+  size_t level_stats_blocks(size_t m, size_t n) const override { return cdiv(n, 1024) * cdiv(m, ix::kStatRows); }
+  void level_stats(const float* M, size_t m, size_t n, float* rowmax, float* colmax, double* sqpart, cudaStream_t s,
                    long* launches) override {
     IX_CK(cudaMemsetAsync(rowmax, 0, m * 4, s));
     IX_CK(cudaMemsetAsync(colmax, 0, n * 4, s));
     dim3 g((unsigned)cdiv(n, 1024), (unsigned)cdiv(m, ix::kStatRows));
-    ix::k_mstats<<<g, 256, 0, s>>>(M, m, n, reinterpret_cast<unsigned*>(rowmax), reinterpret_cast<unsigned*>(colmax));
+    ix::k_mstats<<<g, 256, 0, s>>>(M, m, n, reinterpret_cast<unsigned*>(rowmax), reinterpret_cast<unsigned*>(colmax),
+                                   sqpart);
     IX_CK(cudaGetLastError());
     ++*launches;
   }

@@ -27,8 +27,11 @@ class TcGemm {
   // every row (m floats) and of every column (n floats).  They fix the
   // fixed-point scale of each MMA row: rows of M in A = M W^T, columns of M
   // in C = V^T M.
-  virtual void level_stats(const float* M, size_t m, size_t n, float* rowmax, float* colmax, cudaStream_t s,
-                           long* launches) = 0;
+  // sqpart (optional): level_stats_blocks(m, n) fp64 partial sums of squares,
+  // one per block, whose sum in index order is ||M||_F^2 (the same pass).
+  virtual size_t level_stats_blocks(size_t m, size_t n) const = 0;
+  virtual void level_stats(const float* M, size_t m, size_t n, float* rowmax, float* colmax, double* sqpart,
+                           cudaStream_t s, long* launches) = 0;
   // M fp32 (the streamed operand), factors fp64 (the engine's factor
   // storage; rounded once to the factor's fixed-point grid)
   virtual void mwt(const float* M, const float* rowmax, const double* W, size_t m, size_t n, size_t r, double* A,

@@ -16,6 +16,8 @@ struct RestrictArgs {
   bool f64math;        // fp32 -> fp32 in the reference's unfused fp64 arithmetic (exact mode)
 };
 
+// loads the kernels (call once per process, at session creation)
+void restrict_tma_prepare();
 // 16-byte aligned rows at least four 512-byte slabs wide
 bool restrict_tma_supported(const RestrictArgs& a);
 // strip: coarse pixel rows per CTA; nslots: ring depth in fine pixel columns
