@@ -244,6 +244,11 @@ int mlnmf_session_initialization_bound(mlnmf_session* s, size_t level, const voi
 int mlnmf_session_products(mlnmf_session* s, double* A, double* C);
 /* copy this rank's level-0 M (m x n_local) to a host buffer */
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
+/* copy this rank's level-`level` data R(...R(M)) (m_level x n_local; GridHierarchy::levels[level].data,
+ * transfer.hpp:60-70) to a host buffer of the level's storage type: *level_dtype (0 = fp32, 1 = fp64) is
+ * written first; with M_level == NULL only the type is reported.  Restricted levels of an fp32 session are
+ * fp32 where the tensor path streams them and fp64 otherwise. */
+int mlnmf_session_export_level(mlnmf_session* s, size_t level, void* M_level, int* level_dtype);
 int mlnmf_session_set_profiling(mlnmf_session* s, int on);
 int mlnmf_session_kernel_times(mlnmf_session* s, double* mwt_ms, long* mwt_n, double* vtm_ms, long* vtm_n);
 /* profiled time of the per-step NCCL allreduce of [M W^T | W W^T] (world > 1;

@@ -232,6 +232,7 @@ _proto("mlnmf_session_norm2", C.c_int, _vp, _sz, _dp)
 _proto("mlnmf_session_smoothness", C.c_int, _vp, _sz, _dp)
 _proto("mlnmf_session_initialization_bound", C.c_int, _vp, _sz, _vp, _vp, C.c_int, _sz, _dp, _dp)
 _proto("mlnmf_session_export_data", C.c_int, _vp, _vp, C.c_int)
+_proto("mlnmf_session_export_level", C.c_int, _vp, C.c_size_t, _vp, C.POINTER(C.c_int))
 _proto("mlnmf_session_products", C.c_int, _vp, _dp, _dp)
 _proto("mlnmf_session_set_profiling", C.c_int, _vp, C.c_int)
 _proto("mlnmf_session_kernel_times", C.c_int, _vp, _dp, _lp, _dp, _lp)
@@ -934,6 +935,15 @@ class Session:
             return M
         _check(_lib.mlnmf_session_export_data(self._h, ptr, self.dtype))
         return None
+
+    def export_level(self, level: int):
+        """This rank's level data R(...R(M)) (m_level x n_local) in the level's storage type."""
+        dt = C.c_int(0)
+        _check(_lib.mlnmf_session_export_level(self._h, level, None, C.byref(dt)))
+        g = self.level_grid(level)
+        M = np.zeros((g.pixels(), self.n_local), dtype=np.float32 if dt.value == F32 else np.float64)
+        _check(_lib.mlnmf_session_export_level(self._h, level, M.ctypes.data, C.byref(dt)))
+        return M
 
     def set_profiling(self, on: bool):
         _check(_lib.mlnmf_session_set_profiling(self._h, int(on)))

@@ -303,9 +303,12 @@ struct Engine::Impl {
     if (it == tc_ok.end()) throw std::logic_error("tensor-path decision missing for a level (decide_tc)");
     return it->second;
   }
-  // use_tc(l) where the decision exists (norm2 may precede factor setup)
+  // the level may take the tensor path (norm2 may precede factor setup, when
+  // the rank is not known yet: the maxima pass costs the same as the plain
+  // sum of squares, so it is taken whenever the shape allows the tensor path)
   bool use_tc_known(size_t l) const {
     if (!tc || e->lv_[l].dt != 0) return false;
+    if (e->r_ == 0) return tc->wants(e->lv_[l].m, e->n_loc_, 1);
     auto it = tc_ok.find({e->lv_[l].m, e->r_});
     return it != tc_ok.end() && it->second;
   }
@@ -1201,6 +1204,16 @@ void Engine::export_data(void* M_host, int host_dtype) {
   if (hs != es) throw std::invalid_argument("export_data: host dtype must match the storage dtype");
   CK(cudaMemcpyAsync(M_host, lv_[0].M, count * es, cudaMemcpyDeviceToHost, impl_->s));
   CK(cudaStreamSynchronize(impl_->s));
+}
+
+int Engine::export_level(size_t level, void* M_host) {
+  if (level >= lv_.size()) throw std::invalid_argument("level not built");
+  const Level& L = lv_[level];
+  if (M_host) {
+    CK(cudaMemcpyAsync(M_host, L.M, L.m * n_loc_ * (L.dt == 0 ? 4 : 8), cudaMemcpyDeviceToHost, impl_->s));
+    CK(cudaStreamSynchronize(impl_->s));
+  }
+  return L.dt;
 }
 
 void Engine::products(double* A, double* C) {
