@@ -69,25 +69,33 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled (every 20 ms) during the timed region: only the samples
+    whose timestamps fall between mark_start() and mark_end() are summarised (all of them if never marked)."""
 
     def __init__(self, index=0):
         self.index, self.proc = index, None
         self.path = f"/tmp/mlb_clocks_{os.getpid()}.csv"
+        self.t0 = self.t1 = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -98,20 +106,32 @@ class ClockSampler:
                 self.proc.kill()
             self.f.close()
 
+    @staticmethod
+    def _stamp(text):
+        import datetime
+        try:
+            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except Exception:
+            return None
+
     def summary(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         try:
             rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
         except Exception:
             return out
-        sm, mx, reasons, power = [], [], set(), []
+        sm, mx, reasons, power, total = [], [], set(), [], 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
-                sm.append(float(r[0]))
-                mx.append(float(r[1]))
-                power.append(float(r[2]))
-                for nm, v in zip(names, r[4:8]):
+                total += 1
+                ts = self._stamp(r[0])
+                if self.t0 is not None and self.t1 is not None and ts is not None and not (self.t0 <= ts <= self.t1):
+                    continue
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                power.append(float(r[3]))
+                for nm, v in zip(names, r[5:9]):
                     if v.strip().lower() == "active":
                         reasons.add(nm)
             except Exception:
@@ -119,6 +139,7 @@ class ClockSampler:
         if sm:
             out.update(sm_mhz=float(np.median(sm)), sm_max_mhz=float(max(mx)), samples=len(sm),
                        power_w_max=float(max(power)) if power else None)
+        out["samples_total"] = total
         out["reasons"] = sorted(reasons)
         return out
 
@@ -263,10 +284,12 @@ def run_b200(args):
     launches0 = s.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.mark_start()
         ev0.record(ext)
         s.steps("hals", args.steps)
         ev1.record(ext)
         ev1.synchronize()
+        clk.mark_end()
     ms = ev0.elapsed_time(ev1)
     launches = s.launches - launches0
     ms_max = allreduce_max(ms, world)
@@ -314,7 +337,7 @@ def run_b200(args):
         "data": "synthetic (BASELINE config-4 generator on the device, seed 0)",
         "config": {"workload": WORKLOAD, "global_batch": N_TOTAL, "seq_len": M_ROWS,
                    "parallelism": f"column-shard x{world}", "l2": "inputs larger than L2 (M = 64 GiB fp32)",
-                   "gemm_path": "tcgen05 kind::i8 digit products (fp32 operands as 23-bit fixed point, exact int32 accumulation)" if tc else "SIMT fp64-accumulate"},
+                   "gemm_path": "tcgen05 kind::i8 digit products (fp32 M and fp64 factors on per-row 31-bit fixed-point grids, four int8 digits each, exact int32 accumulation)" if tc else "SIMT fp64-accumulate"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -137,7 +137,11 @@ struct Engine::Impl {
     if (tc) mix(reinterpret_cast<const void*>(tc->signature()));
     return h;
   }
-  bool graphs_on = std::getenv("MLNMF_NO_GRAPHS") == nullptr;
+  // development switches, read once per engine (tests and tools/ set them before creating a session)
+  const bool graphs_on = std::getenv("MLNMF_NO_GRAPHS") == nullptr;
+  const bool env_exact_sweeps = std::getenv("MLNMF_EXACT_SWEEPS") != nullptr;
+  const bool env_thread_sweeps = std::getenv("MLNMF_THREAD_SWEEPS") != nullptr;
+  const bool env_warp_sweeps = std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
 
   explicit Impl(Engine* eng) : e(eng) {}
   ~Impl() {
@@ -239,7 +243,9 @@ struct Engine::Impl {
       part.ensure((size_t)spr * rows * ny * 8);
       dst = part.as<double>();
     }
-    auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, X, Y, rows, ny, K, kchunk, dst); };
+    auto go = [&](auto kern) {
+      launch(kern, g, dim3(256), 0, X, (const double*)nullptr, rows, Y, rows, ny, K, kchunk, dst);
+    };
     if (exact())
       tc == 32 ? go(k_gemm_abt<TX, TY, true, 32>) : tc == 48 ? go(k_gemm_abt<TX, TY, true, 48>)
                : go(k_gemm_abt<TX, TY, true, 64>);
@@ -266,7 +272,9 @@ struct Engine::Impl {
       part.ensure((size_t)spr * r * ncols * 8);
       dst = part.as<double>();
     }
-    auto go = [&](auto kern) { launch(kern, g, dim3(256), 0, V, X, K, r, ncols, kchunk, dst); };
+    auto go = [&](auto kern) {
+      launch(kern, g, dim3(256), 0, V, X, (const double*)nullptr, ncols, K, r, ncols, kchunk, dst);
+    };
     if (exact())
       tr == 32 ? go(k_gemm_atb<TV, TX, true, 32>) : tr == 48 ? go(k_gemm_atb<TV, TX, true, 48>)
                : go(k_gemm_atb<TV, TX, true, 64>);
@@ -277,6 +285,69 @@ struct Engine::Impl {
       const size_t cnt = r * ncols;
       reduce_splits(part.as<double>(), cnt, spr, out);
     }
+  }
+
+  // Stacked products of a half-iteration on the SIMT path (non-exact runs):
+  // [A; B] = [M_l; W] W^T in ONE launch + one split-K epilogue instead of two
+  // of each -- the small configurations are launch-bound (config 0: ten
+  // launches of a few microseconds per sweep).  Returns false (nothing
+  // launched) where the stacked product would not be split: the epilogue is
+  // what scatters the two results, and unsplit shapes gain nothing.
+  static constexpr size_t kStackedMaxK = 32768;
+  template <typename T>
+  bool stacked_ab(size_t l) {
+    const auto& L = e->lv_[l];
+    const size_t r = e->r_, rows = L.m + r, K = e->n_loc_;
+    const int tc = narrow_tile(r);
+    // K split as for A alone (the Gram's tile rides along: config 3 measured
+    // slower with the split chosen for the stacked tile count, r02)
+    const size_t tiles = ceil_div(L.m, GT) * ceil_div(r, (size_t)tc);
+    const int sp = splits_for(tiles, K);
+    const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
+    const int spr = (int)ceil_div(K, kchunk);
+    if (spr < 2 || K > kStackedMaxK) return false;
+    part.ensure((size_t)spr * rows * r * 8);
+    const dim3 g((unsigned)ceil_div(rows, GT), (unsigned)ceil_div(r, (size_t)tc), (unsigned)spr);
+    auto go = [&](auto kern) {
+      launch(kern, g, dim3(256), 0, static_cast<const T*>(L.M), (const double*)W.as<double>(), L.m,
+             (const double*)W.as<double>(), rows, r, K, kchunk, part.as<double>());
+    };
+    tc == 32 ? go(k_gemm_abt<T, double, false, 32>) : tc == 48 ? go(k_gemm_abt<T, double, false, 48>)
+             : go(k_gemm_abt<T, double, false, 64>);
+    reduce_splits2(rows * r, spr, r, L.m, 1, A(), B());
+    return true;
+  }
+  // [C | D] = V_l^T [M_l | V_l]
+  template <typename T>
+  bool stacked_cd(size_t l) {
+    const auto& L = e->lv_[l];
+    const size_t r = e->r_, ncols = e->n_loc_ + r, K = L.m;
+    const int tr = narrow_tile(r);
+    const size_t tiles = ceil_div(e->n_loc_, GT) * ceil_div(r, (size_t)tr);  // K split as for C alone
+    const int sp = splits_for(tiles, K);
+    const size_t kchunk = ceil_div(ceil_div(K, sp), GK) * GK;
+    const int spr = (int)ceil_div(K, kchunk);
+    // long contractions keep the two launches: config 3 (K = 77760, 348 K
+    // ranges) measured 60 us per step slower stacked (r02, same box)
+    if (spr < 2 || K > kStackedMaxK) return false;
+    part.ensure((size_t)spr * r * ncols * 8);
+    const dim3 g((unsigned)ceil_div(ncols, GT), (unsigned)ceil_div(r, (size_t)tr), (unsigned)spr);
+    auto go = [&](auto kern) {
+      launch(kern, g, dim3(256), 0, static_cast<const double*>(L.V), static_cast<const T*>(L.M),
+             static_cast<const double*>(L.V), e->n_loc_, K, r, ncols, kchunk, part.as<double>());
+    };
+    tr == 32 ? go(k_gemm_atb<double, T, false, 32>) : tr == 48 ? go(k_gemm_atb<double, T, false, 48>)
+             : go(k_gemm_atb<double, T, false, 64>);
+    reduce_splits2(r * ncols, spr, ncols, e->n_loc_, 0, Cb.as<double>(), Db.as<double>());
+    return true;
+  }
+  void reduce_splits2(size_t cnt, int spr, size_t rl, size_t cut, int by_row, double* out0, double* out1) {
+    if (spr >= 16 && cnt <= ((size_t)1 << 16))
+      launch(k_reduce_splits2_wide, dim3((unsigned)ceil_div(cnt, 32)), dim3(256), 0, (const double*)part.as<double>(),
+             cnt, spr, rl, cut, by_row, out0, out1);
+    else
+      launch(k_reduce_splits2, dim3((unsigned)std::min<size_t>(ceil_div(cnt, 256), 4096)), dim3(256), 0,
+             (const double*)part.as<double>(), cnt, spr, rl, cut, by_row, out0, out1);
   }
 
   // out[e] = sum over spr split partials (deterministic; wide form for many splits)
@@ -355,6 +426,20 @@ struct Engine::Impl {
     return L.mstat;
   }
 
+  // f() bracketed by CUDA events on the engine stream when profiling (the
+  // per-product times of kernel_times); the pair is kept only if f launched
+  template <typename F>
+  bool bracketed(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& into, F&& f) {
+    if (!e->profiling_) return f();
+    std::pair<cudaEvent_t, cudaEvent_t> evp{ev(), ev()};
+    CK(cudaEventRecord(evp.first, s));
+    const bool done = f();
+    CK(cudaEventRecord(evp.second, s));
+    if (done) into.push_back(evp);
+    else ev_pool.push_back(evp.first), ev_pool.push_back(evp.second);
+    return done;
+  }
+
   // A = M_l W^T (the first M pass), timed when profiling.
   template <typename T>
   void product_mwt(size_t l) {
@@ -415,11 +500,11 @@ struct Engine::Impl {
   // register sweeps at the config-4 rank: interleaved fused dot chains in
   // non-exact runs (MLNMF_EXACT_SWEEPS=1 keeps the reference order)
   bool fast_sweeps() const {
-    return e->opt_.dtype == 0 && !exact() && std::getenv("MLNMF_EXACT_SWEEPS") == nullptr;
+    return e->opt_.dtype == 0 && !exact() && !env_exact_sweeps;
   }
   bool warp_sweeps(size_t r, size_t count) const {
-    if (exact() || r > 64 || std::getenv("MLNMF_THREAD_SWEEPS") != nullptr) return false;
-    return count < kWarpSweepMax || std::getenv("MLNMF_WARP_SWEEPS") != nullptr;
+    if (exact() || r > 64 || env_thread_sweeps) return false;
+    return count < kWarpSweepMax || env_warp_sweeps;
   }
   // threads per block of the thread-per-row sweeps with the Gram and the
   // rows in shared memory; 0 when r is too large for that (r > ~160): the
@@ -443,8 +528,13 @@ struct Engine::Impl {
     int* deg = flags.as<int>();
     // ---- V half: A = M W^T, B = W W^T (solvers.cpp:82-83,105-106,251-252)
     const bool needB = !B_valid;
-    if (needB) timed(kPhB, [&] { gram_W<T>(); });
-    timed(kPhA, [&] { product_mwt<T>(l); });
+    // small SIMT shapes: A and B from one stacked launch (booked under phase A)
+    bool ab_done = false;
+    if (needB && !use_tc(l) && !exact()) timed(kPhA, [&] { ab_done = bracketed(ev_mwt, [&] { return stacked_ab<T>(l); }); });
+    if (!ab_done) {
+      if (needB) timed(kPhB, [&] { gram_W<T>(); });
+      timed(kPhA, [&] { product_mwt<T>(l); });
+    }
     if (multi()) {
       std::pair<cudaEvent_t, cudaEvent_t> evp{};
       if (e->profiling_) {
@@ -491,8 +581,12 @@ struct Engine::Impl {
       }
     });
     // ---- W half: C = V^T M, D = V^T V (solvers.cpp:91-92,124-125,272-273)
-    timed(kPhD, [&] { gram_V<T>(l); });
-    timed(kPhC, [&] { product_vtm<T>(l); });
+    bool cd_done = false;
+    if (!use_tc(l) && !exact()) timed(kPhC, [&] { cd_done = bracketed(ev_vtm, [&] { return stacked_cd<T>(l); }); });
+    if (!cd_done) {
+      timed(kPhD, [&] { gram_V<T>(l); });
+      timed(kPhC, [&] { product_vtm<T>(l); });
+    }
     timed(kPhW, [&] {
       double* Wp = W.as<double>();
       const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));

@@ -64,10 +64,13 @@ constexpr int GKS = 16;  // K step of the two-stage kernels (2 x 2 x 16 x 65 dou
 //   X: rows x K (row-major, ld = K), Y: ny x K (row-major, ld = K).
 //   (A = M W^T with X = M, Y = W; B = W W^T with X = Y = W.)
 // TC: the output tile's width along Y (32 / 48 / 64; ny = r is narrow)
+// Stacked form (one launch for A and B of a half-iteration): rows >= rows0
+// come from a second operand X1 (fp64, rows - rows0 rows of length K), so
+// X = M, X1 = Y = W gives [A; B] = [M; W] W^T.  rows0 = rows: X alone.
 template <typename TX, typename TY, bool EXACT, int TC = GT>
-__global__ void __launch_bounds__(256) k_gemm_abt(const TX* __restrict__ X, const TY* __restrict__ Y,
-                                                  size_t rows, size_t ny, size_t K, size_t kchunk,
-                                                  double* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_gemm_abt(const TX* __restrict__ X, const double* __restrict__ X1,
+                                                  size_t rows0, const TY* __restrict__ Y, size_t rows, size_t ny,
+                                                  size_t K, size_t kchunk, double* __restrict__ part) {
   // two stages: the next K step's operands are loaded into registers while
   // the current one is multiplied (one barrier per step; the single-stage
   // version exposed an L2 round trip per 32-wide K step)
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const TX* __restrict__ X, cons
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, rr = e / GKS, pp = e % GKS;
       const size_t p = p0 + pp, gi = i0 + rr;
-      rx[q] = (gi < rows && p < ke) ? (double)X[gi * K + p] : 0.0;
+      rx[q] = (gi < rows && p < ke) ? (gi < rows0 ? (double)X[gi * K + p] : X1[(gi - rows0) * K + p]) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < PQY; ++q) {
@@ -145,10 +148,13 @@ __global__ void __launch_bounds__(256) k_gemm_abt(const TX* __restrict__ X, cons
 //   V: K x r (row-major), X: K x ncols (row-major).
 //   (C = V^T M with X = M; D = V^T V with X = V, ncols = r.)
 // TR: the output tile's height along r (32 / 48 / 64)
+// Stacked form (one launch for C and D): columns >= ncols0 come from a second
+// operand X1 (fp64, K x (ncols - ncols0)), so X = M, X1 = V gives
+// [C | D] = V^T [M | V].  ncols0 = ncols: X alone.
 template <typename TV, typename TX, bool EXACT, int TR = GT>
 __global__ void __launch_bounds__(256) k_gemm_atb(const TV* __restrict__ V, const TX* __restrict__ X,
-                                                  size_t K, size_t r, size_t ncols, size_t kchunk,
-                                                  double* __restrict__ part) {
+                                                  const double* __restrict__ X1, size_t ncols0, size_t K, size_t r,
+                                                  size_t ncols, size_t kchunk, double* __restrict__ part) {
   constexpr int NA = TR / 16;            // outputs per thread along r
   __shared__ double Xs[2][GKS][GT + 1];  // two stages, as k_gemm_abt
   __shared__ double Vs[2][GKS][TR + 1];
@@ -169,7 +175,9 @@ __global__ void __launch_bounds__(256) k_gemm_atb(const TV* __restrict__ V, cons
     for (int q = 0; q < PQ; ++q) {
       const int e = tid + 256 * q, ii = e / GT, cc = e % GT;
       const size_t i = p0 + ii, gj = j0 + cc;
-      rx[q] = (i < ie && gj < ncols) ? (double)X[i * ncols + gj] : 0.0;
+      rx[q] = (i < ie && gj < ncols)
+                  ? (gj < ncols0 ? (double)X[i * ncols0 + gj] : X1[i * (ncols - ncols0) + (gj - ncols0)])
+                  : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < PQV; ++q) {
@@ -227,6 +235,45 @@ __global__ void k_reduce_splits(const double* __restrict__ part, size_t count, i
     double s = part[e];
     for (int z = 1; z < splits; ++z) s += part[(size_t)z * count + e];
     out[e] = s;
+  }
+}
+
+// The stacked products' epilogue: element e = row * rl + col of the stacked
+// partials goes to out0 or out1.  by_row: rows < cut form out0 (cut x rl),
+// the rest out1 ([A; B]); otherwise columns < cut form out0 (rows x cut),
+// the rest out1 (rows x (rl - cut)) ([C | D]).
+__device__ __forceinline__ double* stacked_dst(size_t e, size_t rl, size_t cut, int by_row, double* out0,
+                                               double* out1) {
+  if (by_row) return e < cut * rl ? out0 + e : out1 + (e - cut * rl);
+  const size_t row = e / rl, col = e - row * rl;
+  return col < cut ? out0 + row * cut + col : out1 + row * (rl - cut) + (col - cut);
+}
+// z ascending, as k_reduce_splits
+__global__ void k_reduce_splits2(const double* __restrict__ part, size_t count, int splits, size_t rl, size_t cut,
+                                 int by_row, double* __restrict__ out0, double* __restrict__ out1) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (size_t)gridDim.x * blockDim.x) {
+    double s = part[e];
+    for (int z = 1; z < splits; ++z) s += part[(size_t)z * count + e];
+    *stacked_dst(e, rl, cut, by_row, out0, out1) = s;
+  }
+}
+// 8 groups of splits per output, as k_reduce_splits_wide
+__global__ void __launch_bounds__(256) k_reduce_splits2_wide(const double* __restrict__ part, size_t count,
+                                                             int splits, size_t rl, size_t cut, int by_row,
+                                                             double* __restrict__ out0, double* __restrict__ out1) {
+  __shared__ double ps[8][33];
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const size_t e = (size_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < count)
+    for (int z = q; z < splits; z += 8) s += part[(size_t)z * count + e];
+  ps[q][lane] = s;
+  __syncthreads();
+  if (q == 0 && e < count) {
+    double t = ps[0][lane];
+    for (int g = 1; g < 8; ++g) t += ps[g][lane];
+    *stacked_dst(e, rl, cut, by_row, out0, out1) = t;
   }
 }
 
