@@ -242,6 +242,9 @@ int mlnmf_session_initialization_bound(mlnmf_session* s, size_t level, const voi
  * fp64 host buffers (either may be NULL).  Note: A is this rank's partial
  * (not allreduced). */
 int mlnmf_session_products(mlnmf_session* s, double* A, double* C);
+/* B = W W^T (r x r, fp64 host buffer) of this rank's W shard through the active implementation
+ * (kernels::matmul_abt with X = Y = W, kernels.cpp:24-34); not allreduced. */
+int mlnmf_session_gram_w(mlnmf_session* s, double* B);
 /* copy this rank's level-0 M (m x n_local) to a host buffer */
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
 /* copy this rank's level-`level` data R(...R(M)) (m_level x n_local; GridHierarchy::levels[level].data,

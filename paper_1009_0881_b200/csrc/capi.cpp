@@ -533,6 +533,10 @@ int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype) {
   return guard([&] { s->e->export_data(M_local, host_dtype); });
 }
 
+int mlnmf_session_gram_w(mlnmf_session* s, double* B) {
+  return guard([&] { s->e->gram_w(B); });
+}
+
 int mlnmf_session_export_level(mlnmf_session* s, size_t level, void* M_level, int* level_dtype) {
   return guard([&] {
     const int dt = s->e->export_level(level, M_level);

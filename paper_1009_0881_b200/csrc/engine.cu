@@ -28,6 +28,7 @@
 #include "nccl_shim.hpp"
 #include "nnls.cuh"
 #include "ix_gemm.hpp"
+#include "gram_dmma.hpp"
 #include "restrict_tma.hpp"
 #include "transfer_ops.hpp"
 
@@ -480,6 +481,15 @@ struct Engine::Impl {
   }
   template <typename T>
   void gram_W() {  // B = W W^T over all ranks
+    if (!exact() && gram_dmma_supported(e->r_, e->n_loc_)) {
+      // wide factor: fp64 tensor-core tiles, upper triangle only (gram_dmma.cu)
+      const int nb = gram_dmma_blocks(e->n_loc_, sm_count);
+      part.ensure((size_t)nb * e->r_ * e->r_ * 8);
+      gram_dmma(W.as<double>(), e->r_, e->n_loc_, sm_count, part.as<double>(), s);
+      ++e->launches_;
+      reduce_splits(part.as<double>(), e->r_ * e->r_, nb, B());
+      return;
+    }
     gemm_abt(W.as<double>(), W.as<double>(), e->r_, e->r_, e->n_loc_, B());
   }
   template <typename T>
@@ -1297,6 +1307,15 @@ void Engine::export_data(void* M_host, int host_dtype) {
   const size_t count = lv_[0].m * n_loc_, es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
   if (hs != es) throw std::invalid_argument("export_data: host dtype must match the storage dtype");
   CK(cudaMemcpyAsync(M_host, lv_[0].M, count * es, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+}
+
+void Engine::gram_w(double* B_host) {
+  if (lv_.empty() || r_ == 0) throw std::invalid_argument("gram_w: no data or factors");
+  if (opt_.dtype == 0) impl_->gram_W<float>();
+  else impl_->gram_W<double>();
+  impl_->B_valid = false;  // a rank-local value: the step's allreduced B is recomputed
+  CK(cudaMemcpyAsync(B_host, impl_->B(), r_ * r_ * 8, cudaMemcpyDeviceToHost, impl_->s));
   CK(cudaStreamSynchronize(impl_->s));
 }
 

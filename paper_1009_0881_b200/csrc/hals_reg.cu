@@ -21,22 +21,48 @@ __device__ __forceinline__ double to_t<double>(double v) { return v; }
 // reference: `s -= a * b` (solvers.cpp:118,136), unfused
 __device__ __forceinline__ double msub(double acc, double a, double b) { return __dsub_rn(acc, __dmul_rn(a, b)); }
 
+// FAST sweeps: kChains independent fused dot chains per update (the l-sum is
+// latency-bound at 12 warps per SM and 168 registers), summed pairwise.
+// Measured r02, W sweep at n = 262144: 4 chains + a per-thread reciprocal
+// 0.49-0.52 ms; 8 chains + per-block reciprocals 0.43-0.47 ms.  Not kept: the
+// Gram as constant-bank / uniform-register operand (LDCU.128 per pair: 0.56
+// ms), one 384-thread block per SM with a barrier per update against
+// instruction-fetch stalls (no_instructions is ncu's top stall reason on the
+// ~160 KB unrolled sweep: neutral for W, worse for V).
+constexpr int kChains = 8;
+__device__ __forceinline__ double chain_sum(const double (&p)[kChains]) {
+  double s[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s[c] = p[c];
+#pragma unroll
+  for (int w = kChains; w > 1; w /= 2)
+#pragma unroll
+    for (int c = 0; c < w / 2; ++c) s[c] = s[2 * c] + s[2 * c + 1];
+  return s[0];
+}
+
 // Register-resident HALS sweeps for a compile-time rank R (the config-4 rank):
 // the factor row / column lives in R registers instead of shared memory, the
 // Gram row for update k is read as broadcast from shared memory, and both k
 // and l loops are unrolled.  Same arithmetic and operation order as k_hals_v /
 // k_hals_w (the reference's, unfused), so results are bitwise identical;
 // ~10x fewer shared-memory accesses.
-// FAST (non-exact runs): the l-sum as four interleaved fused chains and the
+// FAST (non-exact runs): the l-sum as kChains interleaved fused chains and the
 // division by a per-block reciprocal -- the reference-order chain is 2R
 // dependent fp64 operations per update (~1000 cycles of latency at R = 64),
-// the interleaved one R / 4 fused ones.
+// the interleaved one R / kChains fused ones.
 template <typename T, int R, bool FAST = false>
 __global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A, const double* __restrict__ B,
                                                     T* __restrict__ V, size_t m, int* __restrict__ degenerate) {
   __shared__ double Bt[R * R];  // Bt[k][l] = B[l][k]: row k is the column the update reads
+  __shared__ double inv[R];     // FAST: reciprocal pivots, once per block (a per-thread fp64 division per k
+                                // was a quarter of the sweep's instructions, ncu r02)
   const int t = threadIdx.x;
   for (int e = t; e < R * R; e += blockDim.x) Bt[e] = B[(e % R) * R + e / R];
+  if (FAST && t < R) {
+    const double d = B[t * R + t];
+    inv[t] = d > 0.0 ? 1.0 / d : 0.0;
+  }
   __syncthreads();
   const size_t i = (size_t)blockIdx.x * blockDim.x + t;
   const bool act = i < m;
@@ -53,10 +79,12 @@ __global__ void __launch_bounds__(128) k_hals_v_reg(const double* __restrict__ A
     const double a = act ? A[i * R + k] : 0.0;
     double q;
     if (FAST) {
-      double p4[4] = {0.0, 0.0, 0.0, 0.0};
+      double p[kChains];
 #pragma unroll
-      for (int l = 0; l < R; ++l) p4[l & 3] = fma(v[l], Bt[k * R + l], p4[l & 3]);
-      q = (fma(v[k], bkk, a) - ((p4[0] + p4[1]) + (p4[2] + p4[3]))) * (1.0 / bkk);
+      for (int c = 0; c < kChains; ++c) p[c] = 0.0;
+#pragma unroll
+      for (int l = 0; l < R; ++l) p[l % kChains] = fma(v[l], Bt[k * R + l], p[l % kChains]);
+      q = (fma(v[k], bkk, a) - chain_sum(p)) * inv[k];
     } else {
       double num = __dadd_rn(a, __dmul_rn(v[k], bkk));
 #pragma unroll
@@ -74,8 +102,13 @@ template <typename T, int R, bool FAST = false>
 __global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ Cm, const double* __restrict__ D,
                                                     T* __restrict__ W, size_t n, int* __restrict__ degenerate) {
   __shared__ double Ds[R * R];
+  __shared__ double inv[R];  // FAST: reciprocal pivots, once per block
   const int t = threadIdx.x;
   for (int e = t; e < R * R; e += blockDim.x) Ds[e] = D[e];
+  if (FAST && t < R) {
+    const double d = D[t * R + t];
+    inv[t] = d > 0.0 ? 1.0 / d : 0.0;
+  }
   __syncthreads();
   const size_t j = (size_t)blockIdx.x * blockDim.x + t;
   const bool act = j < n;
@@ -92,10 +125,12 @@ __global__ void __launch_bounds__(128) k_hals_w_reg(const double* __restrict__ C
     const double c = act ? Cm[(size_t)k * n + j] : 0.0;
     double q;
     if (FAST) {
-      double p4[4] = {0.0, 0.0, 0.0, 0.0};
+      double p[kChains];
 #pragma unroll
-      for (int l = 0; l < R; ++l) p4[l & 3] = fma(Ds[k * R + l], w[l], p4[l & 3]);
-      q = (fma(dkk, w[k], c) - ((p4[0] + p4[1]) + (p4[2] + p4[3]))) * (1.0 / dkk);
+      for (int cc = 0; cc < kChains; ++cc) p[cc] = 0.0;
+#pragma unroll
+      for (int l = 0; l < R; ++l) p[l % kChains] = fma(Ds[k * R + l], w[l], p[l % kChains]);
+      q = (fma(dkk, w[k], c) - chain_sum(p)) * inv[k];
     } else {
       double num = __dadd_rn(c, __dmul_rn(dkk, w[k]));
 #pragma unroll

@@ -195,3 +195,22 @@ def test_fast_register_sweeps_match_reference_order(P, gpu, monkeypatch):
             out.append(s.get_factors())
     (V0, W0), (V1, W1) = out
     assert relnorm(V0, V1) < 1e-6 and relnorm(W0, W1) < 1e-6, (relnorm(V0, V1), relnorm(W0, W1))
+
+
+@pytest.mark.parametrize("r,n", [(64, 16384), (64, 4100), (49, 8192), (20, 2048), (7, 33002), (64, 2047)])
+def test_gram_w_dmma(P, gpu, r, n):
+    """B = W W^T of a wide factor on the fp64 tensor-core path (gram_dmma.cu: upper-triangle DMMA tiles,
+    mirrored; ragged ranks and K ranges, an odd K taking the scalar staging path; n < 2048 the SIMT tiles)
+    against fp64 numpy; exactly symmetric."""
+    rng = np.random.default_rng(r * 1000 + n)
+    m = 256
+    M = rng.random((m, n)).astype(np.float32)
+    V = rng.random((m, r))
+    W = rng.random((r, n)) * (rng.random((r, n)) > 0.3)  # NMF factors are sparse
+    with P.Session(dtype=P.F32) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V, W)
+        B = s.gram_w()
+    ref = W @ W.T
+    assert np.array_equal(B, B.T)
+    assert np.max(np.abs(B - ref)) <= 1e-13 * np.max(np.abs(ref)) * np.sqrt(n), np.max(np.abs(B - ref))
