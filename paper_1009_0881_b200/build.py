@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libmlnmf_b200.so")
 REPO = os.path.dirname(HERE)
 
-SOURCES = ["engine.cu", "ix_gemm.cu", "hals_reg.cu", "restrict_tma.cu", "gram_dmma.cu", "scheduler.cpp", "capi.cpp", "host_io.cpp"]
+SOURCES = ["engine.cu", "ix_gemm.cu", "hals_reg.cu", "restrict_tma.cu", "gram_dmma.cu", "hals_dmma.cu", "scheduler.cpp", "capi.cpp", "host_io.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CLI_SOURCES = ["cli_main.cpp"]  # dataset / result I/O from the library (host_io.cpp)
 CLI = os.path.join(OUT_DIR, "mlnmf_b200")  # the CLI executable (reference: tools/mlnmf_main.cpp)

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "hals_dmma.hpp"
 #include "hals_reg.hpp"
 #include "kernels.cuh"
 #include "nccl_shim.hpp"
@@ -604,6 +605,10 @@ struct Engine::Impl {
         launch(k_hals_w_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
                dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
                e->n_loc_, (int)r, deg);
+      } else if (kind == kHals && fast_sweeps() && hals_w_dmma_supported(r, e->n_loc_)) {
+        // wide factor, non-exact: updates in blocks of 8 on the fp64 tensor cores (hals_dmma.cu)
+        hals_w_dmma(Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
+        ++e->launches_;
       } else if (kind == kHals && hals_reg_supported(r)) {
         hals_w_reg(r, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
         ++e->launches_;

@@ -1,0 +1,147 @@
+// hals_dmma.cu -- the HALS W sweep at the config-4 rank (r = 64) for wide
+// factors, blocked onto the fp64 tensor-core path (hals_step's W half,
+// proj/src/solvers.cpp:124-141), non-exact runs only.
+//
+// Per column j of W the reference runs r sequential projected updates
+//     w_k <- max(0, (C_kj + D_kk w_k - sum_l D_kl w_l) / D_kk)
+//          = max(0, (C_kj - sum_{l != k} D_kl w_l) / D_kk),        k = 0 .. r-1
+// (Gauss-Seidel: w_l already updated for l < k).  The thread-per-column
+// register sweep (hals_reg.cu) issues r^2 = 4096 dependent-chain DFMAs and
+// half as many shared-memory loads per column and runs latency- and
+// instruction-fetch-bound: 0.45 ms per sweep at n = 262144 -- a fixed cost of
+// every step at every pyramid level.  Here the updates are taken in blocks of
+// 8: for block b the contributions of all l OUTSIDE the block,
+//     T_kj = C_kj - sum_{l not in block} D_kl w_l        (8 k x 8 columns x 56 l)
+// are 14 DMMAs (mma.sync m8n8k4 f64) per 8-column tile, and only the 8 x 8
+// inside of the block stays sequential.
+//
+// Layout.  The product is formed transposed, (8 columns x 4 l) . (4 l x 8 k):
+// the A fragment is the lane's own w registers (lane holds column lane / 4,
+// l = 4 q + lane % 4 for the 16 chunks q), the B fragment is -D from shared
+// memory, and the C fragment puts T_kj for column lane / 4 and k = 2 (lane % 4),
+// + 1 in the same QUAD of lanes that holds the column's w: the sequential
+// part of a block is two DFMAs, a quad reduction (two shuffles) and a select
+// per update, four column tiles interleaved.  A warp owns 32 columns (4
+// tiles), a lane 64 doubles of W -- as many registers as the thread-per-column
+// sweep, in ~8 k instructions per warp instead of ~10 k.
+//
+// Measured (r02, n = 262144, same box): 0.39-0.41 ms against 0.45-0.47 ms for
+// the register sweep.  ncu (profiles/README.md): 242 registers, 8 warps per
+// SM, stalls on the block's C loads (long scoreboard) and the fixed-latency
+// chain of the in-block updates; an up-front L2 prefetch of the warp's C
+// slice measured slower (0.42 ms) and is not kept.
+//
+// The accumulation order differs from the reference's (and from the FAST
+// register sweep's); exact mode and fp64 sessions never take this kernel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "hals_dmma.hpp"
+
+namespace mlb {
+namespace {
+
+constexpr int R = 64;
+constexpr int kLd = R + 4;  // padded -D row: a half-warp's 4 rows on distinct bank groups
+constexpr int kTiles = 4;   // 8-column tiles per warp
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_hals_w_dmma(const double* __restrict__ Cm, const double* __restrict__ D,
+                                                     double* __restrict__ W, size_t n, int* __restrict__ degenerate) {
+  __shared__ double nD[R * kLd];  // -D with a zero diagonal
+  __shared__ double inv[R];       // 1 / D_kk, 0 where D_kk <= 0 (the update is skipped, solvers.cpp:127)
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int e = t; e < R * R; e += blockDim.x) {
+    const int k = e / R, l = e % R;
+    nD[k * kLd + l] = k == l ? 0.0 : -D[e];
+  }
+  if (t < R) {
+    const double d = D[t * R + t];
+    inv[t] = d > 0.0 ? 1.0 / d : 0.0;
+    if (!(d > 0.0) && degenerate && blockIdx.x == 0) atomicAdd(degenerate, 1);
+  }
+  __syncthreads();
+  const int lr = lane >> 2, lc = lane & 3;  // column within a tile, l (and k pair) within a chunk
+  const size_t j0 = ((size_t)blockIdx.x * 4 + warp) * (8 * kTiles);
+  size_t col[kTiles];
+  bool act[kTiles];
+#pragma unroll
+  for (int ti = 0; ti < kTiles; ++ti) {
+    col[ti] = j0 + (size_t)ti * 8 + lr;
+    act[ti] = col[ti] < n;
+  }
+  // w[ti][q]: column col[ti], element l = 4 q + lc
+  double w[kTiles][16];
+#pragma unroll
+  for (int ti = 0; ti < kTiles; ++ti)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[ti][q] = act[ti] ? W[(size_t)(4 * q + lc) * n + col[ti]] : 0.0;
+
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    // T = C - sum over l outside the block: accumulators start at C (k = 8 b + 2 lc, + 1)
+    double acc[kTiles][2];
+#pragma unroll
+    for (int ti = 0; ti < kTiles; ++ti) {
+      acc[ti][0] = act[ti] ? Cm[(size_t)(8 * b + 2 * lc) * n + col[ti]] : 0.0;
+      acc[ti][1] = act[ti] ? Cm[(size_t)(8 * b + 2 * lc + 1) * n + col[ti]] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (q == 2 * b || q == 2 * b + 1) continue;
+      const double bf = nD[(8 * b + lr) * kLd + 4 * q + lc];  // B fragment: -D[k = 8 b + lane / 4][l = 4 q + lane % 4]
+#pragma unroll
+      for (int ti = 0; ti < kTiles; ++ti) dmma(acc[ti][0], acc[ti][1], w[ti][q], bf);
+    }
+    // the block's 8 sequential updates
+#pragma unroll
+    for (int kl = 0; kl < 8; ++kl) {
+      const int k = 8 * b + kl;
+      const double d0 = nD[k * kLd + 8 * b + lc], d1 = nD[k * kLd + 8 * b + 4 + lc];  // -D[k][the lane's two l]
+      const double ik = inv[k];
+      double tot[kTiles];
+#pragma unroll
+      for (int ti = 0; ti < kTiles; ++ti) {
+        double p = lc == kl / 2 ? acc[ti][kl & 1] : 0.0;  // the lane holding T_k contributes it
+        p = fma(d0, w[ti][2 * b], p);
+        p = fma(d1, w[ti][2 * b + 1], p);
+        p += __shfl_xor_sync(0xffffffffu, p, 1);
+        p += __shfl_xor_sync(0xffffffffu, p, 2);
+        tot[ti] = p;
+      }
+#pragma unroll
+      for (int ti = 0; ti < kTiles; ++ti) {
+        const double q = tot[ti] * ik;
+        const double wn = q > 0.0 ? q : 0.0;
+        // the lane holding w_k (l = k: chunk 2 b + kl / 4, lc = kl % 4) takes the new value
+        if (lc == (kl & 3) && ik != 0.0) w[ti][2 * b + kl / 4] = wn;
+      }
+    }
+  }
+#pragma unroll
+  for (int ti = 0; ti < kTiles; ++ti)
+    if (act[ti])
+#pragma unroll
+      for (int q = 0; q < 16; ++q) W[(size_t)(4 * q + lc) * n + col[ti]] = w[ti][q];
+}
+
+}  // namespace
+
+bool hals_w_dmma_supported(size_t r, size_t n) { return r == 64 && n >= 4096; }
+
+void hals_w_dmma(const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  k_hals_w_dmma<<<blocks, 128, 0, s>>>(C, D, W, n, deg);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_w_dmma)");
+}
+
+}  // namespace mlb

@@ -1,0 +1,11 @@
+// hals_dmma.hpp -- the blocked fp64 tensor-core HALS W sweep (hals_dmma.cu;
+// reference: hals_step, solvers.cpp:124-141), non-exact runs at r = 64.
+#pragma once
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace mlb {
+bool hals_w_dmma_supported(size_t r, size_t n);
+// W (64 x n, fp64) columns swept with C (64 x n) and D (64 x 64), fp64
+void hals_w_dmma(const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s);
+}  // namespace mlb
