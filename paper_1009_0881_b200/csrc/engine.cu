@@ -156,7 +156,9 @@ struct Engine::Impl {
 
   template <typename... KArgs, typename... Args>
   void launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args... args) {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // opt in from 32 KB: the 48 KB default counts the kernel's static shared memory too (r = 48 with
+    // fp32 data asked k_sqerr_tiled for exactly 48 KB of dynamic memory on top of its static arrays)
+    if (smem > 32 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<g, b, smem, s>>>(args...);
     ++e->launches_;
     CK(cudaGetLastError());

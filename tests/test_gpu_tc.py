@@ -214,3 +214,17 @@ def test_gram_w_dmma(P, gpu, r, n):
     ref = W @ W.T
     assert np.array_equal(B, B.T)
     assert np.max(np.abs(B - ref)) <= 1e-13 * np.max(np.abs(ref)) * np.sqrt(n), np.max(np.abs(B - ref))
+
+
+@pytest.mark.parametrize("r", [48, 33, 16, 1])
+def test_tensor_path_ranks(P, gpu, restated, r):
+    """Ranks other than the benchmarked 64 on the tensor path (r = 48: the direct residual asks for exactly
+    48 KB of dynamic shared memory), every sample within 1e-5 of the oracle fed the same fp32 data."""
+    M = oracle.generate_config(0, n=2048, restated=restated).astype(np.float32)
+    _, _, to = restated.run_configuration(M.astype(np.float64), 32, 32, 2, "hals", "fmg", r, 0, 8.0, 1)
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_TCGEN05) as s:
+        s.set_data(M, P.ImageGrid(32, 32))
+        t = s.run_configuration(2, "hals", "fmg", r, 0, 8.0, 1)
+        assert s.tc_active
+    assert len(t.error) == len(to.error)
+    assert np.max(np.abs(t.error - to.error) / to.error) < 1e-5

@@ -21,13 +21,14 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "auto"])
     ap.add_argument("--steps", type=int, default=0, help="also time full HALS steps")
+    ap.add_argument("--r", type=int, default=64, help="rank (the factor digit planes scale with it)")
     ap.add_argument("--residual", type=int, default=0, help="also time this many error samples (||M - VW||_F)")
     a = ap.parse_args()
     import paper_1009_0881_b200 as P
     gemm = {"tc": P.GEMM_TCGEN05, "simt": P.GEMM_SIMT, "auto": P.GEMM_AUTO}[a.gemm]
     with P.Session(dtype=P.F32, gemm_path=gemm) as s:
         s.generate(4, seed=0, n_total=a.n)
-        s.run_configuration(1, "hals", "none", 64, 0, 0.0, 0)  # random_init
+        s.run_configuration(1, "hals", "none", a.r, 0, 0.0, 0)  # random_init
         s.products()  # warm-up (buffer allocation)
         s.set_profiling(True)
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
