@@ -1,5 +1,5 @@
-// hals_dmma.cu -- the HALS W sweep at the config-4 rank (r = 64) for wide
-// factors, blocked onto the fp64 tensor-core path (hals_step's W half,
+// hals_dmma.cu -- the HALS sweeps at the config-4 rank (r = 64) for wide / tall
+// factors (written for W; the V half is the same kernel over V's layout), blocked onto the fp64 tensor-core path (hals_step's W half,
 // proj/src/solvers.cpp:124-141), non-exact runs only.
 //
 // Per column j of W the reference runs r sequential projected updates
@@ -54,14 +54,19 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128) k_hals_w_dmma(const double* __restrict__ Cm, const double* __restrict__ D,
-                                                     double* __restrict__ W, size_t n, int* __restrict__ degenerate) {
+// IS_W: the factor is W (64 x n, element (l, column j) at l n + j) with H = C (64 x n) and G = D;
+// otherwise V (m x 64 row-major: "column" = row i of V, element (l, i) at i 64 + l) with H = A (m x 64)
+// and G = B, whose entry for update k and term l is B[l][k] (the -G tile is stored transposed then).
+template <bool IS_W>
+__global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm, const double* __restrict__ D,
+                                                   double* __restrict__ W, size_t n, int* __restrict__ degenerate) {
+  auto at = [n](int l, size_t j) { return IS_W ? (size_t)l * n + j : j * (size_t)R + (size_t)l; };
   __shared__ double nD[R * kLd];  // -D with a zero diagonal
   __shared__ double inv[R];       // 1 / D_kk, 0 where D_kk <= 0 (the update is skipped, solvers.cpp:127)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int e = t; e < R * R; e += blockDim.x) {
     const int k = e / R, l = e % R;
-    nD[k * kLd + l] = k == l ? 0.0 : -D[e];
+    nD[(IS_W ? k * kLd + l : l * kLd + k)] = k == l ? 0.0 : -D[e];
   }
   if (t < R) {
     const double d = D[t * R + t];
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(128) k_hals_w_dmma(const double* __restrict__ 
 #pragma unroll
   for (int ti = 0; ti < kTiles; ++ti)
 #pragma unroll
-    for (int q = 0; q < 16; ++q) w[ti][q] = act[ti] ? W[(size_t)(4 * q + lc) * n + col[ti]] : 0.0;
+    for (int q = 0; q < 16; ++q) w[ti][q] = act[ti] ? W[at(4 * q + lc, col[ti])] : 0.0;
 
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
@@ -91,8 +96,8 @@ __global__ void __launch_bounds__(128) k_hals_w_dmma(const double* __restrict__ 
     double acc[kTiles][2];
 #pragma unroll
     for (int ti = 0; ti < kTiles; ++ti) {
-      acc[ti][0] = act[ti] ? Cm[(size_t)(8 * b + 2 * lc) * n + col[ti]] : 0.0;
-      acc[ti][1] = act[ti] ? Cm[(size_t)(8 * b + 2 * lc + 1) * n + col[ti]] : 0.0;
+      acc[ti][0] = act[ti] ? Cm[at(8 * b + 2 * lc, col[ti])] : 0.0;
+      acc[ti][1] = act[ti] ? Cm[at(8 * b + 2 * lc + 1, col[ti])] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -130,18 +135,26 @@ __global__ void __launch_bounds__(128) k_hals_w_dmma(const double* __restrict__ 
   for (int ti = 0; ti < kTiles; ++ti)
     if (act[ti])
 #pragma unroll
-      for (int q = 0; q < 16; ++q) W[(size_t)(4 * q + lc) * n + col[ti]] = w[ti][q];
+      for (int q = 0; q < 16; ++q) W[at(4 * q + lc, col[ti])] = w[ti][q];
 }
 
 }  // namespace
 
 bool hals_w_dmma_supported(size_t r, size_t n) { return r == 64 && n >= 4096; }
+bool hals_v_dmma_supported(size_t r, size_t m) { return r == 64 && m >= 4096; }
 
 void hals_w_dmma(const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
   const unsigned blocks = (unsigned)((n + 127) / 128);
-  k_hals_w_dmma<<<blocks, 128, 0, s>>>(C, D, W, n, deg);
+  k_hals_dmma<true><<<blocks, 128, 0, s>>>(C, D, W, n, deg);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_w_dmma)");
+}
+
+void hals_v_dmma(const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((m + 127) / 128);
+  k_hals_dmma<false><<<blocks, 128, 0, s>>>(A, B, V, m, deg);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_v_dmma)");
 }
 
 }  // namespace mlb
