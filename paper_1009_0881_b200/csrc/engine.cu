@@ -572,12 +572,12 @@ struct Engine::Impl {
     double* gv_ws = bd0 ? nullptr : gsweep_ws(std::max(L.m, e->n_loc_), bd, r);
     timed(kPhV, [&] {
       const dim3 gv((unsigned)ceil_div(L.m, bd));
-      if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
-        launch(k_hals_v_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
-               (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
-      } else if (kind == kHals && fast_sweeps() && hals_v_dmma_supported(r, L.m)) {
+      if (kind == kHals && fast_sweeps() && hals_v_dmma_supported(r, L.m)) {
         hals_v_dmma(A(), B(), V, L.m, deg, s);  // blocks of 8 updates on the fp64 tensor cores (hals_dmma.cu)
         ++e->launches_;
+      } else if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
+        launch(k_hals_v_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
+               (r * r + r) * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg);
       } else if (kind == kHals && hals_reg_supported(r)) {  // register-resident sweep, reference order
         hals_v_reg(r, fast_sweeps(), A(), B(), V, L.m, deg, s);
         ++e->launches_;

@@ -21,14 +21,13 @@
 // memory, and the C fragment puts T_kj for column lane / 4 and k = 2 (lane % 4),
 // + 1 in the same QUAD of lanes that holds the column's w: the sequential
 // part of a block is two DFMAs, a quad reduction (two shuffles) and a select
-// per update, four column tiles interleaved.  A warp owns 32 columns (4
-// tiles), a lane 64 doubles of W -- as many registers as the thread-per-column
-// sweep, in ~8 k instructions per warp instead of ~10 k.
+// per update, the warp's column tiles interleaved.  A warp owns 16 columns (2
+// tiles), a lane 32 doubles of W.
 //
-// Measured (r02, n = 262144, same box): 0.39-0.41 ms against 0.45-0.47 ms for
-// the register sweep.  ncu (profiles/README.md): 242 registers, 8 warps per
-// SM, stalls on the block's C loads (long scoreboard) and the fixed-latency
-// chain of the in-block updates; an up-front L2 prefetch of the warp's C
+// Measured (r02, n = 262144, same box): 0.28 ms against 0.45-0.47 ms for the
+// register sweep (0.39-0.41 ms with 4 tiles per warp: ncu, profiles/README.md,
+// showed 242 registers, 8 warps per SM, stalls on the block's C loads and the
+// fixed-latency chain of the in-block updates -- it is occupancy that pays); an up-front L2 prefetch of the warp's C
 // slice measured slower (0.42 ms) and is not kept.
 //
 // The accumulation order differs from the reference's (and from the FAST
@@ -46,7 +45,10 @@ namespace {
 
 constexpr int R = 64;
 constexpr int kLd = R + 4;  // padded -D row: a half-warp's 4 rows on distinct bank groups
-constexpr int kTiles = 4;   // 8-column tiles per warp
+// 8-column tiles per warp.  Measured r02 (W sweep, n = 262144, same box): 4 tiles (242 registers, 8 warps
+// per SM) 0.41 ms; 3 tiles 0.38; 2 tiles (135 registers, 12 warps) 0.28; 1 tile 0.29-0.32; forcing 4 or 6
+// blocks per SM through launch bounds 0.30-0.35.
+constexpr int kTiles = 2;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -141,17 +143,17 @@ __global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm
 }  // namespace
 
 bool hals_w_dmma_supported(size_t r, size_t n) { return r == 64 && n >= 4096; }
-bool hals_v_dmma_supported(size_t r, size_t m) { return r == 64 && m >= 4096; }
+bool hals_v_dmma_supported(size_t r, size_t m) { return r == 64 && m >= 256; }
 
 void hals_w_dmma(const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((n + 127) / 128);
+  const unsigned blocks = (unsigned)((n + 32 * kTiles - 1) / (32 * kTiles));
   k_hals_dmma<true><<<blocks, 128, 0, s>>>(C, D, W, n, deg);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_w_dmma)");
 }
 
 void hals_v_dmma(const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((m + 127) / 128);
+  const unsigned blocks = (unsigned)((m + 32 * kTiles - 1) / (32 * kTiles));
   k_hals_dmma<false><<<blocks, 128, 0, s>>>(A, B, V, m, deg);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_v_dmma)");
