@@ -573,7 +573,7 @@ struct Engine::Impl {
     timed(kPhV, [&] {
       const dim3 gv((unsigned)ceil_div(L.m, bd));
       if (kind == kHals && fast_sweeps() && hals_v_dmma_supported(r, L.m)) {
-        hals_v_dmma(A(), B(), V, L.m, deg, s);  // blocks of 8 updates on the fp64 tensor cores (hals_dmma.cu)
+        hals_v_dmma(r, A(), B(), V, L.m, deg, s);  // blocks of 8 updates on the fp64 tensor cores (hals_dmma.cu)
         ++e->launches_;
       } else if (kind == kHals && warp_sweeps(r, L.m)) {  // warp per row (non-exact, few rows)
         launch(k_hals_v_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)), dim3(256),
@@ -612,7 +612,7 @@ struct Engine::Impl {
                e->n_loc_, (int)r, deg);
       } else if (kind == kHals && fast_sweeps() && hals_w_dmma_supported(r, e->n_loc_)) {
         // wide factor, non-exact: updates in blocks of 8 on the fp64 tensor cores (hals_dmma.cu)
-        hals_w_dmma(Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
+        hals_w_dmma(r, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
         ++e->launches_;
       } else if (kind == kHals && hals_reg_supported(r)) {
         hals_w_reg(r, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);

@@ -61,19 +61,21 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // and G = B, whose entry for update k and term l is B[l][k] (the -G tile is stored transposed then).
 template <bool IS_W>
 __global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm, const double* __restrict__ D,
-                                                   double* __restrict__ W, size_t n, int* __restrict__ degenerate) {
-  auto at = [n](int l, size_t j) { return IS_W ? (size_t)l * n + j : j * (size_t)R + (size_t)l; };
+                                                   double* __restrict__ W, size_t n, int r,
+                                                   int* __restrict__ degenerate) {
+  // r <= 64: the factor's rows r .. 63 are zero padding (never loaded or stored; their updates are skipped)
+  auto at = [n, r](int l, size_t j) { return IS_W ? (size_t)l * n + j : j * (size_t)r + (size_t)l; };
   __shared__ double nD[R * kLd];  // -D with a zero diagonal
   __shared__ double inv[R];       // 1 / D_kk, 0 where D_kk <= 0 (the update is skipped, solvers.cpp:127)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int e = t; e < R * R; e += blockDim.x) {
     const int k = e / R, l = e % R;
-    nD[(IS_W ? k * kLd + l : l * kLd + k)] = k == l ? 0.0 : -D[e];
+    nD[(IS_W ? k * kLd + l : l * kLd + k)] = (k == l || k >= r || l >= r) ? 0.0 : -D[k * r + l];
   }
   if (t < R) {
-    const double d = D[t * R + t];
+    const double d = t < r ? D[t * r + t] : 0.0;
     inv[t] = d > 0.0 ? 1.0 / d : 0.0;
-    if (!(d > 0.0) && degenerate && blockIdx.x == 0) atomicAdd(degenerate, 1);
+    if (t < r && !(d > 0.0) && degenerate && blockIdx.x == 0) atomicAdd(degenerate, 1);
   }
   __syncthreads();
   const int lr = lane >> 2, lc = lane & 3;  // column within a tile, l (and k pair) within a chunk
@@ -90,20 +92,22 @@ __global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm
 #pragma unroll
   for (int ti = 0; ti < kTiles; ++ti)
 #pragma unroll
-    for (int q = 0; q < 16; ++q) w[ti][q] = act[ti] ? W[at(4 * q + lc, col[ti])] : 0.0;
+    for (int q = 0; q < 16; ++q) w[ti][q] = (act[ti] && 4 * q + lc < r) ? W[at(4 * q + lc, col[ti])] : 0.0;
 
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
+    if (8 * b >= r) break;  // padding blocks (warp-uniform)
     // T = C - sum over l outside the block: accumulators start at C (k = 8 b + 2 lc, + 1)
     double acc[kTiles][2];
 #pragma unroll
     for (int ti = 0; ti < kTiles; ++ti) {
-      acc[ti][0] = act[ti] ? Cm[at(8 * b + 2 * lc, col[ti])] : 0.0;
-      acc[ti][1] = act[ti] ? Cm[at(8 * b + 2 * lc + 1, col[ti])] : 0.0;
+      acc[ti][0] = (act[ti] && 8 * b + 2 * lc < r) ? Cm[at(8 * b + 2 * lc, col[ti])] : 0.0;
+      acc[ti][1] = (act[ti] && 8 * b + 2 * lc + 1 < r) ? Cm[at(8 * b + 2 * lc + 1, col[ti])] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       if (q == 2 * b || q == 2 * b + 1) continue;
+      if (4 * q >= r) continue;  // all-zero padding chunk (warp-uniform)
       const double bf = nD[(8 * b + lr) * kLd + 4 * q + lc];  // B fragment: -D[k = 8 b + lane / 4][l = 4 q + lane % 4]
 #pragma unroll
       for (int ti = 0; ti < kTiles; ++ti) dmma(acc[ti][0], acc[ti][1], w[ti][q], bf);
@@ -137,24 +141,27 @@ __global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm
   for (int ti = 0; ti < kTiles; ++ti)
     if (act[ti])
 #pragma unroll
-      for (int q = 0; q < 16; ++q) W[at(4 * q + lc, col[ti])] = w[ti][q];
+      for (int q = 0; q < 16; ++q)
+        if (4 * q + lc < r) W[at(4 * q + lc, col[ti])] = w[ti][q];
 }
 
 }  // namespace
 
-bool hals_w_dmma_supported(size_t r, size_t n) { return r == 64 && n >= 4096; }
-bool hals_v_dmma_supported(size_t r, size_t m) { return r == 64 && m >= 256; }
+// r = 64 from a few hundred rows / columns; smaller ranks (zero-padded to 64: config 3's r = 49 spends a
+// quarter of the tensor work on padding) where the factor is long enough to pay for it
+bool hals_w_dmma_supported(size_t r, size_t n) { return r >= 8 && r <= 64 && n >= 4096; }
+bool hals_v_dmma_supported(size_t r, size_t m) { return r >= 8 && r <= 64 && ((r == 64 && m >= 256) || m >= 4096); }
 
-void hals_w_dmma(const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
+void hals_w_dmma(size_t r, const double* C, const double* D, double* W, size_t n, int* deg, cudaStream_t s) {
   const unsigned blocks = (unsigned)((n + 32 * kTiles - 1) / (32 * kTiles));
-  k_hals_dmma<true><<<blocks, 128, 0, s>>>(C, D, W, n, deg);
+  k_hals_dmma<true><<<blocks, 128, 0, s>>>(C, D, W, n, (int)r, deg);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_w_dmma)");
 }
 
-void hals_v_dmma(const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s) {
+void hals_v_dmma(size_t r, const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s) {
   const unsigned blocks = (unsigned)((m + 32 * kTiles - 1) / (32 * kTiles));
-  k_hals_dmma<false><<<blocks, 128, 0, s>>>(A, B, V, m, deg);
+  k_hals_dmma<false><<<blocks, 128, 0, s>>>(A, B, V, m, (int)r, deg);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_v_dmma)");
 }
