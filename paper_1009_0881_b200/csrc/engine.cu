@@ -583,6 +583,9 @@ struct Engine::Impl {
         ++e->launches_;
       } else if (kind == kHals) {
         launch(k_hals_v<double>, gv, dim3(bd), smem, (const double*)A(), (const double*)B(), V, L.m, (int)r, deg, gv_ws);
+      } else if (kind == kMu && fast_sweeps() && mu_dmma_supported(r, L.m)) {
+        mu_v_dmma(r, A(), B(), V, L.m, s);  // (V B) on the fp64 tensor cores (hals_dmma.cu)
+        ++e->launches_;
       } else if (kind == kMu && warp_sweeps(r, L.m)) {
         launch(k_mu_warp<double, false>, dim3((unsigned)std::min<size_t>(ceil_div(L.m, 8), (size_t)sm_count * 4)),
                dim3(256), r * r * 8, (const double*)A(), (const double*)B(), V, L.m, (int)r);
@@ -606,20 +609,23 @@ struct Engine::Impl {
     timed(kPhW, [&] {
       double* Wp = W.as<double>();
       const dim3 gw((unsigned)ceil_div(e->n_loc_, bd));
-      if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
-        launch(k_hals_w_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
-               dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
-               e->n_loc_, (int)r, deg);
-      } else if (kind == kHals && fast_sweeps() && hals_w_dmma_supported(r, e->n_loc_)) {
+      if (kind == kHals && fast_sweeps() && hals_w_dmma_supported(r, e->n_loc_)) {
         // wide factor, non-exact: updates in blocks of 8 on the fp64 tensor cores (hals_dmma.cu)
         hals_w_dmma(r, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
         ++e->launches_;
+      } else if (kind == kHals && warp_sweeps(r, e->n_loc_)) {
+        launch(k_hals_w_warp<double>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
+               dim3(256), (r * r + r) * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
+               e->n_loc_, (int)r, deg);
       } else if (kind == kHals && hals_reg_supported(r)) {
         hals_w_reg(r, fast_sweeps(), Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, deg, s);
         ++e->launches_;
       } else if (kind == kHals) {
         launch(k_hals_w<double>, gw, dim3(bd), smem, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp,
                e->n_loc_, (int)r, deg, gv_ws);
+      } else if (kind == kMu && fast_sweeps() && mu_dmma_supported(r, e->n_loc_)) {
+        mu_w_dmma(r, Cb.as<double>(), Db.as<double>(), Wp, e->n_loc_, s);
+        ++e->launches_;
       } else if (kind == kMu && warp_sweeps(r, e->n_loc_)) {
         launch(k_mu_warp<double, true>, dim3((unsigned)std::min<size_t>(ceil_div(e->n_loc_, 8), (size_t)sm_count * 4)),
                dim3(256), r * r * 8, (const double*)Cb.as<double>(), (const double*)Db.as<double>(), Wp, e->n_loc_,

@@ -145,6 +145,67 @@ __global__ void __launch_bounds__(128) k_hals_dmma(const double* __restrict__ Cm
         if (4 * q + lc < r) W[at(4 * q + lc, col[ti])] = w[ti][q];
 }
 
+// MU (mu_step, solvers.cpp:79-99) through the same tiles: the update
+//     f_k <- f_k H_k / max((G f)_k, 1e-16)        (Jacobi: the old f throughout)
+// has no sequential part at all -- (G f) for the warp's 16 columns is 16 x 8 DMMAs, and the quad
+// shuffles bring each sum to the lane that holds f_k.  IS_W as above (W against D, V against B).
+template <bool IS_W>
+__global__ void __launch_bounds__(128) k_mu_dmma(const double* __restrict__ H, const double* __restrict__ G,
+                                                 double* __restrict__ F, size_t n, int r) {
+  __shared__ double Gs[R * kLd];  // Gs[k][l] = the Gram entry of output k and term l
+  auto at = [n, r](int l, size_t j) { return IS_W ? (size_t)l * n + j : j * (size_t)r + (size_t)l; };
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int e = t; e < R * R; e += blockDim.x) {
+    const int k = e / R, l = e % R;
+    Gs[k * kLd + l] = (k >= r || l >= r) ? 0.0 : (IS_W ? G[k * r + l] : G[l * r + k]);
+  }
+  __syncthreads();
+  const int lr = lane >> 2, lc = lane & 3;
+  const size_t j0 = ((size_t)blockIdx.x * 4 + warp) * (8 * kTiles);
+  size_t col[kTiles];
+  bool act[kTiles];
+#pragma unroll
+  for (int ti = 0; ti < kTiles; ++ti) {
+    col[ti] = j0 + (size_t)ti * 8 + lr;
+    act[ti] = col[ti] < n;
+  }
+  double w[kTiles][16];
+#pragma unroll
+  for (int ti = 0; ti < kTiles; ++ti)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[ti][q] = (act[ti] && 4 * q + lc < r) ? F[at(4 * q + lc, col[ti])] : 0.0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (8 * b >= r) break;
+    double acc[kTiles][2];
+#pragma unroll
+    for (int ti = 0; ti < kTiles; ++ti) acc[ti][0] = acc[ti][1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (4 * q >= r) continue;
+      const double bf = Gs[(8 * b + lr) * kLd + 4 * q + lc];
+#pragma unroll
+      for (int ti = 0; ti < kTiles; ++ti) dmma(acc[ti][0], acc[ti][1], w[ti][q], bf);
+    }
+    // the lane's two elements of the block: k = 8 b + 4 h + lc, h = 0, 1; their sums sit in quad lane
+    // 2 h + lc / 2, register lc % 2
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int src = (lane & ~3) | (2 * h + (lc >> 1));
+      const int k = 8 * b + 4 * h + lc;
+#pragma unroll
+      for (int ti = 0; ti < kTiles; ++ti) {
+        const double s0 = __shfl_sync(0xffffffffu, acc[ti][0], src), s1 = __shfl_sync(0xffffffffu, acc[ti][1], src);
+        const double sk = (lc & 1) ? s1 : s0;
+        if (act[ti] && k < r) {
+          const size_t a = at(k, col[ti]);
+          F[a] = w[ti][2 * b + h] * (H[a] / (sk < 1e-16 ? 1e-16 : sk));
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // r = 64 from a few hundred rows / columns; smaller ranks (zero-padded to 64: config 3's r = 49 spends a
@@ -166,4 +227,18 @@ void hals_v_dmma(size_t r, const double* A, const double* B, double* V, size_t m
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (hals_v_dmma)");
 }
 
+}  // namespace mlb
+
+namespace mlb {
+bool mu_dmma_supported(size_t r, size_t count) { return r >= 8 && r <= 64 && count >= 4096; }
+void mu_v_dmma(size_t r, const double* A, const double* B, double* V, size_t m, cudaStream_t s) {
+  k_mu_dmma<false><<<(unsigned)((m + 32 * kTiles - 1) / (32 * kTiles)), 128, 0, s>>>(A, B, V, m, (int)r);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (mu_v_dmma)");
+}
+void mu_w_dmma(size_t r, const double* C, const double* D, double* W, size_t n, cudaStream_t s) {
+  k_mu_dmma<true><<<(unsigned)((n + 32 * kTiles - 1) / (32 * kTiles)), 128, 0, s>>>(C, D, W, n, (int)r);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (mu_w_dmma)");
+}
 }  // namespace mlb

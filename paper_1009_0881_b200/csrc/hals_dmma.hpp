@@ -11,4 +11,8 @@ void hals_w_dmma(size_t r, const double* C, const double* D, double* W, size_t n
 // V (m x r row-major, fp64) rows swept with A (m x r) and B (r x r): hals_step's V half (solvers.cpp:105-122)
 bool hals_v_dmma_supported(size_t r, size_t m);
 void hals_v_dmma(size_t r, const double* A, const double* B, double* V, size_t m, int* deg, cudaStream_t s);
+// MU updates (mu_step, solvers.cpp:79-99) of long factors on the same tiles, non-exact runs
+bool mu_dmma_supported(size_t r, size_t count);
+void mu_v_dmma(size_t r, const double* A, const double* B, double* V, size_t m, cudaStream_t s);
+void mu_w_dmma(size_t r, const double* C, const double* D, double* W, size_t n, cudaStream_t s);
 }  // namespace mlb
