@@ -228,3 +228,24 @@ def test_tensor_path_ranks(P, gpu, restated, r):
         assert s.tc_active
     assert len(t.error) == len(to.error)
     assert np.max(np.abs(t.error - to.error) / to.error) < 1e-5
+
+
+@pytest.mark.parametrize("kind", ["hals", "mu"])
+@pytest.mark.parametrize("r,m,n", [(64, 4224, 4100), (49, 4100, 4228), (12, 8192, 4096), (64, 260, 4100)])
+def test_dmma_sweeps_against_oracle(P, gpu, restated, kind, r, m, n):
+    """One HALS / MU step of an fp32 non-exact session whose sweeps run on the fp64 tensor cores
+    (hals_dmma.cu: blocked HALS sweeps, MU products; ranks below 64 zero-padded, ragged last warps) with
+    fp64-accumulated SIMT products, against the oracle's step on the same fp32 data: the sweeps only reorder
+    fp64 sums."""
+    rng = np.random.default_rng(m + n + r)
+    M = rng.random((m, n)).astype(np.float32)
+    V0 = rng.random((m, r))
+    W0 = rng.random((r, n)) * (rng.random((r, n)) > 0.25)
+    step = restated.hals_step if kind == "hals" else restated.mu_step
+    Vo, Wo = step(M.astype(np.float64), V0, W0)[:2]
+    with P.Session(dtype=P.F32, gemm_path=P.GEMM_SIMT) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V0, W0)
+        s.steps(kind, 1)
+        V, W = s.get_factors()
+    assert relnorm(V, Vo) < 1e-11 and relnorm(W, Wo) < 1e-11, (relnorm(V, Vo), relnorm(W, Wo))
