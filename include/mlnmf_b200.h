@@ -245,6 +245,9 @@ int mlnmf_session_products(mlnmf_session* s, double* A, double* C);
 /* B = W W^T (r x r, fp64 host buffer) of this rank's W shard through the active implementation
  * (kernels::matmul_abt with X = Y = W, kernels.cpp:24-34); not allreduced. */
 int mlnmf_session_gram_w(mlnmf_session* s, double* B);
+/* D = V^T V (r x r, fp64 host buffer) of the level-0 V through the active implementation
+ * (kernels::matmul_atb with X = V, kernels.cpp:36-46). */
+int mlnmf_session_gram_v(mlnmf_session* s, double* D);
 /* copy this rank's level-0 M (m x n_local) to a host buffer */
 int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype);
 /* copy this rank's level-`level` data R(...R(M)) (m_level x n_local; GridHierarchy::levels[level].data,

@@ -232,6 +232,7 @@ _proto("mlnmf_session_norm2", C.c_int, _vp, _sz, _dp)
 _proto("mlnmf_session_smoothness", C.c_int, _vp, _sz, _dp)
 _proto("mlnmf_session_initialization_bound", C.c_int, _vp, _sz, _vp, _vp, C.c_int, _sz, _dp, _dp)
 _proto("mlnmf_session_gram_w", C.c_int, _vp, _vp)
+_proto("mlnmf_session_gram_v", C.c_int, _vp, _vp)
 _proto("mlnmf_session_export_data", C.c_int, _vp, _vp, C.c_int)
 _proto("mlnmf_session_export_level", C.c_int, _vp, C.c_size_t, _vp, C.POINTER(C.c_int))
 _proto("mlnmf_session_products", C.c_int, _vp, _dp, _dp)
@@ -927,6 +928,12 @@ class Session:
         Cm = np.zeros((self.r, self.n_local))
         _check(_lib.mlnmf_session_products(self._h, _d(A), _d(Cm)))
         return A, Cm
+
+    def gram_v(self):
+        """D = V^T V of the level-0 V through the active kernel."""
+        D = np.zeros((self.r, self.r))
+        _check(_lib.mlnmf_session_gram_v(self._h, _d(D)))
+        return D
 
     def gram_w(self):
         """B = W W^T of this rank's W shard through the active kernel (not allreduced)."""

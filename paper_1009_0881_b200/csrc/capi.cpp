@@ -533,6 +533,10 @@ int mlnmf_session_export_data(mlnmf_session* s, void* M_local, int host_dtype) {
   return guard([&] { s->e->export_data(M_local, host_dtype); });
 }
 
+int mlnmf_session_gram_v(mlnmf_session* s, double* D) {
+  return guard([&] { s->e->gram_v(D); });
+}
+
 int mlnmf_session_gram_w(mlnmf_session* s, double* B) {
   return guard([&] { s->e->gram_w(B); });
 }

@@ -498,6 +498,14 @@ struct Engine::Impl {
   template <typename T>
   void gram_V(size_t l) {  // D = V_l^T V_l (replicated)
     const auto& L = e->lv_[l];
+    if (!exact() && gram_dmma_supported(e->r_, L.m)) {  // tall factor: fp64 tensor-core tiles (gram_dmma.cu)
+      const int nb = gram_dmma_blocks(L.m, sm_count);
+      part.ensure((size_t)nb * e->r_ * e->r_ * 8);
+      gram_dmma(static_cast<const double*>(L.V), e->r_, L.m, sm_count, part.as<double>(), s, true);
+      ++e->launches_;
+      reduce_splits(part.as<double>(), e->r_ * e->r_, nb, Db.as<double>());
+      return;
+    }
     gemm_atb(static_cast<const double*>(L.V), static_cast<const double*>(L.V), L.m, e->r_, e->r_, Db.as<double>());
   }
 
@@ -1323,6 +1331,15 @@ void Engine::export_data(void* M_host, int host_dtype) {
   const size_t count = lv_[0].m * n_loc_, es = impl_->esz(), hs = host_dtype == 0 ? 4 : 8;
   if (hs != es) throw std::invalid_argument("export_data: host dtype must match the storage dtype");
   CK(cudaMemcpyAsync(M_host, lv_[0].M, count * es, cudaMemcpyDeviceToHost, impl_->s));
+  CK(cudaStreamSynchronize(impl_->s));
+}
+
+void Engine::gram_v(double* D_host) {
+  if (lv_.empty() || r_ == 0) throw std::invalid_argument("gram_v: no data or factors");
+  if (opt_.dtype == 0) impl_->gram_V<float>(0);
+  else impl_->gram_V<double>(0);
+  impl_->CD_valid = false;
+  CK(cudaMemcpyAsync(D_host, impl_->Db.p, r_ * r_ * 8, cudaMemcpyDeviceToHost, impl_->s));
   CK(cudaStreamSynchronize(impl_->s));
 }
 

@@ -110,6 +110,7 @@ class Engine {
   void set_factors(size_t l, const void* V, const void* W, int host_dtype, size_t r);  // V at level l, W
   void get_factors(size_t l, void* V, void* W, int host_dtype);
   void export_data(void* M_host, int host_dtype);  // level-0 M to a host buffer
+  void gram_v(double* D_host);                     // D = V^T V of level 0 through the active kernel
   void gram_w(double* B_host);                     // B = W W^T (this rank's shard, not allreduced) through the active kernel
   int export_level(size_t level, void* M_host);    // level data to a host buffer (NULL: only the dtype); returns the level's dtype
   // the two M-streaming products at level 0 with the current factors, through

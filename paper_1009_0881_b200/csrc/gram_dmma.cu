@@ -1,4 +1,5 @@
-// gram_dmma.cu -- the r x r Gram of a wide fp64 factor, B = W W^T
+// gram_dmma.cu -- the r x r Gram of a long fp64 factor, B = W W^T (and D = V^T V, the
+// same tiles over V's K-major layout)
 // (kernels::matmul_abt with X = Y = W, kernels.cpp:24-34; solvers.cpp:83,106,
 // 252), on the fp64 tensor-core path (mma.sync m8n8k4 f64, "DMMA").
 //
@@ -51,7 +52,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // (tiles RB .. 7), 9 tiles, all indices compile-time (the accumulators stay
 // in registers).  Every warp of the block runs the same tile loop and
 // barriers; only the tile set differs.
-template <int RA, typename Stage>
+template <int RA, bool TRANS, typename Stage>
 __device__ __forceinline__ void warp_tiles(const double* tile, int ntiles, Stage& stage, int lane, int r,
                                            double* __restrict__ out) {
   constexpr int RB = 7 - RA;
@@ -67,12 +68,14 @@ __device__ __forceinline__ void warp_tiles(const double* tile, int ntiles, Stage
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const double* src = tile + (size_t)(it & 1) * kR * kLd + (lane >> 2) * kLd + (lane & 3);
+    // tile layout: [factor row i][k] (W, row-major r x K) or [k][factor row i] (TRANS: V, K x r row-major)
+    const double* src = tile + (size_t)(it & 1) * kR * kLd +
+                        (TRANS ? (lane & 3) * kLd + (lane >> 2) : (lane >> 2) * kLd + (lane & 3));
 #pragma unroll 4
     for (int k4 = 0; k4 < kKC / 4; ++k4) {
-      double f[8];  // fragment of row block b: W[8 b + lane / 4][4 k4 + lane % 4]
+      double f[8];  // fragment of row block b: X[8 b + lane / 4][4 k4 + lane % 4]
 #pragma unroll
-      for (int b = 0; b < 8; ++b) f[b] = src[b * 8 * kLd + k4 * 4];
+      for (int b = 0; b < 8; ++b) f[b] = TRANS ? src[k4 * 4 * kLd + b * 8] : src[b * 8 * kLd + k4 * 4];
 #pragma unroll
       for (int j = RA; j < 8; ++j) dmma(acc[j - RA][0], acc[j - RA][1], f[RA], f[j]);
 #pragma unroll
@@ -103,7 +106,9 @@ __device__ __forceinline__ void warp_tiles(const double* tile, int ntiles, Stage
   }
 }
 
-// part[blockIdx.x][i][j] (r x r) = sum over this block's K range of W[i][p] W[j][p]
+// part[blockIdx.x][i][j] (r x r) = sum over this block's K range of X[i][p] X[j][p], X[i][p] = W[i K + p]
+// (TRANS = false: B = W W^T) or V[p r + i] (TRANS = true: D = V^T V, kernels::matmul_atb, kernels.cpp:36-46)
+template <bool TRANS>
 __global__ void __launch_bounds__(kThreads) k_gram_dmma(const double* __restrict__ W, int r, size_t K, size_t kchunk,
                                                         double* __restrict__ part) {
   extern __shared__ __align__(16) double tile[];  // [2][kR][kLd]
@@ -111,33 +116,49 @@ __global__ void __launch_bounds__(kThreads) k_gram_dmma(const double* __restrict
   const size_t kb = (size_t)blockIdx.x * kchunk;
   const size_t ke = kb + kchunk < K ? kb + kchunk : K;
   const int ntiles = kb < ke ? (int)((ke - kb + kKC - 1) / kKC) : 0;
-  const bool vec_ok = (K % 2 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
+  const bool vec_ok = ((TRANS ? (size_t)r : K) % 2 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
 
-  // stage tile `it` (columns kb + 64 it ..) into buffer it & 1: 16-byte
+  // stage tile `it` (K indices kb + 64 it ..) into buffer it & 1: 16-byte
   // asynchronous copies where the pair lies inside the range, zeros elsewhere
   auto stage = [&](int it) {
     double* dst = tile + (size_t)(it & 1) * kR * kLd;
     const size_t c0 = kb + (size_t)it * kKC;
-    for (int e = t; e < kR * (kKC / 2); e += kThreads) {
-      const int row = e / (kKC / 2), c2 = (e % (kKC / 2)) * 2;
-      const size_t col = c0 + c2;
-      double* d = dst + row * kLd + c2;
-      if (row < r && vec_ok && col + 1 < ke) {
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(d);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(W + (size_t)row * K + col) : "memory");
-      } else {
-        d[0] = (row < r && col < ke) ? W[(size_t)row * K + col] : 0.0;
-        d[1] = (row < r && col + 1 < ke) ? W[(size_t)row * K + col + 1] : 0.0;
+    if (!TRANS) {
+      for (int e = t; e < kR * (kKC / 2); e += kThreads) {
+        const int row = e / (kKC / 2), c2 = (e % (kKC / 2)) * 2;
+        const size_t col = c0 + c2;
+        double* d = dst + row * kLd + c2;
+        if (row < r && vec_ok && col + 1 < ke) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(d);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(W + (size_t)row * K + col) : "memory");
+        } else {
+          d[0] = (row < r && col < ke) ? W[(size_t)row * K + col] : 0.0;
+          d[1] = (row < r && col + 1 < ke) ? W[(size_t)row * K + col + 1] : 0.0;
+        }
+      }
+    } else {
+      // tile row = K index p, 64 factor entries (r of them real) of V's row p
+      for (int e = t; e < kKC * (kR / 2); e += kThreads) {
+        const int pr = e / (kR / 2), i2 = (e % (kR / 2)) * 2;
+        const size_t p = c0 + pr;
+        double* d = dst + pr * kLd + i2;
+        if (p < ke && vec_ok && i2 + 1 < r) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(d);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(W + p * (size_t)r + i2) : "memory");
+        } else {
+          d[0] = (p < ke && i2 < r) ? W[p * (size_t)r + i2] : 0.0;
+          d[1] = (p < ke && i2 + 1 < r) ? W[p * (size_t)r + i2 + 1] : 0.0;
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
   switch (warp) {
-    case 0: warp_tiles<0>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
-    case 1: warp_tiles<1>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
-    case 2: warp_tiles<2>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
-    default: warp_tiles<3>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
+    case 0: warp_tiles<0, TRANS>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
+    case 1: warp_tiles<1, TRANS>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
+    case 2: warp_tiles<2, TRANS>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
+    default: warp_tiles<3, TRANS>(tile, ntiles, stage, lane, r, part + (size_t)blockIdx.x * r * r); break;
   }
 }
 
@@ -151,7 +172,7 @@ int gram_dmma_blocks(size_t K, int sm_count) {
   return (int)((K + kchunk - 1) / kchunk);
 }
 
-void gram_dmma(const double* W, size_t r, size_t K, int sm_count, double* part, cudaStream_t s) {
+void gram_dmma(const double* W, size_t r, size_t K, int sm_count, double* part, cudaStream_t s, bool trans) {
   if (!gram_dmma_supported(r, K)) throw std::invalid_argument("gram_dmma: unsupported shape");
   const size_t target = (size_t)sm_count * 3;
   const size_t kchunk = ((K + target - 1) / target + kKC - 1) / kKC * kKC;
@@ -159,11 +180,14 @@ void gram_dmma(const double* W, size_t r, size_t K, int sm_count, double* part, 
   const size_t smem = 2 * (size_t)kR * kLd * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_gram_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_gram_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gram_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (gram_dmma)");
     attr = true;
   }
-  k_gram_dmma<<<blocks, kThreads, smem, s>>>(W, (int)r, K, kchunk, part);
+  if (trans) k_gram_dmma<true><<<blocks, kThreads, smem, s>>>(W, (int)r, K, kchunk, part);
+  else k_gram_dmma<false><<<blocks, kThreads, smem, s>>>(W, (int)r, K, kchunk, part);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " (gram_dmma)");
 }

@@ -9,6 +9,7 @@ namespace mlb {
 bool gram_dmma_supported(size_t r, size_t K);
 // number of split-K partials gram_dmma writes (r x r fp64 each)
 int gram_dmma_blocks(size_t K, int sm_count);
-// part[b] = the b-th K range's W W^T, b < gram_dmma_blocks(K, sm_count); W is r x K row-major
-void gram_dmma(const double* W, size_t r, size_t K, int sm_count, double* part, cudaStream_t s);
+// part[b] = the b-th K range's Gram, b < gram_dmma_blocks(K, sm_count).  trans = false: W W^T of W (r x K
+// row-major); trans = true: V^T V of V (K x r row-major)
+void gram_dmma(const double* W, size_t r, size_t K, int sm_count, double* part, cudaStream_t s, bool trans = false);
 }  // namespace mlb

@@ -249,3 +249,21 @@ def test_dmma_sweeps_against_oracle(P, gpu, restated, kind, r, m, n):
         s.steps(kind, 1)
         V, W = s.get_factors()
     assert relnorm(V, Vo) < 1e-11 and relnorm(W, Wo) < 1e-11, (relnorm(V, Vo), relnorm(W, Wo))
+
+
+@pytest.mark.parametrize("r,m", [(64, 16384), (49, 4100), (20, 2048), (7, 33001), (64, 2047)])
+def test_gram_v_dmma(P, gpu, r, m):
+    """D = V^T V of a tall factor on the fp64 tensor-core path (gram_dmma.cu over V's K-major layout; an odd
+    rank takes the scalar staging path, m < 2048 the SIMT tiles) against fp64 numpy; exactly symmetric."""
+    rng = np.random.default_rng(r * 1000 + m)
+    n = 128
+    M = rng.random((m, n)).astype(np.float32)
+    V = rng.random((m, r)) * (rng.random((m, r)) > 0.3)
+    W = rng.random((r, n))
+    with P.Session(dtype=P.F32) as s:
+        s.set_data(M, P.ImageGrid(m, 1))
+        s.set_factors(V, W)
+        D = s.gram_v()
+    ref = V.T @ V
+    assert np.array_equal(D, D.T)
+    assert np.max(np.abs(D - ref)) <= 1e-13 * np.max(np.abs(ref)) * np.sqrt(m), np.max(np.abs(D - ref))
