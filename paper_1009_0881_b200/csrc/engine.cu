@@ -676,7 +676,15 @@ struct Engine::Impl {
     // staged once per block, so one wide block per SM beats several narrow
     // ones; 8 warps per block left large-rank problems at 8 warps per SM and
     // latency-bound), but no more than spreads the problems over every SM
-    const size_t nw_max = std::max<size_t>(1, std::min<size_t>(32, (kSmemMax - gbytes) / wb));
+    // ... and no more than the register file holds: the runtime's own bound (registers are allocated
+    // per group of warps, so 65536 / (registers x 32) overestimates it)
+    static const size_t nw_regs = [] {
+      cudaFuncAttributes fa{}, fb{};
+      CK(cudaFuncGetAttributes(&fa, k_nnls_batch<double, true>));
+      CK(cudaFuncGetAttributes(&fb, k_nnls_batch<double, false>));
+      return (size_t)std::max(1, std::min(fa.maxThreadsPerBlock, fb.maxThreadsPerBlock) / 32);
+    }();
+    const size_t nw_max = std::max<size_t>(1, std::min<size_t>(std::min<size_t>(32, nw_regs), (kSmemMax - gbytes) / wb));
     const int nw = (int)std::min(nw_max, std::max<size_t>(1, ceil_div(nprob, (size_t)sm_count)));
     const size_t smem = gbytes + nw * wb;
     const size_t per_sm = std::max<size_t>(1, std::min<size_t>(kSmemMax / smem, 64 / nw));

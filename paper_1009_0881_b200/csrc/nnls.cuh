@@ -52,23 +52,37 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
   auto sub = [](double acc, double a, double b) { return EXACT ? msub(acc, a, b) : fma(-a, b, acc); };
   for (int k = 0; k < p; ++k) {
     const double* Lk = L + (unsigned)(k * (k + 1) / 2);
-    double d = Lk[k];
-    int q = 0;
-    for (; q + 4 <= k; q += 4) {
-      const double a0 = Lk[q], a1 = Lk[q + 1], a2 = Lk[q + 2], a3 = Lk[q + 3];
-      d = sub(d, a0, a0);
-      d = sub(d, a1, a1);
-      d = sub(d, a2, a2);
-      d = sub(d, a3, a3);
+    // Column k in one pass: lane j takes row i = k + j, so lane 0's "row" is
+    // the pivot itself -- d = G_kk - sum_q L_kq^2 is the same chain of
+    // subtractions as a row's s = G_ik - sum_q L_iq L_kq with i = k.  The
+    // pivot dot used to run first, on every lane, before the rows: 2 k
+    // dependent operations per column instead of k (same per-element order:
+    // results unchanged bit for bit).
+    const int i0 = k + lane;
+    double s0 = 0.0;
+    double* Li0 = L + (unsigned)(i0 * (i0 + 1) / 2);
+    if (i0 < p) {
+      s0 = Li0[k];
+      int qq = 0;
+      for (; qq + 4 <= k; qq += 4) {
+        s0 = sub(s0, Li0[qq], Lk[qq]);
+        s0 = sub(s0, Li0[qq + 1], Lk[qq + 1]);
+        s0 = sub(s0, Li0[qq + 2], Lk[qq + 2]);
+        s0 = sub(s0, Li0[qq + 3], Lk[qq + 3]);
+      }
+      for (; qq < k; ++qq) s0 = sub(s0, Li0[qq], Lk[qq]);
     }
-    for (; q < k; ++q) d = sub(d, Lk[q], Lk[q]);
+    const double d = __shfl_sync(0xffffffffu, s0, 0);
     if (d <= 0.0 || !isfinite(d)) {
       __syncwarp();
       return false;
     }
     const double lkk = sqrt(d);
     const double ilkk = EXACT ? 0.0 : 1.0 / lkk;
-    for (int i = k + 1 + lane; i < p; i += 32) {
+    __syncwarp();  // every lane has read row k before its diagonal is overwritten
+    if (lane == 0) Li0[k] = EXACT ? lkk : ilkk;
+    else if (i0 < p) Li0[k] = EXACT ? s0 / lkk : s0 * ilkk;
+    for (int i = i0 + 32; i < p; i += 32) {  // rows beyond the first 32 (p - k > 32: the first columns only)
       double* Li = L + (unsigned)(i * (i + 1) / 2);
       double s = Li[k];
       int qq = 0;
@@ -81,8 +95,6 @@ __device__ inline bool warp_cholesky(double* L, int p, int lane) {
       for (; qq < k; ++qq) s = sub(s, Li[qq], Lk[qq]);
       Li[k] = EXACT ? s / lkk : s * ilkk;
     }
-    __syncwarp();
-    if (lane == 0) L[(unsigned)(k * (k + 1) / 2) + k] = EXACT ? lkk : ilkk;
     __syncwarp();
   }
   return true;
